@@ -1,0 +1,522 @@
+"""Offline inputs of the hot path: Q1 meshes, the precomputed graph matrices
+and the BASELINE.json problem setups (C1-C5), vectorized.
+
+The time step consumes only `PrecomputedMatrices` (m_ij, c_ij, m_i, 1/m_i on
+a CSR stencil pattern) plus a `BoundaryConditions`, exactly the input contract
+of the reference (`assembly.py:22-50`, `stepper.py:40-52`).  The reference
+builds those with per-cell Python loops (`mesh.py:65-362`, `assembly.py:76-137`)
+that do not scale to the 10^6-10^7-node configs, and its `assemble` rejects
+uniform 3D hex meshes (beta pruning).  This module is the
+vectorized replacement:
+
+* `assemble_q1`: 2-point tensor Gauss assembly of m_ij and c_ij = ∫φ_i∇φ_j
+  (same quadrature and the same exact symmetrization of m as
+  `assembly.py:53-137`); beta is returned as zeros on m's pattern because the
+  time step never reads it (`indicator.py:49-51`).
+* mesh generators for the five BASELINE.json configs and the small reference
+  problems used by the parity tests.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable, Optional
+
+import numpy as np
+import scipy.sparse as sp
+
+from .physics import AIR, GasConstants
+
+__all__ = [
+    "PrecomputedMatrices",
+    "BoundaryConditions",
+    "Mesh",
+    "ProblemSetup",
+    "assemble_q1",
+    "rectangle_mesh",
+    "box_mesh",
+    "disc_channel_mesh",
+    "boundary_faces",
+    "isentropic_vortex",
+    "mach3_disc",
+    "sod_box",
+    "periodic_fourier_box",
+    "random_state",
+    "make_config",
+]
+
+
+@dataclass
+class PrecomputedMatrices:
+    """Stencil-graph matrices on a canonical CSR pattern (reference `assembly.py:22-50`)."""
+
+    n: int
+    dim: int
+    indptr: np.ndarray
+    indices: np.ndarray
+    m: np.ndarray
+    c: np.ndarray
+    beta: np.ndarray
+    m_lumped: np.ndarray
+    inv_m: np.ndarray
+
+    @property
+    def nnz(self) -> int:
+        return len(self.indices)
+
+    @property
+    def card(self) -> np.ndarray:
+        return np.diff(self.indptr)
+
+    def connectivity(self) -> sp.csr_matrix:
+        return sp.csr_matrix(
+            (np.ones(self.nnz, dtype=np.int8), self.indices, self.indptr), shape=(self.n, self.n)
+        )
+
+
+@dataclass
+class BoundaryConditions:
+    """Strong boundary data (reference `stepper.py:40-52`); ids in original numbering."""
+
+    inflow_nodes: Optional[np.ndarray] = None
+    farfield: Optional[np.ndarray] = None
+    slip_nodes: Optional[np.ndarray] = None
+    slip_normals: Optional[np.ndarray] = None
+
+
+@dataclass
+class Mesh:
+    points: np.ndarray          # (n_full, dim)
+    cells: np.ndarray           # (M, 2^dim), reference corner order (mesh.py:217-231)
+    dim: int
+    reduced_index: Optional[np.ndarray] = None
+
+    def __post_init__(self):
+        if self.reduced_index is None:
+            self.reduced_index = np.arange(len(self.points), dtype=np.int64)
+
+    @property
+    def n_nodes(self) -> int:
+        return int(self.reduced_index.max()) + 1
+
+
+@dataclass
+class ProblemSetup:
+    name: str
+    matrices: PrecomputedMatrices
+    U0: np.ndarray
+    boundary: Optional[BoundaryConditions]
+    c_cfl: float
+    steps: int
+    mesh: Optional[Mesh] = None
+    exact: Optional[Callable] = None
+
+
+_CORNERS = {
+    2: np.array([(0, 0), (1, 0), (1, 1), (0, 1)], dtype=np.float64),
+    3: np.array(
+        [(0, 0, 0), (1, 0, 0), (1, 1, 0), (0, 1, 0), (0, 0, 1), (1, 0, 1), (1, 1, 1), (0, 1, 1)],
+        dtype=np.float64,
+    ),
+}
+
+
+def _shape(dim: int, xi: np.ndarray):
+    corners = _CORNERS[dim]
+    facs = np.where(corners > 0.5, xi[None, :], 1.0 - xi[None, :])  # (nv, dim)
+    N = facs.prod(axis=1)
+    dN = np.empty((len(corners), dim))
+    for k in range(dim):
+        other = np.delete(facs, k, axis=1).prod(axis=1)
+        dN[:, k] = np.where(corners[:, k] > 0.5, 1.0, -1.0) * other
+    return N, dN
+
+
+def _inv_det(J: np.ndarray):
+    if J.shape[-1] == 2:
+        det = J[:, 0, 0] * J[:, 1, 1] - J[:, 0, 1] * J[:, 1, 0]
+        inv = np.empty_like(J)
+        inv[:, 0, 0] = J[:, 1, 1]
+        inv[:, 0, 1] = -J[:, 0, 1]
+        inv[:, 1, 0] = -J[:, 1, 0]
+        inv[:, 1, 1] = J[:, 0, 0]
+        return inv / det[:, None, None], det
+    det = np.linalg.det(J)
+    return np.linalg.inv(J), det
+
+
+def assemble_q1(mesh: Mesh, chunk: int = 1 << 18) -> PrecomputedMatrices:
+    """Assemble m_ij, c_ij and the lumped mass on the Q1 stencil graph."""
+    d = mesh.dim
+    cells = mesh.cells
+    red = np.asarray(mesh.reduced_index, dtype=np.int64)
+    n = mesh.n_nodes
+    nv = cells.shape[1]
+    g = np.array([0.5 - 0.5 / np.sqrt(3.0), 0.5 + 0.5 / np.sqrt(3.0)])
+    qpts = np.stack(np.meshgrid(*([g] * d), indexing="ij"), axis=-1).reshape(-1, d)
+    w = 0.5**d
+    shapes = [_shape(d, xi) for xi in qpts]
+
+    rows_all, cols_all, mv_all, cv_all = [], [], [], []
+    for lo in range(0, len(cells), chunk):
+        cc = cells[lo : lo + chunk]
+        X = mesh.points[cc]  # (M, nv, d)
+        m_loc = np.zeros((len(cc), nv, nv))
+        c_loc = np.zeros((len(cc), nv, nv, d))
+        for N, dN in shapes:
+            J = np.einsum("mak,al->mkl", X, dN)
+            Jinv, det = _inv_det(J)
+            if np.any(det <= 0.0):
+                raise ValueError("degenerate cell: non-positive Jacobian determinant")
+            grad = np.einsum("al,mlk->mak", dN, Jinv)
+            scale = w * det
+            m_loc += scale[:, None, None] * (N[:, None] * N[None, :])[None]
+            c_loc += scale[:, None, None, None] * N[None, :, None, None] * grad[:, None, :, :]
+        rc = red[cc]
+        rows_all.append(np.repeat(rc, nv, axis=1).ravel())
+        cols_all.append(np.tile(rc, (1, nv)).ravel())
+        mv_all.append(m_loc.ravel())
+        cv_all.append(c_loc.reshape(-1, d))
+    rows = np.concatenate(rows_all)
+    cols = np.concatenate(cols_all)
+    mv = np.concatenate(mv_all)
+    cv = np.concatenate(cv_all)
+    del rows_all, cols_all, mv_all, cv_all
+
+    # canonical pattern: sort by (row, col), sum duplicates in a fixed order
+    key = rows * n + cols
+    order = np.argsort(key, kind="stable")
+    key = key[order]
+    first = np.ones(len(key), dtype=bool)
+    first[1:] = key[1:] != key[:-1]
+    seg = np.flatnonzero(first)
+    m_data = np.add.reduceat(mv[order], seg)
+    c_data = np.add.reduceat(cv[order], seg, axis=0)
+    ukey = key[seg]
+    r_u = ukey // n
+    indices = (ukey % n).astype(np.int64)
+    indptr = np.zeros(n + 1, dtype=np.int64)
+    np.add.at(indptr, r_u + 1, 1)
+    indptr = np.cumsum(indptr)
+    # exact symmetry of m (as assembly.py:113): 0.5 * (m + m^T) on the shared pattern
+    mat = sp.csr_matrix((m_data, indices, indptr), shape=(n, n))
+    mt = mat.T.tocsr()
+    mt.sort_indices()
+    if not (np.array_equal(mt.indptr, indptr) and np.array_equal(mt.indices, indices)):
+        raise AssertionError("stencil pattern is not structurally symmetric")
+    m_sym = 0.5 * (m_data + mt.data)
+    m_lumped = np.add.reduceat(m_sym, indptr[:-1])
+    if np.any(m_lumped <= 0.0):
+        raise ValueError("non-positive lumped mass entry")
+    return PrecomputedMatrices(
+        n=n, dim=d, indptr=indptr, indices=indices, m=m_sym, c=c_data,
+        beta=np.zeros_like(m_sym), m_lumped=m_lumped, inv_m=1.0 / m_lumped,
+    )
+
+
+# --------------------------------------------------------------------------- meshes
+
+def rectangle_mesh(nx, ny, x_range=(0.0, 1.0), y_range=(0.0, 1.0), periodic=(False, False)) -> Mesh:
+    xs = np.linspace(*x_range, nx + 1)
+    ys = np.linspace(*y_range, ny + 1)
+    X, Y = np.meshgrid(xs, ys, indexing="ij")
+    pts = np.column_stack([X.ravel(), Y.ravel()])
+    i, j = np.meshgrid(np.arange(nx), np.arange(ny), indexing="ij")
+    i, j = i.ravel(), j.ravel()
+    nid = lambda a, b: a * (ny + 1) + b  # noqa: E731
+    cells = np.stack([nid(i, j), nid(i + 1, j), nid(i + 1, j + 1), nid(i, j + 1)], axis=1)
+    ri = np.arange(nx + 1)
+    rj = np.arange(ny + 1)
+    if periodic[0]:
+        ri[nx] = 0
+    if periodic[1]:
+        rj[ny] = 0
+    rep = (ri[:, None] * (ny + 1) + rj[None, :]).ravel()
+    _, reduced = np.unique(rep, return_inverse=True)
+    return Mesh(points=pts, cells=cells.astype(np.int64), dim=2, reduced_index=reduced.astype(np.int64))
+
+
+def box_mesh(nx, ny, nz, x_range=(0.0, 1.0), y_range=(0.0, 1.0), z_range=(0.0, 1.0),
+             periodic=(False, False, False), jitter=0.0, seed=0) -> Mesh:
+    """Tensor hex mesh with nx*ny*nz cells; interior nodes optionally jittered
+    i.i.d. U(-jitter*h, jitter*h) per axis (BASELINE C3)."""
+    xs = np.linspace(*x_range, nx + 1)
+    ys = np.linspace(*y_range, ny + 1)
+    zs = np.linspace(*z_range, nz + 1)
+    X, Y, Z = np.meshgrid(xs, ys, zs, indexing="ij")
+    pts = np.column_stack([X.ravel(), Y.ravel(), Z.ravel()])
+    if jitter > 0.0:
+        rng = np.random.default_rng(seed)
+        h = np.array([(x_range[1] - x_range[0]) / nx, (y_range[1] - y_range[0]) / ny,
+                      (z_range[1] - z_range[0]) / nz])
+        I, J, K = np.meshgrid(np.arange(nx + 1), np.arange(ny + 1), np.arange(nz + 1), indexing="ij")
+        interior = ((I > 0) & (I < nx) & (J > 0) & (J < ny) & (K > 0) & (K < nz)).ravel()
+        pts[interior] += rng.uniform(-jitter, jitter, (int(interior.sum()), 3)) * h
+    i, j, k = np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz), indexing="ij")
+    i, j, k = i.ravel(), j.ravel(), k.ravel()
+    nid = lambda a, b, c: (a * (ny + 1) + b) * (nz + 1) + c  # noqa: E731
+    cells = np.stack([
+        nid(i, j, k), nid(i + 1, j, k), nid(i + 1, j + 1, k), nid(i, j + 1, k),
+        nid(i, j, k + 1), nid(i + 1, j, k + 1), nid(i + 1, j + 1, k + 1), nid(i, j + 1, k + 1),
+    ], axis=1)
+    ri, rj, rk = np.arange(nx + 1), np.arange(ny + 1), np.arange(nz + 1)
+    if periodic[0]:
+        ri[nx] = 0
+    if periodic[1]:
+        rj[ny] = 0
+    if periodic[2]:
+        rk[nz] = 0
+    rep = ((ri[:, None, None] * (ny + 1) + rj[None, :, None]) * (nz + 1) + rk[None, None, :]).ravel()
+    if any(periodic):
+        _, reduced = np.unique(rep, return_inverse=True)
+        reduced = reduced.astype(np.int64)
+    else:
+        reduced = None
+    return Mesh(points=pts, cells=cells.astype(np.int64), dim=3, reduced_index=reduced)
+
+
+def disc_channel_mesh(ny: int, center=(0.6, 0.5), radius=0.1, half_box=0.2,
+                      x_len=4.0, y_len=1.0, grading=1.04) -> Mesh:
+    """Channel [0,x_len]x[0,y_len] minus a disc: a uniform Cartesian far field of
+    spacing h = y_len/ny whose square block [c-a, c+a]^2 is replaced by a graded
+    quad O-grid from the square perimeter to the circle (BASELINE C2 geometry)."""
+    h = y_len / ny
+    nx = int(round(x_len / h))
+    cx, cy = center
+    na = int(round(half_box / h))
+    i0, i1 = int(round((cx - half_box) / h)), int(round((cx + half_box) / h))
+    j0, j1 = int(round((cy - half_box) / h)), int(round((cy + half_box) / h))
+    if i1 - i0 != 2 * na or j1 - j0 != 2 * na:
+        raise ValueError("disc box must align with the grid; choose ny accordingly")
+    xs = np.linspace(0.0, x_len, nx + 1)
+    ys = np.linspace(0.0, y_len, ny + 1)
+    I, J = np.meshgrid(np.arange(nx + 1), np.arange(ny + 1), indexing="ij")
+    inside = (I > i0) & (I < i1) & (J > j0) & (J < j1)
+    keep = ~inside.ravel()
+    gid = np.full((nx + 1) * (ny + 1), -1, dtype=np.int64)
+    gid[keep] = np.arange(int(keep.sum()))
+    pts = np.column_stack([xs[I.ravel()], ys[J.ravel()]])[keep]
+    ci, cj = np.meshgrid(np.arange(nx), np.arange(ny), indexing="ij")
+    ci, cj = ci.ravel(), cj.ravel()
+    cell_in = (ci >= i0) & (ci < i1) & (cj >= j0) & (cj < j1)
+    ci, cj = ci[~cell_in], cj[~cell_in]
+    nid = lambda a, b: gid[a * (ny + 1) + b]  # noqa: E731
+    cells = [np.stack([nid(ci, cj), nid(ci + 1, cj), nid(ci + 1, cj + 1), nid(ci, cj + 1)], axis=1)]
+
+    # square perimeter, counterclockwise from (i0, j0)
+    side = 2 * na
+    pi = np.concatenate([np.arange(i0, i1), np.full(side, i1), np.arange(i1, i0, -1), np.full(side, i0)])
+    pj = np.concatenate([np.full(side, j0), np.arange(j0, j1), np.full(side, j1), np.arange(j1, j0, -1)])
+    ring0 = nid(pi, pj)
+    S = np.column_stack([xs[pi], ys[pj]])
+    v = S - np.array(center)
+    rS = np.linalg.norm(v, axis=1)
+    C = np.array(center) + radius * v / rS[:, None]
+    # graded radial layers: tangential spacing at the disc -> h at the box
+    P = len(ring0)
+    dr_min = 2.0 * np.pi * radius / P
+    nlay = max(2, int(np.ceil((half_box - radius) / (0.5 * (dr_min + h)))))
+    q = (h / dr_min) ** (1.0 / nlay)
+    s = (q ** np.arange(0, nlay + 1) - 1.0) / (q**nlay - 1.0)  # s[0]=0 disc, s[nlay]=1 box
+    rings = [ring0]
+    base = len(pts)
+    new_pts = []
+    for k in range(nlay - 1, 0, -1):  # interior rings from the box inward (s decreasing)
+        new_pts.append(C + s[k] * (S - C))
+        rings.append(base + np.arange(P))
+        base += P
+    new_pts.append(C)
+    rings.append(base + np.arange(P))
+    pts = np.concatenate([pts] + new_pts)
+    for a, b in zip(rings[:-1], rings[1:]):
+        an = np.roll(a, -1)
+        bn = np.roll(b, -1)
+        cells.append(np.stack([a, an, bn, b], axis=1))
+    cells = np.concatenate(cells).astype(np.int64)
+    # orient all cells counterclockwise (positive Jacobian)
+    X = pts[cells]
+    area2 = ((X[:, 1, 0] - X[:, 0, 0]) * (X[:, 3, 1] - X[:, 0, 1])
+             - (X[:, 1, 1] - X[:, 0, 1]) * (X[:, 3, 0] - X[:, 0, 0]))
+    flip = area2 < 0
+    cells[flip] = cells[flip][:, [0, 3, 2, 1]]
+    return Mesh(points=pts, cells=cells, dim=2)
+
+
+_LOCAL_FACES = {
+    2: np.array([(0, 1), (1, 2), (2, 3), (3, 0)]),
+    3: np.array([(0, 3, 2, 1), (4, 5, 6, 7), (0, 1, 5, 4), (1, 2, 6, 5), (2, 3, 7, 6), (3, 0, 4, 7)]),
+}
+
+
+def boundary_faces(mesh: Mesh):
+    """Vectorized `mesh.boundary_faces` (reference mesh.py:318-362): faces that
+    belong to exactly one cell, their outward unit normals and measures."""
+    d = mesh.dim
+    lf = _LOCAL_FACES[d]
+    faces = mesh.cells[:, lf].reshape(-1, lf.shape[1])
+    owner = np.repeat(np.arange(len(mesh.cells)), len(lf))
+    red = mesh.reduced_index[faces]
+    key = np.sort(red, axis=1)
+    _, inv, counts = np.unique(key, axis=0, return_inverse=True, return_counts=True)
+    single = counts[inv.ravel()] == 1
+    faces = faces[single]
+    owner = owner[single]
+    P = mesh.points[faces]
+    if d == 2:
+        t = P[:, 1] - P[:, 0]
+        normal = np.column_stack([t[:, 1], -t[:, 0]])
+        measure = np.linalg.norm(t, axis=1)
+    else:
+        normal = 0.5 * np.cross(P[:, 2] - P[:, 0], P[:, 3] - P[:, 1])
+        measure = np.linalg.norm(normal, axis=1)
+    nn = np.linalg.norm(normal, axis=1)
+    normal = normal / np.where(nn > 0, nn, 1.0)[:, None]
+    outward = P.mean(axis=1) - mesh.points[mesh.cells[owner]].mean(axis=1)
+    flip = (normal * outward).sum(axis=1) < 0
+    normal[flip] *= -1.0
+    return faces, normal, measure
+
+
+def _conserved(rho, vel, p, gas: GasConstants):
+    U = np.empty((len(rho), vel.shape[1] + 2))
+    U[:, 0] = rho
+    U[:, 1:-1] = rho[:, None] * vel
+    U[:, -1] = p / gas.gm1 + 0.5 * rho * (vel * vel).sum(axis=1)
+    return U
+
+
+def _slip_inflow_bc(mesh: Mesh, inflow_mask_fn, outflow_mask_fn, farfield):
+    """Classify boundary nodes as in `problems.mach3_channel` (problems.py:49-80)."""
+    faces, normals, measures = boundary_faces(mesh)
+    red = mesh.reduced_index
+    n = mesh.n_nodes
+    fx = mesh.points[faces]  # (nf, k, d)
+    is_in = inflow_mask_fn(fx).all(axis=1) if inflow_mask_fn else np.zeros(len(faces), bool)
+    is_out = outflow_mask_fn(fx).all(axis=1) if outflow_mask_fn else np.zeros(len(faces), bool)
+    is_out &= ~is_in
+    slip_f = ~(is_in | is_out)
+    inflow = np.zeros(n, dtype=bool)
+    inflow[red[faces[is_in]].ravel()] = True
+    slip = np.zeros(n, dtype=bool)
+    slip[red[faces[slip_f]].ravel()] = True
+    acc = np.zeros((n, mesh.dim))
+    contrib = (measures[slip_f, None] * normals[slip_f])
+    for k in range(faces.shape[1]):
+        np.add.at(acc, red[faces[slip_f, k]], contrib)
+    slip &= ~inflow
+    slip_nodes = np.flatnonzero(slip)
+    nrm = acc[slip_nodes]
+    ln = np.linalg.norm(nrm, axis=1, keepdims=True)
+    nrm = nrm / np.where(ln > 0.0, ln, 1.0)
+    return BoundaryConditions(
+        inflow_nodes=np.flatnonzero(inflow) if inflow.any() else None,
+        farfield=np.asarray(farfield, dtype=np.float64) if farfield is not None else None,
+        slip_nodes=slip_nodes if len(slip_nodes) else None,
+        slip_normals=nrm if len(slip_nodes) else None,
+    )
+
+
+# --------------------------------------------------------------------------- problems
+
+def isentropic_vortex(n: int = 128, beta: float = 5.0, gas: GasConstants = AIR,
+                      steps: int = 100) -> ProblemSetup:
+    """BASELINE C1: [-5,5]^2, (n+1)^2 nodes, vortex on (rho, u, p) = (1, (1,1), 1);
+    Dirichlet far field = background state on every boundary node."""
+    mesh = rectangle_mesh(n, n, (-5.0, 5.0), (-5.0, 5.0))
+    mat = assemble_q1(mesh)
+    x, y = mesh.points[:, 0], mesh.points[:, 1]
+    r2 = x * x + y * y
+    g = gas.gamma
+    e = np.exp(0.5 * (1.0 - r2))
+    du = -beta / (2.0 * np.pi) * e * y
+    dv = beta / (2.0 * np.pi) * e * x
+    T = 1.0 - (g - 1.0) * beta**2 / (8.0 * g * np.pi**2) * np.exp(1.0 - r2)
+    rho = T ** (1.0 / (g - 1.0))
+    p = rho**g
+    U0 = _conserved(rho, np.column_stack([1.0 + du, 1.0 + dv]), p, gas)
+    ff = _conserved(np.array([1.0]), np.array([[1.0, 1.0]]), np.array([1.0]), gas)[0]
+    on_bnd = (np.abs(np.abs(x) - 5.0) < 1e-12) | (np.abs(np.abs(y) - 5.0) < 1e-12)
+    bc = BoundaryConditions(inflow_nodes=np.flatnonzero(on_bnd), farfield=ff)
+    return ProblemSetup("c1-vortex", mat, U0, bc, c_cfl=0.5, steps=steps, mesh=mesh)
+
+
+def mach3_disc(ny: int = 550, seed: int = 2007, gas: GasConstants = AIR,
+               steps: int = 200, shuffle: bool = True) -> ProblemSetup:
+    """BASELINE C2: Mach 3 past a disc r=0.1 at (0.6,0.5) in [0,4]x[0,1]; ny=550
+    gives ~1.24M nodes.  Node ids are shuffled with a seeded permutation (the
+    solver applies RCM itself).  Inflow x=0, do-nothing x=4, slip elsewhere."""
+    mesh = disc_channel_mesh(ny)
+    if shuffle:
+        perm = np.random.default_rng(seed).permutation(len(mesh.points))  # old -> new
+        pts = np.empty_like(mesh.points)
+        pts[perm] = mesh.points
+        mesh = Mesh(points=pts, cells=perm[mesh.cells], dim=2)
+    mat = assemble_q1(mesh)
+    ff = _conserved(np.array([1.4]), np.array([[3.0, 0.0]]), np.array([1.0]), gas)[0]
+    bc = _slip_inflow_bc(mesh, lambda X: X[..., 0] < 1e-9, lambda X: X[..., 0] > 4.0 - 1e-9, ff)
+    U0 = np.tile(ff, (mat.n, 1))
+    return ProblemSetup("c2-mach3-disc", mat, U0, bc, c_cfl=0.9, steps=steps, mesh=mesh)
+
+
+def sod_box(nx: int = 511, ny: int = 127, nz: int = 127, jitter: float = 0.2, seed: int = 2007,
+            gas: GasConstants = AIR, steps: int = 100) -> ProblemSetup:
+    """BASELINE C3: [0,1]x[0,.25]^2 hex box, (nx+1)(ny+1)(nz+1) nodes, interior
+    jitter ±0.2h, Sod states split at x=0.5, slip walls."""
+    mesh = box_mesh(nx, ny, nz, (0.0, 1.0), (0.0, 0.25), (0.0, 0.25), jitter=jitter, seed=seed)
+    mat = assemble_q1(mesh)
+    left = mesh.points[:, 0] < 0.5
+    rho = np.where(left, 1.0, 0.125)
+    p = np.where(left, 1.0, 0.1)
+    U0 = _conserved(rho, np.zeros((len(rho), 3)), p, gas)
+    bc = _slip_inflow_bc(mesh, None, None, None)
+    return ProblemSetup("c3-sod-box", mat, U0, bc, c_cfl=0.9, steps=steps, mesh=mesh)
+
+
+def periodic_fourier_box(n: int = 320, seed: int = 2007, gas: GasConstants = AIR,
+                         steps: int = 50, modes: int = 8) -> ProblemSetup:
+    """BASELINE C5: periodic n^3 hex mesh; rho, p in [0.5,1.5], |u| <= 1 from a
+    sum of `modes` random low-frequency Fourier modes per field."""
+    mesh = box_mesh(n, n, n, periodic=(True, True, True))
+    mat = assemble_q1(mesh)
+    rep = np.zeros((mat.n, 3))
+    rep[mesh.reduced_index] = mesh.points
+    rng = np.random.default_rng(seed)
+    fields = []
+    for _ in range(5):
+        k = rng.integers(-2, 3, (modes, 3))
+        while np.any(np.all(k == 0, axis=1)):
+            bad = np.all(k == 0, axis=1)
+            k[bad] = rng.integers(-2, 3, (int(bad.sum()), 3))
+        a = rng.uniform(-1.0, 1.0, modes)
+        ph = rng.uniform(0.0, 2.0 * np.pi, modes)
+        gsum = np.sin(2.0 * np.pi * (rep @ k.T) + ph[None, :]) @ a
+        fields.append(gsum / np.abs(a).sum())
+    rho = 1.0 + 0.5 * fields[0]
+    p = 1.0 + 0.5 * fields[1]
+    vel = np.column_stack(fields[2:5]) / np.sqrt(3.0)
+    U0 = _conserved(rho, vel, p, gas)
+    return ProblemSetup("c5-periodic-box", mat, U0, None, c_cfl=0.9, steps=steps, mesh=mesh)
+
+
+def random_state(rng, n: int, dim: int = 2) -> np.ndarray:
+    """Seeded admissible random field (the reference's test fixture, test_stepper.py:15-21)."""
+    U = np.zeros((n, dim + 2))
+    U[:, 0] = 1.0 + 0.5 * rng.random(n)
+    U[:, 1:-1] = rng.normal(0.0, 0.3, (n, dim)) * U[:, 0:1]
+    p = 0.5 + rng.random(n)
+    U[:, -1] = p / 0.4 + 0.5 * (U[:, 1:-1] ** 2).sum(axis=1) / U[:, 0]
+    return U
+
+
+def make_config(name: str, scale: str = "full", gas: GasConstants = AIR) -> ProblemSetup:
+    """BASELINE.json configs by name; scale='small' gives oracle-sized instances."""
+    small = scale == "small"
+    if name == "c1":
+        return isentropic_vortex(32 if small else 128, gas=gas)
+    if name == "c2":
+        return mach3_disc(50 if small else 550, gas=gas)
+    if name == "c3":
+        return sod_box(*((31, 7, 7) if small else (511, 127, 127)), gas=gas)
+    if name == "c5":
+        return periodic_fourier_box(12 if small else 320, gas=gas)
+    raise ValueError(f"unknown config {name!r}")
