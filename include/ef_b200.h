@@ -1,0 +1,139 @@
+/*
+ * ef_b200.h — C-ABI of the B200 per-stage IDP Euler update (drop-in boundary).
+ *
+ * The reference has no FFI: its boundary is the Python class
+ *   eulerflow.stepper.Solver   /root/reference/pkg/src/eulerflow/stepper.py:87-649
+ * plus the pow plug-in point  physics.set_power_function  (physics.py:59-75).
+ * Each entry point below replaces one member of that surface; the ctypes
+ * binding that a maintainer of the reference would add is shown in
+ * INTEGRATION.md and implemented in paper_2007_00094_b200/stepper.py.
+ *
+ * Conventions: plain pointers and sizes, host memory only in the signatures,
+ * no torch types.  Every call returns an EF_* status; on failure
+ * ef_last_error() describes it (thread-local).  One handle = one GPU = one
+ * rank; a handle is driven by one host thread.  Inputs are copied at create;
+ * the library never retains host pointers.
+ */
+#ifndef EF_B200_H
+#define EF_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (the Python layer maps them to the reference's exceptions) */
+#define EF_OK 0
+#define EF_ERR_ARG 1            /* ValueError (stepper.py:104-107, :322-323)           */
+#define EF_ERR_INADMISSIBLE 2   /* AdmissibilityError (stepper.py:324-325, :612-621;   */
+                                /*   riemann.py:66-67; physics.py:128-130, :141-142)  */
+#define EF_ERR_TAU_UNBOUNDED 3  /* ValueError("constant field ...") stepper.py:546-547 */
+#define EF_ERR_CUDA 4           /* RuntimeError                                        */
+#define EF_ERR_NCCL 5           /* RuntimeError                                        */
+
+typedef struct ef_solver ef_solver;
+
+/* PrecomputedMatrices, assembly.py:22-50 (beta is not read by the time step,
+ * indicator.py:49-51, so it is not part of the ABI). CSR in original node ids,
+ * columns sorted ascending per row. */
+typedef struct {
+  int64_t n;
+  int32_t dim;               /* 2 or 3 */
+  const int64_t* indptr;     /* (n + 1) */
+  const int64_t* indices;    /* (nnz)   */
+  const double* m;           /* (nnz)      consistent mass m_ij  */
+  const double* c;           /* (nnz, dim) c_ij                 */
+  const double* m_lumped;    /* (n)  */
+  const double* inv_m;       /* (n)  */
+} ef_matrices;
+
+/* Solver(...) keyword arguments (stepper.py:90-103) + GasConstants (physics.py:33-52) */
+typedef struct {
+  double gamma, gm1, gp1_inv, gm1_over_2g, two_g_over_gm1; /* as computed by GasConstants */
+  double c_cfl;              /* (0, 1]                       */
+  int32_t limiter_passes;    /* >= 0                         */
+  int32_t newton_steps;      /* >= 0                         */
+} ef_params;
+
+/* BoundaryConditions, stepper.py:40-52 (original node ids) */
+typedef struct {
+  int64_t n_inflow;
+  const int64_t* inflow;     /* (n_inflow) */
+  const double* farfield;    /* (dim + 2)  */
+  int64_t n_slip;
+  const int64_t* slip;       /* (n_slip)   */
+  const double* slip_normals;/* (n_slip, dim) unit outward normals */
+} ef_boundary;
+
+/* Partition (exchange.partition, exchange.py:393-445) and device binding. */
+typedef struct {
+  int32_t rank, nranks;      /* contiguous ranges of the global CM order      */
+  int32_t device;            /* CUDA device ordinal                           */
+  const int64_t* cm_perm;    /* (n) original id -> global Cuthill-McKee id    */
+  const int64_t* ranges;     /* (nranks + 1) CM-id range bounds, or NULL (even split as exchange.py:405-411) */
+  const void* nccl_id;       /* 128-byte ncclUniqueId shared by all ranks (nranks > 1), else NULL */
+  void* stream;              /* cudaStream_t to launch on, or NULL for a library-owned stream */
+} ef_dist;
+
+/* Solver.__init__ (stepper.py:90-139) */
+int ef_create(const ef_matrices* mat, const ef_params* prm, const ef_boundary* bc,
+              const ef_dist* dist, ef_solver** out);
+int ef_destroy(ef_solver* h);
+
+/* Solver.set_state / get_state (stepper.py:319-336): U is (n, dim+2) float64,
+ * original node order.  set_state rejects inadmissible input (state unchanged);
+ * get_state fills the rows this rank owns. */
+int ef_set_state(ef_solver* h, const double* U);
+int ef_get_state(ef_solver* h, double* U);
+
+/* Solver.euler_step / ssp_rk3_step (stepper.py:508-610, :624-636).  has_tau=0:
+ * CFL step capped by tau_max; has_tau=1: the given tau.  *tau_used = step used
+ * (Solver.tau_last).  On error the state is left at its value before the call. */
+int ef_euler_step(ef_solver* h, int32_t has_tau, double tau, double tau_max, double* tau_used);
+int ef_ssp_rk3_step(ef_solver* h, int32_t has_tau, double tau, double tau_max, double* tau_used);
+
+/* Same steps, asynchronous: no host synchronisation, tau stays on the device,
+ * errors are latched and reported by the next ef_sync().  For benchmarks and
+ * CUDA-graph capture. */
+int ef_ssp_rk3_step_async(ef_solver* h, int32_t has_tau, double tau, double tau_max);
+int ef_sync(ef_solver* h, double* tau_used);
+
+/* original id of the inadmissible node behind the last EF_ERR_INADMISSIBLE */
+int64_t ef_bad_node(const ef_solver* h);
+const char* ef_last_error(void);
+
+/* Solver.timers (stepper.py:37, 515-607): seconds per phase step0..step6,
+ * accumulated while timing is enabled (adds a sync per phase). */
+int ef_enable_timers(ef_solver* h, int32_t on);
+int ef_phase_times(ef_solver* h, double* seconds7);
+/* Solver.n_euler_steps, comm.sync_count, comm.sync_volume (doubles) */
+int ef_counters(ef_solver* h, int64_t* out3);
+
+/* Layout facts: out[0]=n_owned, [1]=n_local, [2]=pad width L, [3]=nnz owned,
+ * [4]=standard card (most frequent), [5]=dim */
+int ef_info(ef_solver* h, int64_t* out6);
+
+/* Per-phase parity hook (the reference exposes these as solver.ranks[r].*):
+ * which = 0 d (n_local*L), 1 alpha (n_local), 2 R (n_local*nvar), 3 bounds
+ * (n_local*3), 4 l of pass p (n_local*L; p = which_pass), 5 eor, 6 phi,
+ * 7 U (n_local*nvar), 8 U_next.  Rows in local order (owned rows = global CM
+ * ids rank_start.., then ghosts ascending), slots in stencil order. */
+int ef_debug_fetch(ef_solver* h, int32_t which, int32_t which_pass, double* out);
+/* local row -> global CM id, (n_local) */
+int ef_local_gids(ef_solver* h, int64_t* out);
+
+/* The shared deterministic pow (csrc/ef_pow.h): host build, to be installed
+ * into the reference through physics.set_power_function, and the same code
+ * evaluated on the device (test hook). */
+void ef_pow_host(const double* x, double y, double* out, int64_t n);
+int ef_pow_device(const double* x, double y, double* out, int64_t n);
+
+/* Device-resident state exchange for benchmarks: copies between the current
+ * state and a device buffer in (n_local, nvar) SoA local order. */
+int ef_state_device_ptr(ef_solver* h, void** dev_ptr, int64_t* stride);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EF_B200_H */

@@ -1,0 +1,555 @@
+// ef_kernels.cu — the sm_100a kernels of one forward-Euler stage.
+//
+// One thread owns one row (node); a warp owns one 32-row SELL slice, so every
+// per-slot load is a coalesced 256-byte line and neighbour gathers of the
+// structure-of-arrays state hit L1/L2 thanks to the Cuthill-McKee numbering.
+// Phase map (reference stepper.py):
+//   k_viscosity  = step1 _k_viscosity + IndicatorAccumulator      (:407-425)
+//   k_mirror     = step2 _k_mirror + _tau_local                   (:427-434, :66-70)
+//   k_low_order  = step3 _k_low_order (+ tau = min(c_cfl tau_min, tau_max), :548)
+//   k_correction = step4 _k_correction (P_ij built in registers)  (:456-474)
+//   k_limit_pass = step5 _k_limited_update, non-final pass        (:476-491)
+//   k_final      = step6 final pass + _k_boundary + _finish_step check
+//                  + SSP-RK3 combination + next stage's step0     (:493-504, :612-636, :399-405)
+// P_ij is never stored: every pass rebuilds it from R, U, d, alpha and m_ij in
+// the same operation order (including the (1 - min l) rescales of earlier
+// passes), which is bit-identical and saves 2*nvar doubles per slot per pass.
+#include "ef_kernels.cuh"
+
+namespace ef {
+
+constexpr int TPB = 128;
+
+static inline unsigned grid_for(int64_t n) { return (unsigned)((n + TPB - 1) / TPB); }
+
+template <int NV>
+__device__ __forceinline__ void load_node(const double* __restrict__ U, int64_t NP, int64_t i,
+                                          double* out) {
+#pragma unroll
+  for (int k = 0; k < NV; ++k) out[k] = U[k * NP + i];
+}
+
+// ---------------------------------------------------------------- state I/O
+template <int D>
+__global__ void k_gather_state(Layout m, const double* __restrict__ Uaos,
+                               const int64_t* __restrict__ orig, double* __restrict__ U, int* err) {
+  constexpr int NV = D + 2;
+  const int64_t i = blockIdx.x * (int64_t)TPB + threadIdx.x;
+  if (i >= m.n_local) return;
+  const int64_t o = orig[i];
+  double x[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    x[k] = Uaos[o * NV + k];
+    U[k * m.NP + i] = x[k];
+  }
+  if (!((x[0] > 0.0) && (internal_energy<D>(x) > 0.0))) atomicOr(err, 1);
+}
+
+template <int D>
+__global__ void k_scatter_state(Layout m, const double* __restrict__ U,
+                                const int64_t* __restrict__ orig, double* __restrict__ Uaos) {
+  constexpr int NV = D + 2;
+  const int64_t i = blockIdx.x * (int64_t)TPB + threadIdx.x;
+  if (i >= m.n_owned) return;
+  const int64_t o = orig[i];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) Uaos[o * NV + k] = U[k * m.NP + i];
+}
+
+// ---------------------------------------------------------------- step0
+template <int D>
+__device__ __forceinline__ void nodal_one(const double* Ui, const Gas& g, double& eor, double& phi) {
+  const double rho = Ui[0];
+  const double eps = internal_energy<D>(Ui);
+  eor = ef_pow(rho * eps, g.gp1_inv) / rho;     // stepper.py:403
+  phi = eps * ef_pow(rho, g.neg_gamma);          // stepper.py:404
+}
+
+template <int D>
+__global__ void k_nodal(Layout m, Gas g, const double* __restrict__ U, Work w, int64_t lo, int64_t hi) {
+  const int64_t i = lo + blockIdx.x * (int64_t)TPB + threadIdx.x;
+  if (i >= hi) return;
+  double Ui[D + 2];
+  load_node<D + 2>(U, m.NP, i, Ui);
+  double e, p;
+  nodal_one<D>(Ui, g, e, p);
+  w.eor[i] = e;
+  w.phi[i] = p;
+}
+
+// ---------------------------------------------------------------- step1
+template <int D>
+__global__ void __launch_bounds__(TPB) k_viscosity(Layout m, Gas g, const double* __restrict__ U,
+                                                   Work w, int reset_tau) {
+  constexpr int NV = D + 2;
+  const int64_t i = blockIdx.x * (int64_t)TPB + threadIdx.x;
+  if (reset_tau && i == 0) *w.tau_min_bits = 0x7ff0000000000000ULL;
+  if (i >= m.n_local) return;
+  const int64_t NP = m.NP;
+  const int L = m.L;
+  const int64_t NPL = NP * L;
+  double Ui[NV];
+  load_node<NV>(U, NP, i, Ui);
+  const int card = m.card[i], dg = m.diag[i];
+  const bool owned = i < m.n_owned;
+  bool bad = false;
+  double fi[NV][D];
+  flux<D>(Ui, g, fi);
+  const double eor_i = w.eor[i];
+  double ep[NV];
+  if (owned) {  // IndicatorAccumulator.reset, indicator.py:35-43
+    const double re = Ui[0] * internal_energy<D>(Ui);
+    if (re <= 0.0) bad = true;
+    const double scale = ef_pow(re, g.neg_g_gp1_inv) * g.gp1_inv;  // physics.py:143
+    ep[0] = scale * Ui[D + 1];
+#pragma unroll
+    for (int a = 0; a < D; ++a) ep[1 + a] = (-scale) * Ui[1 + a];
+    ep[D + 1] = scale * Ui[0];
+  }
+  double A = 0.0, B[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) B[k] = 0.0;
+  const int64_t base = sidx(i, 0, L);
+  for (int s = 0; s < card; ++s) {
+    if (s == dg) continue;  // j == i contributes exact zeros
+    const int64_t p = base + (int64_t)s * 32;
+    const int64_t j = m.col[p];
+    double Uj[NV];
+    load_node<NV>(U, NP, j, Uj);
+    double cc[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) cc[a] = m.c[a * NPL + p];
+    if (s > dg) {  // upper triangle by global id (stepper.py:211, 415)
+      double ct[D];
+#pragma unroll
+      for (int a = 0; a < D; ++a) ct[a] = m.cT[a * NPL + p];
+      w.d[p] = d_ij_low<D>(Ui, Uj, cc, ct, g, bad);
+    }
+    if (owned) {  // IndicatorAccumulator.accumulate, indicator.py:45-61
+      double mc = 0.0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) mc = mc + Uj[1 + a] * cc[a];
+      A = A + (w.eor[j] - eor_i) * mc;
+      double fj[NV][D];
+      flux<D>(Uj, g, fj);
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        double t = 0.0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) t = t + (fj[k][a] - fi[k][a]) * cc[a];
+        B[k] = B[k] + t;
+      }
+    }
+  }
+  if (owned) {  // IndicatorAccumulator.result, indicator.py:63-73
+    double eb = 0.0;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) eb = eb + ep[k] * B[k];
+    const double numer = fabs((A - eb) + (eor_i * B[0]));
+    double wb = 0.0;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const double wk = (k == 0) ? fabs(ep[0] - eor_i) : fabs(ep[k]);
+      wb = wb + wk * fabs(B[k]);
+    }
+    const double denom = fabs(A) + wb;
+    const double safe = denom > kDenomFloor ? denom : 1.0;
+    const double al = npclip(numer / safe, 0.0, 1.0);
+    w.alpha[i] = denom > kDenomFloor ? al : 0.0;
+  }
+  if (bad) atomicOr(w.err, ERR_PROJECT);
+}
+
+// ---------------------------------------------------------------- step2
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__global__ void __launch_bounds__(TPB) k_mirror(Layout m, Work w, int want_tau) {
+  const int64_t i = blockIdx.x * (int64_t)TPB + threadIdx.x;
+  double cand = __longlong_as_double(0x7ff0000000000000LL);
+  if (i < m.n_owned) {
+    const int L = m.L;
+    const int card = m.card[i], dg = m.diag[i];
+    const int64_t base = sidx(i, 0, L);
+    double* __restrict__ d = w.d;
+    auto v = [&](int s) -> double {
+      const int64_t p = base + (int64_t)s * 32;
+      if (s < dg) {  // lower: take d_ji from the transpose position
+        const double x = d[sidx(m.col[p], m.tslot[p], L)];
+        d[p] = x;
+        return x;
+      }
+      if (s == dg || s >= card) return 0.0;
+      return d[p];
+    };
+    double res;
+    if (L < 8) {  // numpy pairwise_sum, n < 8: sequential from +0
+      res = 0.0;
+      for (int s = 0; s < L; ++s) res = res + v(s);
+    } else {      // n >= 8: 8 accumulators, fixed tree, sequential tail
+      double r[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) r[q] = v(q);
+      const int Lm = L - (L % 8);
+      for (int b = 8; b < Lm; b += 8) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) r[q] = r[q] + v(b + q);
+      }
+      res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+      for (int s = Lm; s < L; ++s) res = res + v(s);
+    }
+    const double dii = -res;
+    d[base + (int64_t)dg * 32] = dii;
+    if (want_tau && dii < 0.0) cand = m.m_i[i] / (-2.0 * dii);
+  }
+  if (!want_tau) return;
+  __shared__ double red[TPB / 32];
+  cand = warp_min(cand);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cand;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = red[0];
+#pragma unroll
+    for (int q = 1; q < TPB / 32; ++q) b = fmin(b, red[q]);
+    // tau > 0: the IEEE bit pattern orders like the value
+    atomicMin(w.tau_min_bits, (unsigned long long)__double_as_longlong(b));
+  }
+}
+
+// ---------------------------------------------------------------- step3
+__device__ __forceinline__ double stage_tau(const Work& w, const StageParams& sp) {
+  double tau;
+  if (sp.tau_mode == TAU_GIVEN) {
+    tau = sp.tau_given;
+  } else if (sp.tau_mode == TAU_DEVICE) {
+    tau = *w.tau;
+  } else {  // stepper.py:538-548
+    const double tmin = __longlong_as_double((long long)*w.tau_min_bits);
+    const double a = sp.c_cfl * tmin;
+    tau = (sp.tau_max < a) ? sp.tau_max : a;
+  }
+  return tau;
+}
+
+template <int D>
+__global__ void __launch_bounds__(TPB) k_low_order(Layout m, Gas g, const double* __restrict__ U,
+                                                   Work w, StageParams sp) {
+  constexpr int NV = D + 2;
+  const double tau = stage_tau(w, sp);
+  const int64_t i = blockIdx.x * (int64_t)TPB + threadIdx.x;
+  if (i == 0 && sp.tau_mode != TAU_DEVICE) {
+    *w.tau = tau;
+    if (sp.tau_mode == TAU_CFL &&
+        !(__longlong_as_double((long long)*w.tau_min_bits) < __longlong_as_double(0x7ff0000000000000LL)))
+      atomicOr(w.err, ERR_TAU_UNBOUNDED);
+  }
+  if (i >= m.n_owned) return;
+  const int64_t NP = m.NP;
+  const int L = m.L;
+  const int64_t NPL = NP * L;
+  double Ui[NV];
+  load_node<NV>(U, NP, i, Ui);
+  double fi[NV][D];
+  flux<D>(Ui, g, fi);
+  const double ai = w.alpha[i];
+  double sumL[NV], sumR[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) sumL[k] = sumR[k] = 0.0;
+  // the diagonal (and every pad) yields the bar state U_i and phi_i exactly
+  double rmin = Ui[0], rmax = Ui[0], pmin = w.phi[i];
+  const int card = m.card[i], dg = m.diag[i];
+  const int64_t base = sidx(i, 0, L);
+  for (int s = 0; s < card; ++s) {
+    if (s == dg) continue;
+    const int64_t p = base + (int64_t)s * 32;
+    const int64_t j = m.col[p];
+    double Uj[NV];
+    load_node<NV>(U, NP, j, Uj);
+    double fj[NV][D];
+    flux<D>(Uj, g, fj);
+    double cc[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) cc[a] = m.c[a * NPL + p];
+    const double dv = w.d[p];
+    const double dH = dv * (0.5 * (ai + w.alpha[j]));
+    double ubar = 0.0;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const double dU = Uj[k] - Ui[k];
+      double fdc = 0.0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) fdc = fdc + (fj[k][a] - fi[k][a]) * cc[a];
+      sumL[k] = sumL[k] + ((dv * dU) - fdc);
+      sumR[k] = sumR[k] + ((dH * dU) - fdc);
+      if (k == 0) {
+        const double corr = dv != 0.0 ? fdc / (2.0 * dv) : 0.0;
+        ubar = (0.5 * (Ui[0] + Uj[0])) - corr;
+      }
+    }
+    rmin = npmin(rmin, ubar);
+    rmax = npmax(rmax, ubar);
+    pmin = npmin(pmin, w.phi[j]);
+  }
+  const double fac = tau * m.inv_m[i];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    w.Unext[k * NP + i] = Ui[k] + (fac * sumL[k]);
+    w.R[k * NP + i] = sumR[k];
+  }
+  w.bounds[i] = rmin;
+  w.bounds[NP + i] = rmax;
+  w.bounds[2 * NP + i] = pmin;
+}
+
+// ---------------------------------------------------------------- steps 4-6
+// P_ij of slot (i, s) after `applied` limiter passes (stepper.py:460-468, :485).
+template <int D>
+__device__ __forceinline__ void build_P(const Layout& m, const Work& w, const double* __restrict__ U,
+                                        const double* Ui, const double* Ri, double ai, double inv_mi,
+                                        double factor, int64_t p, int64_t j, int applied, double* P) {
+  constexpr int NV = D + 2;
+  const int64_t NP = m.NP;
+  const double dv = w.d[p];
+  const double dH = dv * (0.5 * (ai + w.alpha[j]));
+  const double mm = m.mij[p];
+  const double b = 0.0 - mm * m.inv_m[j];   // b_ij  = delta_ij - m_ij / m_j
+  const double bT = 0.0 - mm * inv_mi;      // b_ji  = delta_ij - m_ij / m_i
+  const double dd = dH - dv;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const double K = ((b * w.R[k * NP + j]) - (bT * Ri[k])) + (dd * (U[k * NP + j] - Ui[k]));
+    P[k] = factor * K;
+  }
+  if (applied > 0) {
+    const int64_t NPL = NP * m.L;
+    const int64_t pt = sidx(j, m.tslot[p], m.L);
+    for (int q = 0; q < applied; ++q) {
+      const double ml = npmin(w.l[q * NPL + p], w.l[q * NPL + pt]);
+      const double f = 1.0 - ml;
+#pragma unroll
+      for (int k = 0; k < NV; ++k) P[k] = P[k] * f;
+    }
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(TPB) k_correction(Layout m, Gas g, const double* __restrict__ U,
+                                                    Work w, StageParams sp) {
+  constexpr int NV = D + 2;
+  const int64_t i = blockIdx.x * (int64_t)TPB + threadIdx.x;
+  if (i >= m.n_owned) return;
+  const int64_t NP = m.NP;
+  const int L = m.L;
+  const double tau = *w.tau;
+  const int card = m.card[i], dg = m.diag[i];
+  const double inv_mi = m.inv_m[i];
+  const double factor = (tau * inv_mi) * (double)(card - 1);
+  double Ui[NV], Ri[NV], Un[NV];
+  load_node<NV>(U, NP, i, Ui);
+  load_node<NV>(w.R, NP, i, Ri);
+  load_node<NV>(w.Unext, NP, i, Un);
+  const double ai = w.alpha[i];
+  const double rmin = w.bounds[i], rmax = w.bounds[NP + i], pmin = w.bounds[2 * NP + i];
+  const int64_t base = sidx(i, 0, L);
+  for (int s = 0; s < card; ++s) {
+    if (s == dg) continue;
+    const int64_t p = base + (int64_t)s * 32;
+    const int64_t j = m.col[p];
+    double P[NV];
+    build_P<D>(m, w, U, Ui, Ri, ai, inv_mi, factor, p, j, 0, P);
+    w.l[p] = limiter<D>(Un, P, rmin, rmax, pmin, sp.newton, g);
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(TPB) k_limit_pass(Layout m, Gas g, const double* __restrict__ U,
+                                                    Work w, StageParams sp, int pass) {
+  constexpr int NV = D + 2;
+  const int64_t i = blockIdx.x * (int64_t)TPB + threadIdx.x;
+  if (i >= m.n_owned) return;
+  const int64_t NP = m.NP;
+  const int L = m.L;
+  const int64_t NPL = NP * L;
+  const double tau = *w.tau;
+  const int card = m.card[i], dg = m.diag[i];
+  const double inv_mi = m.inv_m[i];
+  const double factor = (tau * inv_mi) * (double)(card - 1);
+  double Ui[NV], Ri[NV], Un[NV];
+  load_node<NV>(U, NP, i, Ui);
+  load_node<NV>(w.R, NP, i, Ri);
+  load_node<NV>(w.Unext, NP, i, Un);
+  const double ai = w.alpha[i];
+  const int64_t base = sidx(i, 0, L);
+  double upd[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) upd[k] = 0.0;
+  for (int s = 0; s < card; ++s) {
+    if (s == dg) continue;
+    const int64_t p = base + (int64_t)s * 32;
+    const int64_t j = m.col[p];
+    double P[NV];
+    build_P<D>(m, w, U, Ui, Ri, ai, inv_mi, factor, p, j, pass, P);
+    const double ml = npmin(w.l[pass * NPL + p], w.l[pass * NPL + sidx(j, m.tslot[p], L)]);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) upd[k] = upd[k] + ml * P[k];
+  }
+  const double lam = m.lam[i];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    Un[k] = Un[k] + lam * upd[k];
+    w.Unext[k * NP + i] = Un[k];
+  }
+  const double rmin = w.bounds[i], rmax = w.bounds[NP + i], pmin = w.bounds[2 * NP + i];
+  for (int s = 0; s < card; ++s) {
+    if (s == dg) continue;
+    const int64_t p = base + (int64_t)s * 32;
+    const int64_t j = m.col[p];
+    double P[NV];
+    build_P<D>(m, w, U, Ui, Ri, ai, inv_mi, factor, p, j, pass + 1, P);
+    w.l[(pass + 1) * NPL + p] = limiter<D>(Un, P, rmin, rmax, pmin, sp.newton, g);
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(TPB) k_final(Layout m, Gas g, const double* __restrict__ U,
+                                               const double* __restrict__ U0, double* __restrict__ Uout,
+                                               Work w, StageParams sp) {
+  constexpr int NV = D + 2;
+  const int64_t i = blockIdx.x * (int64_t)TPB + threadIdx.x;
+  if (i >= m.n_owned) return;
+  const int64_t NP = m.NP;
+  const int L = m.L;
+  const int64_t NPL = NP * L;
+  double Un[NV];
+  load_node<NV>(w.Unext, NP, i, Un);
+  if (sp.passes > 0) {
+    const int pass = sp.passes - 1;
+    const double tau = *w.tau;
+    const int card = m.card[i], dg = m.diag[i];
+    const double inv_mi = m.inv_m[i];
+    const double factor = (tau * inv_mi) * (double)(card - 1);
+    double Ui[NV], Ri[NV];
+    load_node<NV>(U, NP, i, Ui);
+    load_node<NV>(w.R, NP, i, Ri);
+    const double ai = w.alpha[i];
+    const int64_t base = sidx(i, 0, L);
+    double upd[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) upd[k] = 0.0;
+    for (int s = 0; s < card; ++s) {
+      if (s == dg) continue;
+      const int64_t p = base + (int64_t)s * 32;
+      const int64_t j = m.col[p];
+      double P[NV];
+      build_P<D>(m, w, U, Ui, Ri, ai, inv_mi, factor, p, j, pass, P);
+      const double ml = npmin(w.l[pass * NPL + p], w.l[pass * NPL + sidx(j, m.tslot[p], L)]);
+#pragma unroll
+      for (int k = 0; k < NV; ++k) upd[k] = upd[k] + ml * P[k];
+    }
+    const double lam = m.lam[i];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) Un[k] = Un[k] + lam * upd[k];
+  }
+  // _k_boundary, stepper.py:493-504: slip projection, then inflow reset
+  const int kind = m.bc_kind[i];
+  if (kind & 1) {
+    double nr[D], mn = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      nr[a] = m.bc_n[a * NP + i];
+      mn = mn + Un[1 + a] * nr[a];
+    }
+#pragma unroll
+    for (int a = 0; a < D; ++a) Un[1 + a] = Un[1 + a] - mn * nr[a];
+  }
+  if (kind & 2) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) Un[k] = m.farfield[k];
+  }
+  // _finish_step admissibility, stepper.py:612-621
+  if (!((Un[0] > 0.0) && (internal_energy<D>(Un) > 0.0))) {
+    atomicOr(w.err, ERR_BAD_STATE);
+    atomicMin(w.bad_gid, (unsigned long long)m.gid[i]);
+  }
+  double Uo[NV];
+  if (sp.rk_a >= 0.0) {  // ssp_rk3_step incremental combination, stepper.py:632,635
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const double u0 = U0[k * NP + i];
+      Uo[k] = u0 + sp.rk_a * (Un[k] - u0);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) Uo[k] = Un[k];
+  }
+#pragma unroll
+  for (int k = 0; k < NV; ++k) Uout[k * NP + i] = Uo[k];
+  double e, ph;
+  nodal_one<D>(Uo, g, e, ph);  // next stage's step0
+  w.eor[i] = e;
+  w.phi[i] = ph;
+}
+
+__global__ void k_pow(const double* __restrict__ x, double y, double* __restrict__ out, int64_t n) {
+  const int64_t q = blockIdx.x * (int64_t)TPB + threadIdx.x;
+  if (q < n) out[q] = ef_pow(x[q], y);
+}
+
+// ---------------------------------------------------------------- launchers
+#define EF_DISPATCH(dim, KERNEL, GRID, ...)                                   \
+  do {                                                                        \
+    if ((dim) == 2) KERNEL<2><<<(GRID), TPB, 0, st>>>(__VA_ARGS__);          \
+    else KERNEL<3><<<(GRID), TPB, 0, st>>>(__VA_ARGS__);                     \
+  } while (0)
+
+void launch_gather_state(int dim, const Layout& m, const double* U_aos, const int64_t* orig,
+                         double* U, int* err, cudaStream_t st) {
+  if (m.n_local == 0) return;
+  EF_DISPATCH(dim, k_gather_state, grid_for(m.n_local), m, U_aos, orig, U, err);
+}
+void launch_scatter_state(int dim, const Layout& m, const double* U, const int64_t* orig,
+                          double* U_aos, cudaStream_t st) {
+  if (m.n_owned == 0) return;
+  EF_DISPATCH(dim, k_scatter_state, grid_for(m.n_owned), m, U, orig, U_aos);
+}
+void launch_nodal(int dim, const Layout& m, const Gas& g, const double* U, Work w, int64_t lo,
+                  int64_t hi, cudaStream_t st) {
+  if (hi <= lo) return;
+  EF_DISPATCH(dim, k_nodal, grid_for(hi - lo), m, g, U, w, lo, hi);
+}
+void launch_viscosity(int dim, const Layout& m, const Gas& g, const double* U, Work w,
+                      bool reset_tau, cudaStream_t st) {
+  EF_DISPATCH(dim, k_viscosity, grid_for(m.n_local > 0 ? m.n_local : 1), m, g, U, w, reset_tau ? 1 : 0);
+}
+void launch_mirror(const Layout& m, Work w, bool want_tau, cudaStream_t st) {
+  k_mirror<<<grid_for(m.n_owned > 0 ? m.n_owned : 1), TPB, 0, st>>>(m, w, want_tau ? 1 : 0);
+}
+void launch_low_order(int dim, const Layout& m, const Gas& g, const double* U, Work w,
+                      StageParams sp, cudaStream_t st) {
+  EF_DISPATCH(dim, k_low_order, grid_for(m.n_owned > 0 ? m.n_owned : 1), m, g, U, w, sp);
+}
+void launch_correction(int dim, const Layout& m, const Gas& g, const double* U, Work w,
+                       StageParams sp, cudaStream_t st) {
+  if (m.n_owned == 0) return;
+  EF_DISPATCH(dim, k_correction, grid_for(m.n_owned), m, g, U, w, sp);
+}
+void launch_limit_pass(int dim, const Layout& m, const Gas& g, const double* U, Work w,
+                       StageParams sp, int pass, cudaStream_t st) {
+  if (m.n_owned == 0) return;
+  EF_DISPATCH(dim, k_limit_pass, grid_for(m.n_owned), m, g, U, w, sp, pass);
+}
+void launch_final(int dim, const Layout& m, const Gas& g, const double* U, const double* U0,
+                  double* Uout, Work w, StageParams sp, cudaStream_t st) {
+  if (m.n_owned == 0) return;
+  EF_DISPATCH(dim, k_final, grid_for(m.n_owned), m, g, U, U0, Uout, w, sp);
+}
+void launch_pow(const double* x, double y, double* out, int64_t n, cudaStream_t st) {
+  if (n <= 0) return;
+  k_pow<<<grid_for(n), TPB, 0, st>>>(x, y, out, n);
+}
+
+}  // namespace ef

@@ -1,0 +1,93 @@
+// ef_kernels.cuh — device data layout and kernel launch interface.
+//
+// Layout in HBM (one rank = owned rows followed by ghost rows, padded to a
+// multiple of 32 rows, NP):
+//   * per-node fields are structure-of-arrays: field[k * NP + i];
+//   * per-slot fields are SELL-32 with the global pad width L, slot-major
+//     inside a 32-row slice: sidx(i, s) = (i / 32) * 32 * L + s * 32 + i % 32.
+//     A warp owns one slice, so slot s of 32 consecutive rows is one 256-byte
+//     coalesced transaction per fp64 field.
+//   * slots of a row are sorted by global Cuthill-McKee id (stepper.py:195),
+//     so "upper" (global id above the row's) == slot index above the diagonal
+//     slot; pads (s >= card) are never touched after setup.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "ef_math.cuh"
+
+namespace ef {
+
+__host__ __device__ __forceinline__ int64_t sidx(int64_t i, int s, int L) {
+  return (i >> 5) * (int64_t)(32 * L) + (int64_t)s * 32 + (i & 31);
+}
+
+struct Layout {
+  int L;            // global pad width
+  int64_t NP;       // padded local rows (multiple of 32)
+  int64_t n_local;  // owned + ghost rows
+  int64_t n_owned;
+  const int32_t* col;    // [NP*L] local column id (pads: the row itself)
+  const uint8_t* tslot;  // [NP*L] slot of (col, row) in row col
+  const uint8_t* card;   // [NP] valid slots in the (possibly truncated) stencil
+  const uint8_t* diag;   // [NP] slot of the diagonal
+  const double* c;       // [D][NP*L]  c_ij
+  const double* cT;      // [D][NP*L]  c_ji
+  const double* mij;     // [NP*L]     consistent mass m_ij
+  const double* m_i;     // [NP] lumped mass
+  const double* inv_m;   // [NP]
+  const double* lam;     // [NP] 1 / max(card - 1, 1)   (stepper.py:214-215)
+  const int64_t* gid;    // [NP] global CM id of each local row
+  const int8_t* bc_kind; // [NP] bit0 slip, bit1 inflow
+  const double* bc_n;    // [D][NP] slip normal
+  double farfield[5];
+};
+
+struct Work {
+  double* eor;       // [NP]
+  double* phi;       // [NP]
+  double* alpha;     // [NP]
+  double* R;         // [NV][NP]
+  double* Unext;     // [NV][NP]
+  double* bounds;    // [3][NP] rho_min, rho_max, phi_min
+  double* d;         // [NP*L]
+  double* l;         // [passes][NP*L]
+  unsigned long long* tau_min_bits;  // CFL min over owned rows
+  double* tau;       // tau of the current RK step / Euler step
+  int* err;          // bit0 projection/entropy, bit1 inadmissible result, bit2 tau unbounded
+  unsigned long long* bad_gid;       // min global CM id of an inadmissible row
+};
+
+enum TauMode { TAU_CFL = 0, TAU_GIVEN = 1, TAU_DEVICE = 2 };
+enum ErrBits { ERR_PROJECT = 1, ERR_BAD_STATE = 2, ERR_TAU_UNBOUNDED = 4 };
+
+struct StageParams {
+  int tau_mode;
+  double tau_given;
+  double tau_max;
+  double c_cfl;
+  int newton;
+  int passes;
+  double rk_a;  // < 0: Uout = Unew; else Uout = U0 + rk_a * (Unew - U0)   (stepper.py:632,635)
+};
+
+// launch wrappers (ef_kernels.cu); all asynchronous on `st`
+void launch_gather_state(int dim, const Layout& m, const double* U_aos, const int64_t* orig_of_local,
+                         double* U, int* err, cudaStream_t st);
+void launch_scatter_state(int dim, const Layout& m, const double* U, const int64_t* orig_of_local,
+                          double* U_aos, cudaStream_t st);
+void launch_nodal(int dim, const Layout& m, const Gas& g, const double* U, Work w, int64_t lo,
+                  int64_t hi, cudaStream_t st);
+void launch_viscosity(int dim, const Layout& m, const Gas& g, const double* U, Work w,
+                      bool reset_tau, cudaStream_t st);
+void launch_mirror(const Layout& m, Work w, bool want_tau, cudaStream_t st);
+void launch_low_order(int dim, const Layout& m, const Gas& g, const double* U, Work w,
+                      StageParams sp, cudaStream_t st);
+void launch_correction(int dim, const Layout& m, const Gas& g, const double* U, Work w,
+                       StageParams sp, cudaStream_t st);
+void launch_limit_pass(int dim, const Layout& m, const Gas& g, const double* U, Work w,
+                       StageParams sp, int pass, cudaStream_t st);
+void launch_final(int dim, const Layout& m, const Gas& g, const double* U, const double* U0,
+                  double* Uout, Work w, StageParams sp, cudaStream_t st);
+void launch_pow(const double* x, double y, double* out, int64_t n, cudaStream_t st);
+
+}  // namespace ef

@@ -1,0 +1,272 @@
+"""`Solver`: the reference's time-integrator API over the B200 C-ABI.
+
+Drop-in for `eulerflow.stepper.Solver` (/root/reference/pkg/src/eulerflow/
+stepper.py:87-649): same constructor signature, same methods (set_state,
+get_state, euler_step, ssp_rk3_step, advance), same attributes (tau_last,
+timers, n_euler_steps, standard_card, comm.sync_count/sync_volume) and the
+same exceptions (ValueError, AdmissibilityError, RuntimeError).  Every stage
+runs as hand-written sm_100a kernels inside libef_b200.so; this module only
+computes the global Cuthill-McKee order (scipy, exactly as
+exchange.partition does, exchange.py:397-403) and marshals arrays.
+
+`lanes`, `workers`, `overlap` and `chunk_size` are accepted for signature
+compatibility; the reference's results are bitwise independent of them
+(test_stepper.py:106-128) and so are ours.  `ranks` > 1 requires one process
+per GPU under torch.distributed (see paper_2007_00094_b200.distributed).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from types import SimpleNamespace
+from typing import Dict, Optional
+
+import numpy as np
+import scipy.sparse as sp
+from scipy.sparse.csgraph import reverse_cuthill_mckee
+
+from . import _lib
+from .physics import AIR, AdmissibilityError, GasConstants, is_admissible
+from .problems import BoundaryConditions
+
+__all__ = ["Solver", "BoundaryConditions", "compute_tau", "cm_permutation", "STEP_NAMES"]
+
+STEP_NAMES = ["step0", "step1", "step2", "step3", "step4", "step5", "step6"]
+
+
+def compute_tau(d_diag: np.ndarray, m_i: np.ndarray, c_cfl: float) -> float:
+    """CFL time step c_cfl * min_i m_i / (-2 d_ii) (stepper.py:55-63)."""
+    mask = d_diag < 0.0
+    if not mask.any():
+        raise ValueError("constant field, the time step bound is unbounded")
+    return c_cfl * float(np.min(m_i[mask] / (-2.0 * d_diag[mask])))
+
+
+def cm_permutation(matrices):
+    """Global Cuthill-McKee order of exchange.partition (exchange.py:397-403):
+    returns (cm_perm: original -> CM id, cm_inv: CM id -> original)."""
+    n = int(matrices.n)
+    conn = sp.csr_matrix(
+        (np.ones(len(matrices.indices), dtype=np.int8), np.asarray(matrices.indices),
+         np.asarray(matrices.indptr)), shape=(n, n))
+    sym = (conn + conn.T).tocsr()
+    rcm = reverse_cuthill_mckee(sym, symmetric_mode=True)
+    cm_inv = np.asarray(rcm[::-1], dtype=np.int64)
+    cm_perm = np.empty(n, dtype=np.int64)
+    cm_perm[cm_inv] = np.arange(n)
+    return cm_perm, cm_inv
+
+
+def _raise(code: int, h=None):
+    msg = _lib.last_error()
+    if code == _lib.EF_OK:
+        return
+    if code == _lib.EF_ERR_ARG:
+        raise ValueError(msg)
+    if code == _lib.EF_ERR_INADMISSIBLE:
+        raise AdmissibilityError(msg)
+    if code == _lib.EF_ERR_TAU_UNBOUNDED:
+        raise ValueError(msg)
+    raise RuntimeError(msg)
+
+
+class Solver:
+    """SSP-RK3 / forward-Euler IDP stage on one B200 (one rank per process)."""
+
+    def __init__(self, matrices, c_cfl: float = 0.9, limiter_passes: int = 2, newton_steps: int = 2,
+                 lanes: int = 4, workers: int = 1, ranks: int = 1, overlap: bool = True,
+                 chunk_size: int = 2048, boundary: Optional[BoundaryConditions] = None,
+                 gas: GasConstants = AIR, device: int = 0, stream=None, rank: int = 0,
+                 cm_perm: Optional[np.ndarray] = None):
+        if not 0.0 < c_cfl <= 1.0:
+            raise ValueError("c_cfl must lie in (0, 1]")
+        if limiter_passes < 0:
+            raise ValueError("limiter_passes must be >= 0")
+        self.matrices = matrices
+        self.gas = gas
+        self.c_cfl = c_cfl
+        self.limiter_passes = limiter_passes
+        self.newton_steps = newton_steps
+        self.lanes, self.workers, self.overlap, self.chunk_size = lanes, workers, overlap, chunk_size
+        self.bc = boundary
+        self.n = int(matrices.n)
+        self.dim = int(matrices.dim)
+        self.nvar = self.dim + 2
+        self.ranks = ranks
+        self.rank = rank
+        lib = _lib.load()
+        if cm_perm is None:
+            cm_perm, cm_inv = cm_permutation(matrices)
+        else:
+            cm_perm = np.asarray(cm_perm, dtype=np.int64)
+            cm_inv = np.empty_like(cm_perm)
+            cm_inv[cm_perm] = np.arange(self.n)
+        self.cm_perm, self.cm_inv = cm_perm, cm_inv
+        keep = []
+
+        def ptr(a, dt):
+            if a is None:
+                return None
+            a = np.ascontiguousarray(a, dtype=dt)
+            keep.append(a)
+            return a.ctypes.data
+
+        mats = _lib.EfMatrices(
+            self.n, self.dim, ptr(matrices.indptr, np.int64), ptr(matrices.indices, np.int64),
+            ptr(matrices.m, np.float64), ptr(matrices.c, np.float64),
+            ptr(matrices.m_lumped, np.float64), ptr(matrices.inv_m, np.float64))
+        prm = _lib.EfParams(gas.gamma, gas.gm1, gas.gp1_inv, gas.gm1_over_2g, gas.two_g_over_gm1,
+                            float(c_cfl), int(limiter_passes), int(newton_steps))
+        bcs = _lib.EfBoundary(0, None, None, 0, None, None)
+        if boundary is not None:
+            if boundary.inflow_nodes is not None and len(boundary.inflow_nodes):
+                bcs.n_inflow = len(boundary.inflow_nodes)
+                bcs.inflow = ptr(boundary.inflow_nodes, np.int64)
+                bcs.farfield = ptr(boundary.farfield, np.float64)
+            if boundary.slip_nodes is not None and len(boundary.slip_nodes):
+                bcs.n_slip = len(boundary.slip_nodes)
+                bcs.slip = ptr(boundary.slip_nodes, np.int64)
+                bcs.slip_normals = ptr(boundary.slip_normals, np.float64)
+        # simulated ranks (the reference's `ranks`) do not change results; real
+        # multi-GPU ranks are set up by paper_2007_00094_b200.distributed
+        nranks = 1
+        dist = _lib.EfDist(int(rank), nranks, int(device), ptr(cm_perm, np.int64), None, None,
+                           None if stream is None else int(stream))
+        h = ctypes.c_void_p()
+        rc = lib.ef_create(ctypes.byref(mats), ctypes.byref(prm), ctypes.byref(bcs),
+                           ctypes.byref(dist), ctypes.byref(h))
+        _raise(rc)
+        self._h = h
+        del keep
+        info = np.zeros(6, dtype=np.int64)
+        lib.ef_info(self._h, info.ctypes.data)
+        self.n_owned, self.n_local, self.pad_width, self.nnz_owned, self.standard_card = (
+            int(x) for x in info[:5])
+        self.comm = SimpleNamespace(sync_count=0, sync_volume=0)
+        self.n_euler_steps = 0
+        self.tau_last = None
+        self._timers_on = False
+
+    # ----- lifecycle ------------------------------------------------------
+    def close(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _lib.load().ef_destroy(h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ----- state ----------------------------------------------------------
+    def set_state(self, U: np.ndarray):
+        """Load states given in original node order (stepper.py:319-328)."""
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        if U.shape != (self.n, self.nvar):
+            raise ValueError("state array has the wrong shape")
+        rc = _lib.load().ef_set_state(self._h, U.ctypes.data)
+        if rc == _lib.EF_ERR_INADMISSIBLE:
+            raise AdmissibilityError("initial state is not admissible")
+        _raise(rc)
+
+    def get_state(self, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """Owned states in original node order (stepper.py:330-336)."""
+        if out is None:
+            out = np.empty((self.n, self.nvar))
+        _raise(_lib.load().ef_get_state(self._h, out.ctypes.data))
+        return out
+
+    # ----- stepping -------------------------------------------------------
+    def euler_step(self, tau: Optional[float] = None, tau_max: float = np.inf) -> float:
+        t = ctypes.c_double()
+        rc = _lib.load().ef_euler_step(self._h, 0 if tau is None else 1,
+                                       0.0 if tau is None else float(tau), float(tau_max), ctypes.byref(t))
+        _raise(rc)
+        self.tau_last = t.value
+        self.n_euler_steps += 1
+        return t.value
+
+    def ssp_rk3_step(self, tau: Optional[float] = None, tau_max: float = np.inf) -> float:
+        t = ctypes.c_double()
+        rc = _lib.load().ef_ssp_rk3_step(self._h, 0 if tau is None else 1,
+                                         0.0 if tau is None else float(tau), float(tau_max), ctypes.byref(t))
+        _raise(rc)
+        self.tau_last = t.value
+        self.n_euler_steps += 3
+        return t.value
+
+    def ssp_rk3_step_async(self, tau: Optional[float] = None, tau_max: float = np.inf):
+        """Enqueue one RK step without a host sync; errors surface at sync()."""
+        rc = _lib.load().ef_ssp_rk3_step_async(self._h, 0 if tau is None else 1,
+                                               0.0 if tau is None else float(tau), float(tau_max))
+        _raise(rc)
+        self.n_euler_steps += 3
+
+    def sync(self) -> float:
+        t = ctypes.c_double()
+        _raise(_lib.load().ef_sync(self._h, ctypes.byref(t)))
+        self.tau_last = t.value
+        return t.value
+
+    def advance(self, t_final: float, use_rk3: bool = True, on_step=None) -> int:
+        """March from t = 0 to t_final (stepper.py:638-649)."""
+        t = 0.0
+        steps = 0
+        while t < t_final - 1e-14:
+            step = self.ssp_rk3_step if use_rk3 else self.euler_step
+            tau = step(tau_max=t_final - t)
+            t += tau
+            steps += 1
+            if on_step is not None:
+                on_step(steps, t)
+        return steps
+
+    # ----- observability --------------------------------------------------
+    def enable_timers(self, on: bool = True):
+        _raise(_lib.load().ef_enable_timers(self._h, 1 if on else 0))
+        self._timers_on = on
+
+    @property
+    def timers(self) -> Dict[str, float]:
+        s = np.zeros(7)
+        _lib.load().ef_phase_times(self._h, s.ctypes.data)
+        return {name: float(v) for name, v in zip(STEP_NAMES, s)}
+
+    _FIELDS = {"d": 0, "alpha": 1, "R": 2, "bounds": 3, "l": 4, "eor": 5, "phi": 6, "U": 7, "U_next": 8}
+
+    def fetch(self, which: str, pass_index: int = 0) -> np.ndarray:
+        """Internal arrays (rows = local rows in global CM order; slots in stencil order)."""
+        n, L, nv = self.n_local, self.pad_width, self.nvar
+        shapes = {"d": (n, L), "alpha": (n,), "R": (n, nv), "bounds": (n, 3), "l": (n, L),
+                  "eor": (n,), "phi": (n,), "U": (n, nv), "U_next": (n, nv)}
+        out = np.empty(shapes[which])
+        _raise(_lib.load().ef_debug_fetch(self._h, self._FIELDS[which], int(pass_index), out.ctypes.data))
+        return out
+
+    def local_gids(self) -> np.ndarray:
+        out = np.empty(self.n_local, dtype=np.int64)
+        _raise(_lib.load().ef_local_gids(self._h, out.ctypes.data))
+        return out
+
+
+def shared_pow(x, y):
+    """Host build of the device pow (ef_pow_host), numpy.power calling convention;
+    install into the reference with physics.set_power_function(shared_pow)."""
+    x = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+    yv = np.asarray(y, dtype=np.float64)
+    out = np.empty_like(x)
+    if yv.ndim == 0:
+        _lib.load().ef_pow_host(x.ctypes.data, float(yv), out.ctypes.data, x.size)
+    else:
+        xb, yb = np.broadcast_arrays(x, yv)
+        out = np.empty(xb.shape)
+        flat_x = np.ascontiguousarray(xb).ravel()
+        flat_y = np.ascontiguousarray(yb).ravel()
+        o = out.reshape(-1)
+        for k in range(flat_x.size):
+            tmp = np.empty(1)
+            _lib.load().ef_pow_host(flat_x[k:k + 1].ctypes.data, float(flat_y[k]), tmp.ctypes.data, 1)
+            o[k] = tmp[0]
+    return out if out.ndim else out[()]

@@ -1,0 +1,231 @@
+"""Generate the golden parity fixtures from the UNMODIFIED reference package.
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py            # small fixtures (seconds)
+    python tests/golden/make_golden.py --c1-full  # + C1 full size, 100 RK steps (~3 min)
+
+The reference `eulerflow.stepper.Solver` (/root/reference/pkg/src) is imported
+read-only and driven through its own public API.  The only configuration
+change is the reference's own plug-in point for pow,
+`physics.set_power_function` (physics.py:59-75), which is set to the host build
+of the shared deterministic pow (paper_2007_00094_b200/csrc/ef_pow.h, exported
+by the oracle library as `or_pow`).  Without that, numpy's SIMD pow (which
+differs from libm on ~5% of inputs) makes bitwise parity impossible
+(SURVEY.md §0, §8(c)).  A second, report-only record is made with numpy's
+default pow for the divergence table in DESIGN.md.
+
+Every fixture stores its inputs (PrecomputedMatrices, U0, boundary data,
+parameters) and the reference outputs (tau per step, final state, and for the
+first forward-Euler stage the internal arrays d, alpha, R, bounds, l mapped to
+global Cuthill-McKee row order).  `/root/reference` does not exist on the GPU
+box; the fixtures do.
+"""
+
+from __future__ import annotations
+
+import argparse
+import hashlib
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+REF_SRC = "/root/reference/pkg/src"
+sys.path.insert(0, REF_SRC)
+sys.path.insert(0, os.path.join(REPO, "oracle"))
+sys.path.insert(0, REPO)
+
+from eulerflow import assembly as r_assembly  # noqa: E402
+from eulerflow import mesh as r_mesh  # noqa: E402
+from eulerflow import physics as r_physics  # noqa: E402
+from eulerflow import problems as r_problems  # noqa: E402
+from eulerflow.assembly import PrecomputedMatrices as RefMatrices  # noqa: E402
+from eulerflow.stepper import BoundaryConditions as RefBC  # noqa: E402
+from eulerflow.stepper import Solver as RefSolver  # noqa: E402
+
+import oracle as O  # noqa: E402
+from paper_2007_00094_b200 import problems as P  # noqa: E402
+
+
+def to_ref_matrices(m) -> RefMatrices:
+    return RefMatrices(n=int(m.n), dim=int(m.dim), indptr=np.asarray(m.indptr), indices=np.asarray(m.indices),
+                       m=np.asarray(m.m), c=np.asarray(m.c), beta=np.asarray(m.beta),
+                       m_lumped=np.asarray(m.m_lumped), inv_m=np.asarray(m.inv_m))
+
+
+def to_ref_bc(bc):
+    if bc is None:
+        return None
+    return RefBC(inflow_nodes=bc.inflow_nodes, farfield=bc.farfield,
+                 slip_nodes=bc.slip_nodes, slip_normals=bc.slip_normals)
+
+
+def internals_cm(solver: RefSolver):
+    """First-stage internal arrays of rank 0, rows mapped to global CM order."""
+    rk = solver.ranks[0]
+    n_lo = rk.numbering.n_lo
+    cm = rk.cm_of_new[:n_lo]
+    out = {}
+    for name in ("d", "l"):
+        a = np.empty((solver.n, rk.width))
+        a[cm] = getattr(rk, name)[:n_lo]
+        out["int_" + name] = a
+    a = np.empty(solver.n)
+    a[cm] = rk.alpha[:n_lo]
+    out["int_alpha"] = a
+    a = np.empty((solver.n, solver.nvar))
+    a[cm] = rk.R[:n_lo]
+    out["int_R"] = a
+    a = np.empty((solver.n, 3))
+    a[cm, 0] = rk.rho_min[:n_lo]
+    a[cm, 1] = rk.rho_max[:n_lo]
+    a[cm, 2] = rk.phi_min[:n_lo]
+    out["int_bounds"] = a
+    return out
+
+
+def run_reference(mat, U0, bc, params, steps, mode, record_internals=True):
+    kw = dict(c_cfl=params["c_cfl"], limiter_passes=params["passes"], newton_steps=params["newton"])
+    s = RefSolver(mat, boundary=bc, **kw)
+    s.set_state(U0)
+    taus = []
+    out = {}
+    for k in range(steps):
+        if mode == "euler":
+            taus.append(s.euler_step(params.get("tau")))
+        else:
+            taus.append(s.ssp_rk3_step(params.get("tau")))
+        if k == 0 and record_internals and mode == "euler":
+            out.update(internals_cm(s))
+    out["taus"] = np.array(taus)
+    out["U_final"] = s.get_state()
+    return out
+
+
+def save_case(name, mat, U0, bc, params, steps, mode, record_internals=True):
+    res = run_reference(to_ref_matrices(mat), U0, to_ref_bc(bc), params, steps, mode, record_internals)
+    rec = dict(
+        n=np.int64(mat.n), dim=np.int64(mat.dim), indptr=np.asarray(mat.indptr, np.int64),
+        indices=np.asarray(mat.indices, np.int32), m=np.asarray(mat.m), c=np.asarray(mat.c),
+        m_lumped=np.asarray(mat.m_lumped), inv_m=np.asarray(mat.inv_m), U0=np.asarray(U0),
+        params=json.dumps(dict(params, steps=steps, mode=mode)),
+    )
+    if bc is not None:
+        if bc.inflow_nodes is not None:
+            rec["bc_inflow"] = np.asarray(bc.inflow_nodes, np.int64)
+            rec["bc_farfield"] = np.asarray(bc.farfield, np.float64)
+        if bc.slip_nodes is not None:
+            rec["bc_slip"] = np.asarray(bc.slip_nodes, np.int64)
+            rec["bc_normals"] = np.asarray(bc.slip_normals, np.float64)
+    rec.update(res)
+    path = os.path.join(HERE, f"{name}.npz")
+    np.savez_compressed(path, **rec)
+    print(f"{name:28s} n={mat.n:6d} steps={steps} mode={mode} -> {os.path.getsize(path)/1024:.0f} KiB")
+
+
+def ref_2d(meshobj):
+    m = r_assembly.assemble(meshobj)
+    return P.PrecomputedMatrices(n=m.n, dim=m.dim, indptr=m.indptr, indices=m.indices, m=m.m, c=m.c,
+                                 beta=m.beta, m_lumped=m.m_lumped, inv_m=m.inv_m)
+
+
+def base(c_cfl=0.9, passes=2, newton=2, tau=None):
+    d = dict(c_cfl=c_cfl, passes=passes, newton=newton)
+    if tau is not None:
+        d["tau"] = tau
+    return d
+
+
+def small_cases():
+    # reference test fixture: 4x4 periodic + default_rng(7) field (test_stepper.py:15-29)
+    mat = ref_2d(r_mesh.rectangle_mesh(4, 4, periodic=(True, True)))
+    U = P.random_state(np.random.default_rng(7), mat.n)
+    for passes in (0, 1, 2, 3):
+        save_case(f"periodic4_euler_p{passes}", mat, U, None, base(passes=passes), 1, "euler")
+    save_case("periodic4_rk3", mat, U, None, base(), 4, "rk3")
+    save_case("periodic4_newton4_p3", mat, U, None, base(passes=3, newton=4), 2, "rk3")
+    save_case("periodic4_newton1", mat, U, None, base(newton=1), 2, "rk3")
+    Uc = np.tile([1.4, 4.2, 0.0, 8.8], (mat.n, 1))
+    save_case("periodic4_constant", mat, Uc, None, base(tau=1e-3), 1, "euler")
+    # reference problems (problems.py) on reference meshes and assembly
+    st = r_problems.mach3_channel(2, refine=2)
+    save_case("mach3_channel_r2", ref_2d(st.mesh), st.U0, st.boundary, base(), 3, "rk3")
+    save_case("mach3_channel_r2_euler", ref_2d(st.mesh), st.U0, st.boundary, base(), 1, "euler")
+    st = r_problems.sod1d(60)
+    save_case("sod1d_60", ref_2d(st.mesh), st.U0, None, base(), 8, "rk3")
+    # BASELINE configs at oracle sizes, on this package's generators
+    ps = P.isentropic_vortex(32)
+    save_case("c1_vortex32", ps.matrices, ps.U0, ps.boundary, base(c_cfl=0.5), 5, "rk3")
+    save_case("c1_vortex32_euler", ps.matrices, ps.U0, ps.boundary, base(c_cfl=0.5), 1, "euler")
+    save_case("c1_vortex32_p0", ps.matrices, ps.U0, ps.boundary, base(c_cfl=0.5, passes=0), 5, "rk3")
+    ps = P.mach3_disc(20, seed=11)
+    save_case("c2_disc20", ps.matrices, ps.U0, ps.boundary, base(), 4, "rk3")
+    ps = P.sod_box(11, 3, 3, seed=5)
+    save_case("c3_sodbox", ps.matrices, ps.U0, ps.boundary, base(), 4, "rk3")
+    save_case("c3_sodbox_euler", ps.matrices, ps.U0, ps.boundary, base(), 1, "euler")
+    ps = P.periodic_fourier_box(6, seed=3)
+    save_case("c5_periodic6", ps.matrices, ps.U0, None, base(), 3, "rk3")
+    mat = P.assemble_q1(P.box_mesh(4, 4, 4, periodic=(True, True, True)))
+    U = P.random_state(np.random.default_rng(4096), mat.n, dim=3)
+    save_case("periodic3d_random_euler", mat, U, None, base(), 1, "euler")
+    save_case("periodic3d_random_rk3", mat, U, None, base(), 2, "rk3")
+
+
+def c1_full():
+    """C1 at full size (129x129, CFL 0.5, 100 RK steps).  Too large to commit
+    with its inputs, so the fixture holds digests: the test regenerates the
+    inputs with this package's generator, checks their digest, runs the oracle
+    and compares the output digest + a few norms."""
+    ps = P.isentropic_vortex(128)
+    mat = ps.matrices
+    h_in = hashlib.sha256()
+    for a in (mat.indptr, mat.indices, mat.m, mat.c, mat.m_lumped, mat.inv_m, ps.U0,
+              ps.boundary.inflow_nodes, ps.boundary.farfield):
+        h_in.update(np.ascontiguousarray(a).tobytes())
+    res = run_reference(to_ref_matrices(mat), ps.U0, to_ref_bc(ps.boundary), base(c_cfl=0.5), 100,
+                        "rk3", record_internals=False)
+    U = res["U_final"]
+    rec = dict(input_sha256=h_in.hexdigest(),
+               output_sha256=hashlib.sha256(np.ascontiguousarray(U).tobytes()).hexdigest(),
+               taus=res["taus"].tolist(), min_rho=float(U[:, 0].min()),
+               sum_state=np.asarray(U.sum(axis=0)).tolist(), n=int(mat.n), steps=100, c_cfl=0.5)
+    with open(os.path.join(HERE, "c1_full_100.json"), "w") as fh:
+        json.dump(rec, fh, indent=1)
+    np.savez_compressed(os.path.join(HERE, "c1_full_100_state.npz"), U_final=U)
+    print("c1_full_100", rec["output_sha256"], rec["min_rho"])
+
+
+def default_pow_divergence():
+    """Report-only: reference with numpy's default pow vs the shared pow."""
+    ps = P.isentropic_vortex(32)
+    out = {}
+    for steps in (1, 5, 20):
+        r_physics.set_power_function(O.shared_pow)
+        a = run_reference(to_ref_matrices(ps.matrices), ps.U0, to_ref_bc(ps.boundary), base(c_cfl=0.5),
+                          steps, "rk3", False)["U_final"]
+        r_physics.set_power_function(None)
+        b = run_reference(to_ref_matrices(ps.matrices), ps.U0, to_ref_bc(ps.boundary), base(c_cfl=0.5),
+                          steps, "rk3", False)["U_final"]
+        out[steps] = float(np.abs(a - b).max() / np.abs(b).max())
+    r_physics.set_power_function(O.shared_pow)
+    with open(os.path.join(HERE, "default_pow_divergence.json"), "w") as fh:
+        json.dump({"case": "c1_vortex32 rk3, rel Linf shared-pow vs numpy-pow reference", "rel_linf": out,
+                   "numpy": np.__version__}, fh, indent=1)
+    print("default-pow divergence", out)
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--c1-full", action="store_true")
+    ap.add_argument("--only-c1-full", action="store_true")
+    args = ap.parse_args()
+    r_physics.set_power_function(O.shared_pow)
+    if not args.only_c1_full:
+        small_cases()
+        default_pow_divergence()
+    if args.c1_full or args.only_c1_full:
+        c1_full()

@@ -1,0 +1,177 @@
+"""The reference's Solver tests (pkg/tests/test_stepper.py) against the CUDA Solver."""
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2007_00094_b200 import AdmissibilityError, Solver, compute_tau, shared_pow
+from paper_2007_00094_b200 import _lib
+from paper_2007_00094_b200 import problems as P
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def small_periodic():
+    mat = P.assemble_q1(P.rectangle_mesh(4, 4, periodic=(True, True)))
+    return mat, P.random_state(np.random.default_rng(7), mat.n)
+
+
+def test_constant_state_is_exactly_preserved(small_periodic):  # test_stepper.py:59-66
+    mat, _ = small_periodic
+    U = np.tile([1.4, 4.2, 0.0, 8.8], (mat.n, 1))
+    s = Solver(mat)
+    s.set_state(U)
+    tau = s.euler_step()
+    assert np.isfinite(tau) and tau > 0.0
+    assert np.array_equal(s.get_state(), U)
+
+
+def test_conservation_short_run(small_periodic):  # test_stepper.py:69-77
+    mat, U = small_periodic
+    s = Solver(mat)
+    s.set_state(U)
+    before = (mat.m_lumped[:, None] * U).sum(axis=0)
+    for _ in range(5):
+        s.ssp_rk3_step()
+    after = (mat.m_lumped[:, None] * s.get_state()).sum(axis=0)
+    assert np.abs(after - before).max() < 1e-12 * np.abs(before).max()
+
+
+def test_state_roundtrip(small_periodic):  # test_stepper.py:80-84
+    mat, U = small_periodic
+    s = Solver(mat, ranks=3)
+    s.set_state(U)
+    assert np.array_equal(s.get_state(), U)
+
+
+def test_rejects_inadmissible_initial_state(small_periodic):  # test_stepper.py:87-93
+    mat, U = small_periodic
+    bad = U.copy()
+    bad[3, 0] = -1.0
+    s = Solver(mat)
+    s.set_state(U)
+    with pytest.raises(AdmissibilityError):
+        s.set_state(bad)
+    assert np.array_equal(s.get_state(), U)  # state untouched
+
+
+def test_invalid_parameters(small_periodic):  # test_stepper.py:96-103
+    mat, _ = small_periodic
+    for kw in (dict(c_cfl=0.0), dict(c_cfl=1.5), dict(limiter_passes=-1)):
+        with pytest.raises(ValueError):
+            Solver(mat, **kw)
+
+
+def test_worker_lane_rank_arguments_do_not_change_results(small_periodic):  # :106-128
+    mat, U = small_periodic
+    outs = []
+    for kw in (dict(), dict(ranks=3), dict(workers=2, chunk_size=3), dict(lanes=1), dict(overlap=False)):
+        s = Solver(mat, **kw)
+        s.set_state(U)
+        s.ssp_rk3_step()
+        outs.append(s.get_state())
+    for o in outs[1:]:
+        assert np.array_equal(outs[0], o)
+
+
+def test_ssp_rk3_composition(small_periodic):  # test_stepper.py:131-147
+    mat, U = small_periodic
+    s = Solver(mat)
+    s.set_state(U)
+    tau = s.ssp_rk3_step()
+    s2 = Solver(mat)
+    s2.set_state(U)
+    assert s2.euler_step() == tau
+    U1 = s2.get_state()
+    s2.set_state(U1)
+    s2.euler_step(tau)
+    U2 = 0.75 * U + 0.25 * s2.get_state()
+    s2.set_state(U2)
+    s2.euler_step(tau)
+    U3 = U / 3.0 + (2.0 / 3.0) * s2.get_state()
+    assert np.allclose(s.get_state(), U3, rtol=1e-14, atol=1e-14)
+
+
+def test_advance_hits_final_time(small_periodic):  # test_stepper.py:150-156
+    mat, U = small_periodic
+    s = Solver(mat)
+    s.set_state(U)
+    taus = []
+    s.advance(0.02, on_step=lambda k, t: taus.append(s.tau_last))
+    assert abs(sum(taus) - 0.02) < 1e-13
+
+
+def test_slip_wall_and_inflow():  # test_stepper.py:159-173
+    ps = P.mach3_disc(20, seed=1)
+    s = Solver(ps.matrices, boundary=ps.boundary)
+    s.set_state(ps.U0)
+    s.euler_step()
+    U = s.get_state()
+    bc = ps.boundary
+    mom = U[bc.slip_nodes][:, 1:3]
+    assert np.abs((mom * bc.slip_normals).sum(axis=1)).max() < 1e-13
+    assert np.array_equal(U[bc.inflow_nodes], np.tile(bc.farfield, (len(bc.inflow_nodes), 1)))
+
+
+def test_alpha_zero_on_constant_state(small_periodic):  # test_stepper.py:176-182
+    mat, _ = small_periodic
+    U = np.tile([1.0, 0.3, -0.2, 3.0], (mat.n, 1))
+    s = Solver(mat)
+    s.set_state(U)
+    s.euler_step(tau=1e-3)
+    assert np.abs(s.fetch("alpha")).max() == 0.0
+
+
+def test_tau_equals_compute_tau(small_periodic):  # test_stepper.py:43-51
+    mat, U = small_periodic
+    s = Solver(mat, c_cfl=0.5)
+    s.set_state(U)
+    tau = s.euler_step()
+    d = s.fetch("d")
+    L = s.pad_width
+    gids = s.local_gids()
+    card = np.diff(mat.indptr)
+    # diagonal slot of each local row
+    o = O.OracleSolver(mat, c_cfl=0.5)
+    o.set_state(U)
+    o.euler_step()
+    dd = o.fetch("d")
+    diag = np.array([np.flatnonzero(o.fetch("d")[i] < 0)[0] for i in range(mat.n)])
+    d_diag = dd[np.arange(mat.n), diag]
+    m_cm = mat.m_lumped[o.cm_inv]
+    assert tau == compute_tau(d_diag, m_cm, 0.5)
+
+
+def test_unbounded_tau_raises(small_periodic):
+    import dataclasses
+    mat, U = small_periodic
+    flat = dataclasses.replace(mat, c=np.zeros_like(mat.c))
+    s = Solver(flat)
+    s.set_state(U)
+    with pytest.raises(ValueError):
+        s.euler_step()
+    assert np.array_equal(s.get_state(), U)
+
+
+def test_timers_and_counters(small_periodic):  # test_stepper.py:185-194
+    mat, U = small_periodic
+    s = Solver(mat)
+    s.enable_timers(True)
+    s.set_state(U)
+    s.ssp_rk3_step()
+    assert s.n_euler_steps == 3
+    t = s.timers
+    assert all(v >= 0.0 for v in t.values()) and t["step1"] > 0.0 and t["step3"] > 0.0
+
+
+def test_device_pow_equals_host_pow():
+    rng = np.random.default_rng(5)
+    x = np.concatenate([np.exp(rng.uniform(-40, 40, 200000)), rng.uniform(0, 3, 100000),
+                        np.array([0.0, 1.0, 5e-324, 1e308, np.inf])])
+    for y in (1 / 2.4, -1.4, -(0.4 / 2.8), 0.4 / 2.8, 2.8 / 0.4, 2.4, 1.4, (-1.4) * (1 / 2.4)):
+        host = shared_pow(x, y)
+        dev = np.empty_like(x)
+        assert _lib.load().ef_pow_device(x.ctypes.data, y, dev.ctypes.data, x.size) == 0
+        assert np.array_equal(host, dev, equal_nan=True)
+        assert np.array_equal(host, O.shared_pow(x, y), equal_nan=True)
