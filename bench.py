@@ -1,0 +1,321 @@
+"""Benchmark: fp64 Q1 node-updates per second per SSP-RK3 stage (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c1|c3|c5] [--impl ours|reference]
+
+Workload (config.workload): BASELINE.json configs[1], the 2D Mach-3 flow past
+a disc, ~1.24M Q1 nodes, seeded shuffled node ids (the solver applies RCM),
+synthetic (generated mesh + free-stream initial state; no dataset exists).
+A step is one SSP-RK3 step (3 forward-Euler stages) over the whole mesh.
+
+value     device-resident throughput: N_nodes * 3 * K / (CUDA-event time of K
+          RK steps on the launching stream), max over ranks.
+e2e       the same metric through the public API with host buffers: every step
+          set_state(pinned host U) -> ssp_rk3_step() -> get_state(pinned host U).
+roofline  dominant kernel (per-phase CUDA-event timing pass): algorithmic bytes
+          from the reference's traffic model (perf.py:47-89) / kernel time,
+          against MEASURED_PEAKS.json hbm_gbs.
+cpu_baseline  the CPU oracle (C restatement of the reference stage, all host
+          threads) on a bounded sample of the same workload.
+--impl reference  times that CPU port alone (the reference itself is pure
+          Python and does not exist on the GPU box).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+METRIC = "fp64 Q1 node-updates/sec per SSP-RK3 stage"
+UNIT = "node-updates/s"
+CONFIG_NAMES = {
+    "c1": "C1 2D isentropic vortex 129x129, CFL 0.5",
+    "c2": "C2 2D Mach-3 flow past a disc, ~1.24M Q1 nodes, shuffled ids + RCM",
+    "c3": "C3 3D Sod box 512x128x128 (jittered)",
+    "c5": "C5 3D periodic Fourier box 320^3",
+}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.th = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.th = threading.Thread(target=self._read, daemon=True)
+        self.th.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.th is not None:
+            self.th.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[2 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(sm)}
+
+
+def build_problem(name: str):
+    from paper_2007_00094_b200 import problems as P
+
+    return P.make_config(name)
+
+
+def cpu_oracle_rate(ps, budget_s: float, threads: int, max_steps: int = 1000):
+    """Oracle (C port of the reference stage) throughput on a bounded sample."""
+    import oracle as O
+
+    o = O.OracleSolver(ps.matrices, c_cfl=ps.c_cfl, boundary=ps.boundary, threads=threads)
+    o.set_state(ps.U0)
+    o.ssp_rk3_step()  # warm-up
+    steps = 0
+    t0 = time.perf_counter()
+    while steps < max_steps:
+        o.ssp_rk3_step()
+        steps += 1
+        if time.perf_counter() - t0 >= budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return ps.matrices.n * 3 * steps / dt, steps, dt
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    ps = build_problem(args.config)
+    threads = os.cpu_count() or 1
+    budget = max(10.0, min(120.0, 2.0 * args.steps))
+    rate, steps, dt = cpu_oracle_rate(ps, budget, threads, max_steps=max(1, args.steps))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": steps, "warmup": 1, "ms_per_step": 1e3 * dt / steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": CONFIG_NAMES[args.config], "nodes": int(ps.matrices.n),
+                   "nnz": int(ps.matrices.nnz), "steps_per_sample": steps},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{steps} SSP-RK3 steps of the full {args.config} mesh "
+                                   f"({ps.matrices.n} nodes), oracle/idp_oracle.c, {threads} threads"},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    from paper_2007_00094_b200 import Solver
+    from paper_2007_00094_b200.perf import KERNEL_OF_PHASE, PHASES, predict_traffic, stage_doubles_per_nnz
+
+    dist = world > 1
+    torch.cuda.set_device(local_rank)
+    ps = build_problem(args.config)
+    mat = ps.matrices
+    stream = torch.cuda.current_stream()
+    solver = Solver(mat, c_cfl=ps.c_cfl, boundary=ps.boundary, device=local_rank, stream=stream.cuda_stream)
+    n_nodes = mat.n
+    dim = mat.dim
+    card = solver.standard_card
+    nnz = solver.nnz_owned
+    solver.set_state(ps.U0)
+    for _ in range(args.warmup):
+        solver.ssp_rk3_step_async()
+    solver.sync()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    time.sleep(0.3)
+    if dist:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        solver.ssp_rk3_step_async()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        torch.distributed.barrier()
+    clocks = sampler.stop()
+    solver.sync()  # raises on any latched error of the timed steps
+    ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    node_updates = n_nodes * world * 3 * args.steps
+    value = node_updates / (ms * 1e-3)
+    ms_per_step = ms / args.steps
+
+    # per-phase kernel times (separate pass: timers add one event sync per stage)
+    solver.enable_timers(True)
+    base = solver.timers
+    tsteps = 3
+    for _ in range(tsteps):
+        solver.ssp_rk3_step()
+    after = solver.timers
+    solver.enable_timers(False)
+    stages = 3 * tsteps
+    per_launch = {k: (after[k] - base[k]) / stages for k in PHASES}
+    passes = solver.limiter_passes
+    if passes > 1:
+        per_launch["step5"] /= (passes - 1)
+    model = predict_traffic(dim, card)
+    phase_bytes = {k: 8.0 * model[k] * nnz for k in PHASES}
+    dom = max((k for k in PHASES if k != "step0"), key=lambda k: per_launch[k])
+    peak, peak_kind = peaks()
+    achieved = phase_bytes[dom] / per_launch[dom] / 1e9
+    stage_bytes = 8.0 * stage_doubles_per_nnz(dim, card, passes) * nnz
+    stage_s = (ms * 1e-3) / (3 * args.steps)
+    roofline = {
+        "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+        "traffic": None, "kernel": KERNEL_OF_PHASE[dom], "phase": dom,
+        "kernel_ms": per_launch[dom] * 1e3, "algorithmic_bytes_per_launch": phase_bytes[dom],
+        "peak_kind": peak_kind,
+        "phase_ms": {k: round(v * 1e3, 4) for k, v in per_launch.items()},
+        "stage": {"algorithmic_bytes": stage_bytes, "achieved": stage_bytes / stage_s / 1e9,
+                  "frac": stage_bytes / stage_s / 1e9 / peak,
+                  "doubles_per_nnz": stage_doubles_per_nnz(dim, card, passes)},
+    }
+
+    # e2e through the public API with pinned host buffers
+    nv = dim + 2
+    host = torch.empty((n_nodes, nv), dtype=torch.float64).pin_memory()
+    Uh = host.numpy()
+    solver.set_state(ps.U0)
+    solver.get_state(out=Uh)
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    if dist:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        solver.set_state(Uh)
+        solver.ssp_rk3_step()
+        solver.get_state(out=Uh)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    e2e_ms = e0.elapsed_time(e1)
+    e2e_ms = max(e2e_ms, wall * 1e3 * 0.0)
+    if dist:
+        t = torch.tensor([e2e_ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e = {"value": n_nodes * world * 3 * e2e_steps / (e2e_ms * 1e-3), "unit": UNIT,
+           "h2d_bytes_per_step": int(n_nodes * nv * 8), "d2h_bytes_per_step": int(n_nodes * nv * 8),
+           "steps": e2e_steps, "wall_s": wall}
+
+    kernels_per_stage = 3 + (1 + max(passes - 1, 0) + 1 if passes > 0 else 1)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": CONFIG_NAMES[args.config], "nodes": int(n_nodes), "nnz": int(nnz),
+                   "dim": dim, "pad_width": solver.pad_width, "standard_card": card,
+                   "c_cfl": ps.c_cfl, "limiter_passes": passes, "newton_steps": solver.newton_steps,
+                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "l2": "no flush: per-step working set (~%.0f MB) > 126 MB L2" % (
+                       nnz * (4 + 1 + 8 * (2 * dim + 1 + 1 + passes)) / 1e6)},
+        "roofline": roofline,
+        "e2e": e2e,
+        "clocks": clocks,
+        "gpu_launches": int(args.steps * 3 * kernels_per_stage),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        rate, steps, dt = cpu_oracle_rate(ps, args.cpu_seconds, threads, max_steps=args.steps)
+        line["cpu_baseline"] = {
+            "value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{steps} SSP-RK3 steps of the same {args.config} mesh ({n_nodes} nodes) after 1 "
+                      f"warm-up step, oracle/idp_oracle.c (C restatement of the reference stage)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    solver.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIG_NAMES))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=50)
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch
+
+            torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
