@@ -9,6 +9,7 @@
 //   * ghost rows (nranks > 1) carry the stencil truncated to local rows
 //     (stepper.py:175-181).
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cstdio>
 #include <cstring>
@@ -67,8 +68,10 @@ struct ef_solver {
   bool timing = false;
   double phase_s[7] = {0, 0, 0, 0, 0, 0, 0};
   int64_t n_euler = 0;
-  cudaEvent_t ev[8];
-  bool ev_made = false;
+  // timing ring: 8 events per stage, recorded without host syncs and folded
+  // into phase_s when the ring fills or the timers are read
+  std::vector<std::array<cudaEvent_t, 8>> ring;
+  int ring_used = 0;
 
   template <class T>
   int alloc(T** p, size_t count) {
@@ -84,8 +87,8 @@ struct ef_solver {
   ~ef_solver() {
     for (void* p : allocs) cudaFree(p);
     if (rb) cudaFreeHost(rb);
-    if (ev_made)
-      for (auto& e : ev) cudaEventDestroy(e);
+    for (auto& set : ring)
+      for (auto& e : set) cudaEventDestroy(e);
     if (own_stream && st) cudaStreamDestroy(st);
   }
 };
@@ -266,6 +269,16 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_params* prm, con
     }
   }
   h->nnz_owned = nnz_owned;
+  // upper-triangle edge list (all local rows: ghost rows need d for the mirror)
+  if (NPL >= (int64_t)1 << 31) return fail(EF_ERR_ARG, "local slot count exceeds int32 positions");
+  std::vector<int32_t> edges;
+  for (int64_t sl = 0; sl < NP / 32; ++sl)
+    for (int s = 0; s < L; ++s)
+      for (int ln = 0; ln < 32; ++ln) {
+        const int64_t i = sl * 32 + ln;
+        if (i >= n_local) continue;
+        if (s > diag[i] && s < card[i]) edges.push_back((int32_t)ef::sidx(i, s, (int)L));
+      }
   // boundary data (stepper.py:258-267): owned rows only
   std::vector<int8_t> bc_kind(NP, 0);
   std::vector<double> bc_n((size_t)D * NP, 0.0);
@@ -317,6 +330,10 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_params* prm, con
   EF_TRY(upload(h, &d_gid, gid));
   EF_TRY(upload(h, &d_bck, bc_kind));
   EF_TRY(upload(h, &d_bcn, bc_n));
+  int32_t* d_edges;
+  EF_TRY(upload(h, &d_edges, edges));
+  m.edges = d_edges;
+  m.n_edges = (int64_t)edges.size();
   m.col = d_col;
   m.tslot = d_tslot;
   m.card = d_card;
@@ -411,8 +428,6 @@ int ef_create(const ef_matrices* mat, const ef_params* prm, const ef_boundary* b
     g_err = msg;
     return rc;
   }
-  for (auto& ev : h->ev) cudaEventCreate(&ev);
-  h->ev_made = true;
   *out = h;
   return EF_OK;
 }
@@ -473,41 +488,58 @@ int ef_get_state(ef_solver* h, double* U) {
 }
 
 // ---- one forward-Euler stage (stepper.py:508-610) --------------------------------
-static void mark(ef_solver* h, int k) {
-  if (h->timing) cudaEventRecord(h->ev[k], h->st);
+static int flush_timers(ef_solver* h) {
+  for (int q = 0; q < h->ring_used; ++q) {
+    EF_CUDA(cudaEventSynchronize(h->ring[q][7]));
+    for (int k = 0; k < 7; ++k) {
+      float ms = 0.f;
+      EF_CUDA(cudaEventElapsedTime(&ms, h->ring[q][k], h->ring[q][k + 1]));
+      h->phase_s[k] += ms * 1e-3;
+    }
+  }
+  h->ring_used = 0;
+  return EF_OK;
+}
+
+static int mark(ef_solver* h, int k) {
+  if (!h->timing) return EF_OK;
+  if (k == 0 && h->ring_used == (int)h->ring.size()) {
+    if (h->ring.size() < 256) {
+      std::array<cudaEvent_t, 8> set;
+      for (auto& e : set) EF_CUDA(cudaEventCreate(&e));
+      h->ring.push_back(set);
+    } else {
+      EF_TRY(flush_timers(h));
+    }
+  }
+  EF_CUDA(cudaEventRecord(h->ring[h->ring_used][k], h->st));
+  if (k == 7) h->ring_used++;
+  return EF_OK;
 }
 
 static int run_stage(ef_solver* h, const double* U, const double* U0, double* Uout, StageParams sp) {
   const int D = h->dim;
   const bool want_tau = sp.tau_mode == ef::TAU_CFL;
-  mark(h, 0);
-  mark(h, 1);  // step0 is fused into the previous stage's final kernel
-  ef::launch_viscosity(D, h->lay, h->gas, U, h->w, want_tau, h->st);
-  mark(h, 2);
-  ef::launch_mirror(h->lay, h->w, want_tau, h->st);
-  mark(h, 3);
+  EF_TRY(mark(h, 0));
+  EF_TRY(mark(h, 1));  // step0 is fused into the previous stage's final kernel
+  ef::launch_edge_visc(D, h->lay, h->gas, U, h->w, want_tau, h->st);
+  EF_TRY(mark(h, 2));
+  ef::launch_row_visc(D, h->lay, h->gas, U, h->w, want_tau, h->st);
+  EF_TRY(mark(h, 3));
   ef::launch_low_order(D, h->lay, h->gas, U, h->w, sp, h->st);
-  mark(h, 4);
+  EF_TRY(mark(h, 4));
   if (h->passes > 0) {
     ef::launch_correction(D, h->lay, h->gas, U, h->w, sp, h->st);
-    mark(h, 5);
+    EF_TRY(mark(h, 5));
     for (int p = 0; p + 1 < h->passes; ++p) ef::launch_limit_pass(D, h->lay, h->gas, U, h->w, sp, p, h->st);
-    mark(h, 6);
+    EF_TRY(mark(h, 6));
   } else {
-    mark(h, 5);
-    mark(h, 6);
+    EF_TRY(mark(h, 5));
+    EF_TRY(mark(h, 6));
   }
   ef::launch_final(D, h->lay, h->gas, U, U0, Uout, h->w, sp, h->st);
-  mark(h, 7);
+  EF_TRY(mark(h, 7));
   EF_CUDA(cudaGetLastError());
-  if (h->timing) {
-    EF_CUDA(cudaEventSynchronize(h->ev[7]));
-    for (int k = 0; k < 7; ++k) {
-      float ms = 0.f;
-      cudaEventElapsedTime(&ms, h->ev[k], h->ev[k + 1]);
-      h->phase_s[k] += ms * 1e-3;
-    }
-  }
   h->n_euler++;
   return EF_OK;
 }
@@ -620,6 +652,7 @@ int ef_enable_timers(ef_solver* h, int32_t on) {
 
 int ef_phase_times(ef_solver* h, double* s7) {
   if (!h || !s7) return fail(EF_ERR_ARG, "null argument");
+  EF_TRY(flush_timers(h));
   for (int k = 0; k < 7; ++k) s7[k] = h->phase_s[k];
   return EF_OK;
 }

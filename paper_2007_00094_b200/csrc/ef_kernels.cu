@@ -4,8 +4,9 @@
 // per-slot load is a coalesced 256-byte line and neighbour gathers of the
 // structure-of-arrays state hit L1/L2 thanks to the Cuthill-McKee numbering.
 // Phase map (reference stepper.py):
-//   k_viscosity  = step1 _k_viscosity + IndicatorAccumulator      (:407-425)
-//   k_mirror     = step2 _k_mirror + _tau_local                   (:427-434, :66-70)
+//   k_edge_visc  = step1 d_ij_low on the upper triangle, one thread per edge (:407-416)
+//   k_row_visc   = step1 IndicatorAccumulator (:417-425) + step2 _k_mirror and
+//                  _tau_local (:427-434, :66-70), one thread per row
 //   k_low_order  = step3 _k_low_order (+ tau = min(c_cfl tau_min, tau_max), :548)
 //   k_correction = step4 _k_correction (P_ij built in registers)  (:456-474)
 //   k_limit_pass = step5 _k_limited_update, non-final pass        (:476-491)
@@ -78,55 +79,88 @@ __global__ void k_nodal(Layout m, Gas g, const double* __restrict__ U, Work w, i
   w.phi[i] = p;
 }
 
-// ---------------------------------------------------------------- step1
+// ---------------------------------------------------------------- step1a
+// One thread per upper edge (global id of the column above the row's, i.e. a
+// slot after the diagonal; stepper.py:211, 415).  The edge list holds SELL
+// positions in ascending order, so a warp reads 32 consecutive positions of
+// one slot row (coalesced) and the row / slot are recovered from the position.
 template <int D>
-__global__ void __launch_bounds__(TPB) k_viscosity(Layout m, Gas g, const double* __restrict__ U,
+__global__ void __launch_bounds__(TPB) k_edge_visc(Layout m, Gas g, const double* __restrict__ U,
                                                    Work w, int reset_tau) {
   constexpr int NV = D + 2;
-  const int64_t i = blockIdx.x * (int64_t)TPB + threadIdx.x;
-  if (reset_tau && i == 0) *w.tau_min_bits = 0x7ff0000000000000ULL;
-  if (i >= m.n_local) return;
-  const int64_t NP = m.NP;
-  const int L = m.L;
-  const int64_t NPL = NP * L;
-  double Ui[NV];
+  const int64_t e = blockIdx.x * (int64_t)TPB + threadIdx.x;
+  if (reset_tau && e == 0) *w.tau_min_bits = 0x7ff0000000000000ULL;
+  if (e >= m.n_edges) return;
+  const int64_t p = m.edges[e];
+  const int64_t slab = 32 * (int64_t)m.L;
+  const int64_t i = (p / slab) * 32 + (p & 31);
+  const int64_t j = m.col[p];
+  const int64_t NP = m.NP, NPL = NP * m.L;
+  double Ui[NV], Uj[NV], cc[D], ct[D];
   load_node<NV>(U, NP, i, Ui);
-  const int card = m.card[i], dg = m.diag[i];
-  const bool owned = i < m.n_owned;
-  bool bad = false;
-  double fi[NV][D];
-  flux<D>(Ui, g, fi);
-  const double eor_i = w.eor[i];
-  double ep[NV];
-  if (owned) {  // IndicatorAccumulator.reset, indicator.py:35-43
-    const double re = Ui[0] * internal_energy<D>(Ui);
-    if (re <= 0.0) bad = true;
-    const double scale = ef_pow(re, g.neg_g_gp1_inv) * g.gp1_inv;  // physics.py:143
-    ep[0] = scale * Ui[D + 1];
+  load_node<NV>(U, NP, j, Uj);
 #pragma unroll
-    for (int a = 0; a < D; ++a) ep[1 + a] = (-scale) * Ui[1 + a];
-    ep[D + 1] = scale * Ui[0];
+  for (int a = 0; a < D; ++a) {
+    cc[a] = m.c[a * NPL + p];
+    ct[a] = m.cT[a * NPL + p];
   }
-  double A = 0.0, B[NV];
+  bool bad = false;
+  w.d[p] = d_ij_low<D>(Ui, Uj, cc, ct, g, bad);
+  if (bad) atomicOr(w.err, ERR_PROJECT);
+}
+
+// ---------------------------------------------------------------- step1b + step2
+__device__ __forceinline__ double warp_min(double v) {
 #pragma unroll
-  for (int k = 0; k < NV; ++k) B[k] = 0.0;
-  const int64_t base = sidx(i, 0, L);
-  for (int s = 0; s < card; ++s) {
-    if (s == dg) continue;  // j == i contributes exact zeros
-    const int64_t p = base + (int64_t)s * 32;
-    const int64_t j = m.col[p];
-    double Uj[NV];
-    load_node<NV>(U, NP, j, Uj);
-    double cc[D];
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Per owned row, in slot order: the entropy-viscosity indicator
+// (IndicatorAccumulator.reset/accumulate/result, indicator.py:35-73), the
+// mirror of the lower triangle with d_ii = -(numpy pairwise row sum)
+// (_k_mirror, stepper.py:427-434) and the CFL bound (_tau_local, :66-70).
+template <int D>
+__global__ void __launch_bounds__(TPB) k_row_visc(Layout m, Gas g, const double* __restrict__ U,
+                                                  Work w, int want_tau) {
+  constexpr int NV = D + 2;
+  const int64_t i = blockIdx.x * (int64_t)TPB + threadIdx.x;
+  double cand = __longlong_as_double(0x7ff0000000000000LL);
+  bool bad = false;
+  if (i < m.n_owned) {
+    const int64_t NP = m.NP;
+    const int L = m.L;
+    const int64_t NPL = NP * L;
+    const int card = m.card[i], dg = m.diag[i];
+    const int64_t base = sidx(i, 0, L);
+    double Ui[NV];
+    load_node<NV>(U, NP, i, Ui);
+    double fi[NV][D];
+    flux<D>(Ui, g, fi);
+    const double eor_i = w.eor[i];
+    double ep[NV];
+    {
+      const double re = Ui[0] * internal_energy<D>(Ui);
+      if (re <= 0.0) bad = true;
+      const double scale = ef_pow(re, g.neg_g_gp1_inv) * g.gp1_inv;  // physics.py:143
+      ep[0] = scale * Ui[D + 1];
 #pragma unroll
-    for (int a = 0; a < D; ++a) cc[a] = m.c[a * NPL + p];
-    if (s > dg) {  // upper triangle by global id (stepper.py:211, 415)
-      double ct[D];
-#pragma unroll
-      for (int a = 0; a < D; ++a) ct[a] = m.cT[a * NPL + p];
-      w.d[p] = d_ij_low<D>(Ui, Uj, cc, ct, g, bad);
+      for (int a = 0; a < D; ++a) ep[1 + a] = (-scale) * Ui[1 + a];
+      ep[D + 1] = scale * Ui[0];
     }
-    if (owned) {  // IndicatorAccumulator.accumulate, indicator.py:45-61
+    double A = 0.0, B[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) B[k] = 0.0;
+    double* __restrict__ d = w.d;
+    auto v = [&](int s) -> double {
+      if (s == dg || s >= card) return 0.0;  // j == i and pads add exact zeros
+      const int64_t p = base + (int64_t)s * 32;
+      const int64_t j = m.col[p];
+      double Uj[NV];
+      load_node<NV>(U, NP, j, Uj);
+      double cc[D];
+#pragma unroll
+      for (int a = 0; a < D; ++a) cc[a] = m.c[a * NPL + p];
       double mc = 0.0;
 #pragma unroll
       for (int a = 0; a < D; ++a) mc = mc + Uj[1 + a] * cc[a];
@@ -140,50 +174,11 @@ __global__ void __launch_bounds__(TPB) k_viscosity(Layout m, Gas g, const double
         for (int a = 0; a < D; ++a) t = t + (fj[k][a] - fi[k][a]) * cc[a];
         B[k] = B[k] + t;
       }
-    }
-  }
-  if (owned) {  // IndicatorAccumulator.result, indicator.py:63-73
-    double eb = 0.0;
-#pragma unroll
-    for (int k = 0; k < NV; ++k) eb = eb + ep[k] * B[k];
-    const double numer = fabs((A - eb) + (eor_i * B[0]));
-    double wb = 0.0;
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      const double wk = (k == 0) ? fabs(ep[0] - eor_i) : fabs(ep[k]);
-      wb = wb + wk * fabs(B[k]);
-    }
-    const double denom = fabs(A) + wb;
-    const double safe = denom > kDenomFloor ? denom : 1.0;
-    const double al = npclip(numer / safe, 0.0, 1.0);
-    w.alpha[i] = denom > kDenomFloor ? al : 0.0;
-  }
-  if (bad) atomicOr(w.err, ERR_PROJECT);
-}
-
-// ---------------------------------------------------------------- step2
-__device__ __forceinline__ double warp_min(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-
-__global__ void __launch_bounds__(TPB) k_mirror(Layout m, Work w, int want_tau) {
-  const int64_t i = blockIdx.x * (int64_t)TPB + threadIdx.x;
-  double cand = __longlong_as_double(0x7ff0000000000000LL);
-  if (i < m.n_owned) {
-    const int L = m.L;
-    const int card = m.card[i], dg = m.diag[i];
-    const int64_t base = sidx(i, 0, L);
-    double* __restrict__ d = w.d;
-    auto v = [&](int s) -> double {
-      const int64_t p = base + (int64_t)s * 32;
-      if (s < dg) {  // lower: take d_ji from the transpose position
-        const double x = d[sidx(m.col[p], m.tslot[p], L)];
+      if (s < dg) {  // lower: d_ij = d_ji from the transpose position
+        const double x = d[sidx(j, m.tslot[p], L)];
         d[p] = x;
         return x;
       }
-      if (s == dg || s >= card) return 0.0;
       return d[p];
     };
     double res;
@@ -205,7 +200,23 @@ __global__ void __launch_bounds__(TPB) k_mirror(Layout m, Work w, int want_tau) 
     const double dii = -res;
     d[base + (int64_t)dg * 32] = dii;
     if (want_tau && dii < 0.0) cand = m.m_i[i] / (-2.0 * dii);
+    // IndicatorAccumulator.result, indicator.py:63-73
+    double eb = 0.0;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) eb = eb + ep[k] * B[k];
+    const double numer = fabs((A - eb) + (eor_i * B[0]));
+    double wb = 0.0;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const double wk = (k == 0) ? fabs(ep[0] - eor_i) : fabs(ep[k]);
+      wb = wb + wk * fabs(B[k]);
+    }
+    const double denom = fabs(A) + wb;
+    const double safe = denom > kDenomFloor ? denom : 1.0;
+    const double al = npclip(numer / safe, 0.0, 1.0);
+    w.alpha[i] = denom > kDenomFloor ? al : 0.0;
   }
+  if (bad) atomicOr(w.err, ERR_PROJECT);
   if (!want_tau) return;
   __shared__ double red[TPB / 32];
   cand = warp_min(cand);
@@ -521,12 +532,13 @@ void launch_nodal(int dim, const Layout& m, const Gas& g, const double* U, Work 
   if (hi <= lo) return;
   EF_DISPATCH(dim, k_nodal, grid_for(hi - lo), m, g, U, w, lo, hi);
 }
-void launch_viscosity(int dim, const Layout& m, const Gas& g, const double* U, Work w,
+void launch_edge_visc(int dim, const Layout& m, const Gas& g, const double* U, Work w,
                       bool reset_tau, cudaStream_t st) {
-  EF_DISPATCH(dim, k_viscosity, grid_for(m.n_local > 0 ? m.n_local : 1), m, g, U, w, reset_tau ? 1 : 0);
+  EF_DISPATCH(dim, k_edge_visc, grid_for(m.n_edges > 0 ? m.n_edges : 1), m, g, U, w, reset_tau ? 1 : 0);
 }
-void launch_mirror(const Layout& m, Work w, bool want_tau, cudaStream_t st) {
-  k_mirror<<<grid_for(m.n_owned > 0 ? m.n_owned : 1), TPB, 0, st>>>(m, w, want_tau ? 1 : 0);
+void launch_row_visc(int dim, const Layout& m, const Gas& g, const double* U, Work w,
+                     bool want_tau, cudaStream_t st) {
+  EF_DISPATCH(dim, k_row_visc, grid_for(m.n_owned > 0 ? m.n_owned : 1), m, g, U, w, want_tau ? 1 : 0);
 }
 void launch_low_order(int dim, const Layout& m, const Gas& g, const double* U, Work w,
                       StageParams sp, cudaStream_t st) {

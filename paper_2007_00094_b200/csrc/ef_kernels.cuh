@@ -39,6 +39,8 @@ struct Layout {
   const int64_t* gid;    // [NP] global CM id of each local row
   const int8_t* bc_kind; // [NP] bit0 slip, bit1 inflow
   const double* bc_n;    // [D][NP] slip normal
+  const int32_t* edges;  // [n_edges] SELL positions of the upper slots of all local rows, ascending
+  int64_t n_edges;
   double farfield[5];
 };
 
@@ -77,9 +79,12 @@ void launch_scatter_state(int dim, const Layout& m, const double* U, const int64
                           double* U_aos, cudaStream_t st);
 void launch_nodal(int dim, const Layout& m, const Gas& g, const double* U, Work w, int64_t lo,
                   int64_t hi, cudaStream_t st);
-void launch_viscosity(int dim, const Layout& m, const Gas& g, const double* U, Work w,
+// step1a: d_ij on every upper edge (one thread per edge)
+void launch_edge_visc(int dim, const Layout& m, const Gas& g, const double* U, Work w,
                       bool reset_tau, cudaStream_t st);
-void launch_mirror(const Layout& m, Work w, bool want_tau, cudaStream_t st);
+// step1b+2: per owned row, indicator alpha, mirror of d, d_ii, CFL bound
+void launch_row_visc(int dim, const Layout& m, const Gas& g, const double* U, Work w,
+                     bool want_tau, cudaStream_t st);
 void launch_low_order(int dim, const Layout& m, const Gas& g, const double* U, Work w,
                       StageParams sp, cudaStream_t st);
 void launch_correction(int dim, const Layout& m, const Gas& g, const double* U, Work w,

@@ -24,8 +24,8 @@ PHASES = ["step0", "step1", "step2", "step3", "step4", "step5", "step6"]
 # phase -> the kernel of libef_b200.so that implements it
 KERNEL_OF_PHASE = {
     "step0": "k_final (fused nodal update)",
-    "step1": "k_viscosity",
-    "step2": "k_mirror",
+    "step1": "k_edge_visc",
+    "step2": "k_row_visc",
     "step3": "k_low_order",
     "step4": "k_correction",
     "step5": "k_limit_pass",

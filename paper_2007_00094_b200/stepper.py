@@ -130,8 +130,11 @@ class Solver:
         # simulated ranks (the reference's `ranks`) do not change results; real
         # multi-GPU ranks are set up by paper_2007_00094_b200.distributed
         nranks = 1
-        dist = _lib.EfDist(int(rank), nranks, int(device), ptr(cm_perm, np.int64), None, None,
-                           None if stream is None else int(stream))
+        if stream is not None:
+            stream = int(stream)
+            if stream == 0:  # the legacy default stream (torch's default) is handle 1
+                stream = 1
+        dist = _lib.EfDist(int(rank), nranks, int(device), ptr(cm_perm, np.int64), None, None, stream)
         h = ctypes.c_void_p()
         rc = lib.ef_create(ctypes.byref(mats), ctypes.byref(prm), ctypes.byref(bcs),
                            ctypes.byref(dist), ctypes.byref(h))
