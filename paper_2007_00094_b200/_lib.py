@@ -11,7 +11,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libef_b200.so")
+LIB_PATH = os.environ.get("EF_B200_LIB") or os.path.join(_HERE, "libef_b200.so")
 
 EF_OK, EF_ERR_ARG, EF_ERR_INADMISSIBLE, EF_ERR_TAU_UNBOUNDED, EF_ERR_CUDA, EF_ERR_NCCL = range(6)
 

@@ -8,8 +8,9 @@
 //   k_row_visc   = step1 IndicatorAccumulator (:417-425) + step2 _k_mirror and
 //                  _tau_local (:427-434, :66-70), one thread per row
 //   k_low_order  = step3 _k_low_order (+ tau = min(c_cfl tau_min, tau_max), :548)
-//   k_correction = step4 _k_correction (P_ij built in registers)  (:456-474)
-//   k_limit_pass = step5 _k_limited_update, non-final pass        (:476-491)
+//   k_slot_limiter(q) = step4 (q = 0) / step5 limiter of pass q, one thread per
+//                  off-diagonal slot, P_ij rebuilt in registers   (:456-474, :485-491)
+//   k_row_update = step5 non-final limited update, one thread per row (:476-481)
 //   k_final      = step6 final pass + _k_boundary + _finish_step check
 //                  + SSP-RK3 combination + next stage's step0     (:493-504, :612-636, :399-405)
 // P_ij is never stored: every pass rebuilds it from R, U, d, alpha and m_ij in
@@ -20,6 +21,9 @@
 namespace ef {
 
 constexpr int TPB = 128;
+#ifndef EF_MINB
+#define EF_MINB 8  // resident blocks per SM requested from ptxas (64-register cap)
+#endif
 
 static inline unsigned grid_for(int64_t n) { return (unsigned)((n + TPB - 1) / TPB); }
 
@@ -63,8 +67,8 @@ template <int D>
 __device__ __forceinline__ void nodal_one(const double* Ui, const Gas& g, double& eor, double& phi) {
   const double rho = Ui[0];
   const double eps = internal_energy<D>(Ui);
-  eor = ef_pow(rho * eps, g.gp1_inv) / rho;     // stepper.py:403
-  phi = eps * ef_pow(rho, g.neg_gamma);          // stepper.py:404
+  eor = dpow(rho * eps, g.gp1_inv) / rho;     // stepper.py:403
+  phi = eps * dpow(rho, g.neg_gamma);          // stepper.py:404
 }
 
 template <int D>
@@ -85,15 +89,14 @@ __global__ void k_nodal(Layout m, Gas g, const double* __restrict__ U, Work w, i
 // positions in ascending order, so a warp reads 32 consecutive positions of
 // one slot row (coalesced) and the row / slot are recovered from the position.
 template <int D>
-__global__ void __launch_bounds__(TPB) k_edge_visc(Layout m, Gas g, const double* __restrict__ U,
+__global__ void __launch_bounds__(TPB, EF_MINB) k_edge_visc(Layout m, Gas g, const double* __restrict__ U,
                                                    Work w, int reset_tau) {
   constexpr int NV = D + 2;
   const int64_t e = blockIdx.x * (int64_t)TPB + threadIdx.x;
   if (reset_tau && e == 0) *w.tau_min_bits = 0x7ff0000000000000ULL;
   if (e >= m.n_edges) return;
   const int64_t p = m.edges[e];
-  const int64_t slab = 32 * (int64_t)m.L;
-  const int64_t i = (p / slab) * 32 + (p & 31);
+  const int64_t i = (int64_t)fdiv((uint32_t)p, m.slab) * 32 + (p & 31);
   const int64_t j = m.col[p];
   const int64_t NP = m.NP, NPL = NP * m.L;
   double Ui[NV], Uj[NV], cc[D], ct[D];
@@ -121,7 +124,7 @@ __device__ __forceinline__ double warp_min(double v) {
 // mirror of the lower triangle with d_ii = -(numpy pairwise row sum)
 // (_k_mirror, stepper.py:427-434) and the CFL bound (_tau_local, :66-70).
 template <int D>
-__global__ void __launch_bounds__(TPB) k_row_visc(Layout m, Gas g, const double* __restrict__ U,
+__global__ void __launch_bounds__(TPB, EF_MINB) k_row_visc(Layout m, Gas g, const double* __restrict__ U,
                                                   Work w, int want_tau) {
   constexpr int NV = D + 2;
   const int64_t i = blockIdx.x * (int64_t)TPB + threadIdx.x;
@@ -142,7 +145,7 @@ __global__ void __launch_bounds__(TPB) k_row_visc(Layout m, Gas g, const double*
     {
       const double re = Ui[0] * internal_energy<D>(Ui);
       if (re <= 0.0) bad = true;
-      const double scale = ef_pow(re, g.neg_g_gp1_inv) * g.gp1_inv;  // physics.py:143
+      const double scale = dpow(re, g.neg_g_gp1_inv) * g.gp1_inv;  // physics.py:143
       ep[0] = scale * Ui[D + 1];
 #pragma unroll
       for (int a = 0; a < D; ++a) ep[1 + a] = (-scale) * Ui[1 + a];
@@ -247,7 +250,7 @@ __device__ __forceinline__ double stage_tau(const Work& w, const StageParams& sp
 }
 
 template <int D>
-__global__ void __launch_bounds__(TPB) k_low_order(Layout m, Gas g, const double* __restrict__ U,
+__global__ void __launch_bounds__(TPB, EF_MINB) k_low_order(Layout m, Gas g, const double* __restrict__ U,
                                                    Work w, StageParams sp) {
   constexpr int NV = D + 2;
   const double tau = stage_tau(w, sp);
@@ -347,38 +350,39 @@ __device__ __forceinline__ void build_P(const Layout& m, const Work& w, const do
   }
 }
 
+// One thread per off-diagonal slot of an owned row: rebuild P^(q)_ij and run
+// the limiter against the row's bounds (limiter.limiter_compute per lane,
+// stepper.py:469-474 for q = 0, :485-491 for q > 0).  Lanes are independent,
+// so the data-dependent Newton iterations of one slot no longer serialise a row.
 template <int D>
-__global__ void __launch_bounds__(TPB) k_correction(Layout m, Gas g, const double* __restrict__ U,
-                                                    Work w, StageParams sp) {
+__global__ void __launch_bounds__(TPB, EF_MINB) k_slot_limiter(Layout m, Gas g, const double* __restrict__ U,
+                                                               Work w, StageParams sp, int q) {
   constexpr int NV = D + 2;
-  const int64_t i = blockIdx.x * (int64_t)TPB + threadIdx.x;
-  if (i >= m.n_owned) return;
+  const int64_t e = blockIdx.x * (int64_t)TPB + threadIdx.x;
+  if (e >= m.n_slots) return;
+  const int64_t p = m.slots[e];
+  const int64_t i = (int64_t)fdiv((uint32_t)p, m.slab) * 32 + (p & 31);
+  const int64_t j = m.col[p];
   const int64_t NP = m.NP;
-  const int L = m.L;
   const double tau = *w.tau;
-  const int card = m.card[i], dg = m.diag[i];
+  const int card = m.card[i];
   const double inv_mi = m.inv_m[i];
   const double factor = (tau * inv_mi) * (double)(card - 1);
   double Ui[NV], Ri[NV], Un[NV];
   load_node<NV>(U, NP, i, Ui);
   load_node<NV>(w.R, NP, i, Ri);
   load_node<NV>(w.Unext, NP, i, Un);
-  const double ai = w.alpha[i];
+  double P[NV];
+  build_P<D>(m, w, U, Ui, Ri, w.alpha[i], inv_mi, factor, p, j, q, P);
   const double rmin = w.bounds[i], rmax = w.bounds[NP + i], pmin = w.bounds[2 * NP + i];
-  const int64_t base = sidx(i, 0, L);
-  for (int s = 0; s < card; ++s) {
-    if (s == dg) continue;
-    const int64_t p = base + (int64_t)s * 32;
-    const int64_t j = m.col[p];
-    double P[NV];
-    build_P<D>(m, w, U, Ui, Ri, ai, inv_mi, factor, p, j, 0, P);
-    w.l[p] = limiter<D>(Un, P, rmin, rmax, pmin, sp.newton, g);
-  }
+  w.l[q * NP * m.L + p] = limiter<D>(Un, P, rmin, rmax, pmin, sp.newton, g);
 }
 
+// Non-final limited update (stepper.py:478-481): the ordered slot sum of
+// min(l_p, l_p^T) P^(p) for one row, then U_next_i += lam_i * upd.
 template <int D>
-__global__ void __launch_bounds__(TPB) k_limit_pass(Layout m, Gas g, const double* __restrict__ U,
-                                                    Work w, StageParams sp, int pass) {
+__global__ void __launch_bounds__(TPB, EF_MINB) k_row_update(Layout m, Gas g, const double* __restrict__ U,
+                                                             Work w, StageParams sp, int pass) {
   constexpr int NV = D + 2;
   const int64_t i = blockIdx.x * (int64_t)TPB + threadIdx.x;
   if (i >= m.n_owned) return;
@@ -389,10 +393,9 @@ __global__ void __launch_bounds__(TPB) k_limit_pass(Layout m, Gas g, const doubl
   const int card = m.card[i], dg = m.diag[i];
   const double inv_mi = m.inv_m[i];
   const double factor = (tau * inv_mi) * (double)(card - 1);
-  double Ui[NV], Ri[NV], Un[NV];
+  double Ui[NV], Ri[NV];
   load_node<NV>(U, NP, i, Ui);
   load_node<NV>(w.R, NP, i, Ri);
-  load_node<NV>(w.Unext, NP, i, Un);
   const double ai = w.alpha[i];
   const int64_t base = sidx(i, 0, L);
   double upd[NV];
@@ -410,23 +413,11 @@ __global__ void __launch_bounds__(TPB) k_limit_pass(Layout m, Gas g, const doubl
   }
   const double lam = m.lam[i];
 #pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    Un[k] = Un[k] + lam * upd[k];
-    w.Unext[k * NP + i] = Un[k];
-  }
-  const double rmin = w.bounds[i], rmax = w.bounds[NP + i], pmin = w.bounds[2 * NP + i];
-  for (int s = 0; s < card; ++s) {
-    if (s == dg) continue;
-    const int64_t p = base + (int64_t)s * 32;
-    const int64_t j = m.col[p];
-    double P[NV];
-    build_P<D>(m, w, U, Ui, Ri, ai, inv_mi, factor, p, j, pass + 1, P);
-    w.l[(pass + 1) * NPL + p] = limiter<D>(Un, P, rmin, rmax, pmin, sp.newton, g);
-  }
+  for (int k = 0; k < NV; ++k) w.Unext[k * NP + i] = w.Unext[k * NP + i] + lam * upd[k];
 }
 
 template <int D>
-__global__ void __launch_bounds__(TPB) k_final(Layout m, Gas g, const double* __restrict__ U,
+__global__ void __launch_bounds__(TPB, EF_MINB) k_final(Layout m, Gas g, const double* __restrict__ U,
                                                const double* __restrict__ U0, double* __restrict__ Uout,
                                                Work w, StageParams sp) {
   constexpr int NV = D + 2;
@@ -544,15 +535,15 @@ void launch_low_order(int dim, const Layout& m, const Gas& g, const double* U, W
                       StageParams sp, cudaStream_t st) {
   EF_DISPATCH(dim, k_low_order, grid_for(m.n_owned > 0 ? m.n_owned : 1), m, g, U, w, sp);
 }
-void launch_correction(int dim, const Layout& m, const Gas& g, const double* U, Work w,
-                       StageParams sp, cudaStream_t st) {
-  if (m.n_owned == 0) return;
-  EF_DISPATCH(dim, k_correction, grid_for(m.n_owned), m, g, U, w, sp);
+void launch_slot_limiter(int dim, const Layout& m, const Gas& g, const double* U, Work w,
+                         StageParams sp, int q, cudaStream_t st) {
+  if (m.n_slots == 0) return;
+  EF_DISPATCH(dim, k_slot_limiter, grid_for(m.n_slots), m, g, U, w, sp, q);
 }
-void launch_limit_pass(int dim, const Layout& m, const Gas& g, const double* U, Work w,
+void launch_row_update(int dim, const Layout& m, const Gas& g, const double* U, Work w,
                        StageParams sp, int pass, cudaStream_t st) {
   if (m.n_owned == 0) return;
-  EF_DISPATCH(dim, k_limit_pass, grid_for(m.n_owned), m, g, U, w, sp, pass);
+  EF_DISPATCH(dim, k_row_update, grid_for(m.n_owned), m, g, U, w, sp, pass);
 }
 void launch_final(int dim, const Layout& m, const Gas& g, const double* U, const double* U0,
                   double* Uout, Work w, StageParams sp, cudaStream_t st) {

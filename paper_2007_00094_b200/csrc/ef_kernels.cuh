@@ -21,6 +21,26 @@ __host__ __device__ __forceinline__ int64_t sidx(int64_t i, int s, int L) {
   return (i >> 5) * (int64_t)(32 * L) + (int64_t)s * 32 + (i & 31);
 }
 
+// Division by a runtime constant d < 2^31 for unsigned n < 2^32 (round-up
+// multiply-high method): q = (umulhi(n, mul) + n) >> shift.
+struct FastDiv {
+  uint32_t d, mul, shift;
+};
+
+inline FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f;
+  f.d = d;
+  uint32_t l = 0;
+  while ((1ull << l) < d) ++l;
+  f.shift = l;
+  f.mul = (uint32_t)((((1ull << 32) * ((1ull << l) - d)) / d) + 1);
+  return f;
+}
+
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
+  return (uint32_t)((((unsigned long long)__umulhi(n, f.mul)) + n) >> f.shift);
+}
+
 struct Layout {
   int L;            // global pad width
   int64_t NP;       // padded local rows (multiple of 32)
@@ -41,6 +61,9 @@ struct Layout {
   const double* bc_n;    // [D][NP] slip normal
   const int32_t* edges;  // [n_edges] SELL positions of the upper slots of all local rows, ascending
   int64_t n_edges;
+  const int32_t* slots;  // [n_slots] SELL positions of the off-diagonal slots of owned rows, ascending
+  int64_t n_slots;
+  FastDiv slab;          // division by 32 * L (SELL slice size)
   double farfield[5];
 };
 
@@ -87,9 +110,11 @@ void launch_row_visc(int dim, const Layout& m, const Gas& g, const double* U, Wo
                      bool want_tau, cudaStream_t st);
 void launch_low_order(int dim, const Layout& m, const Gas& g, const double* U, Work w,
                       StageParams sp, cudaStream_t st);
-void launch_correction(int dim, const Layout& m, const Gas& g, const double* U, Work w,
-                       StageParams sp, cudaStream_t st);
-void launch_limit_pass(int dim, const Layout& m, const Gas& g, const double* U, Work w,
+// steps 4-5: l_q(i, s) = limiter(U_next_i, P^(q)_ij), one thread per off-diagonal slot
+void launch_slot_limiter(int dim, const Layout& m, const Gas& g, const double* U, Work w,
+                         StageParams sp, int q, cudaStream_t st);
+// step 5: U_next_i += lam_i * sum_s min(l_p, l_p^T) P^(p), one thread per owned row
+void launch_row_update(int dim, const Layout& m, const Gas& g, const double* U, Work w,
                        StageParams sp, int pass, cudaStream_t st);
 void launch_final(int dim, const Layout& m, const Gas& g, const double* U, const double* U0,
                   double* Uout, Work w, StageParams sp, cudaStream_t st);

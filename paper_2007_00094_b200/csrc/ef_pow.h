@@ -169,36 +169,41 @@ EF_HD int ef_int_class(double y) {
   return (((int64_t)ay) & 1) ? 2 : 1;
 }
 
-/* Full IEEE/C99 pow semantics (as numpy.power on float64). */
+/* Full IEEE/C99 pow semantics (as numpy.power on float64).  The core is
+ * evaluated at one call site (|x|, sign applied afterwards) to keep the
+ * inlined device code small. */
 EF_HD double ef_pow(double x, double y) {
   const double inf = ef_from_bits(0x7ff0000000000000ULL);
-  if (x > 0.0 && x < inf && y > -inf && y < inf) {
-    if (y == 0.0 || x == 1.0) return 1.0;
-    return ef_pow_pos(x, y);
-  }
-  if (y == 0.0) return 1.0;
-  if (x == 1.0) return 1.0;
-  if (x != x || y != y) return x + y;
   double ax = x < 0.0 ? -x : x;
-  if (y == inf || y == -inf) {
-    if (ax == 1.0) return 1.0;
-    return ((ax < 1.0) == (y < 0.0)) ? inf : 0.0;
+  int sign_flip = 0;
+  int special = !(x > 0.0 && x < inf && y > -inf && y < inf);
+  double r;
+  if (special) {
+    if (y == 0.0 || x == 1.0) return 1.0;
+    if (x != x || y != y) return x + y;
+    if (y == inf || y == -inf) {
+      if (ax == 1.0) return 1.0;
+      return ((ax < 1.0) == (y < 0.0)) ? inf : 0.0;
+    }
+    const int ic = ef_int_class(y);
+    const int neg = (ef_bits(x) >> 63) != 0;
+    if (x == 0.0) {
+      const int odd_neg = neg && ic == 2;
+      if (y < 0.0) return odd_neg ? -inf : inf;
+      return odd_neg ? -0.0 : 0.0;
+    }
+    if (ax == inf) {
+      r = y < 0.0 ? 0.0 : inf;
+      return (neg && ic == 2) ? -r : r;
+    }
+    /* finite x < 0 */
+    if (ic == 0) return ef_from_bits(0x7ff8000000000000ULL);
+    sign_flip = ic == 2;
+  } else if (y == 0.0 || x == 1.0) {
+    return 1.0;
   }
-  int ic = ef_int_class(y);
-  int neg = (ef_bits(x) >> 63) != 0;
-  if (x == 0.0) {
-    int odd_neg = neg && ic == 2;
-    if (y < 0.0) return odd_neg ? -inf : inf;
-    return odd_neg ? -0.0 : 0.0;
-  }
-  if (ax == inf) {
-    double r = y < 0.0 ? 0.0 : inf;
-    return (neg && ic == 2) ? -r : r;
-  }
-  /* finite x < 0 */
-  if (ic == 0) return ef_from_bits(0x7ff8000000000000ULL);
-  double r = ef_pow_pos(ax, y);
-  return ic == 2 ? -r : r;
+  r = ef_pow_pos(ax, y);
+  return sign_flip ? -r : r;
 }
 
 #endif /* EF_POW_H */
