@@ -279,15 +279,6 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_params* prm, con
         if (i >= n_local) continue;
         if (s > diag[i] && s < card[i]) edges.push_back((int32_t)ef::sidx(i, s, (int)L));
       }
-  // off-diagonal slots of owned rows (slot-parallel limiter)
-  std::vector<int32_t> slots;
-  for (int64_t sl = 0; sl < NP / 32; ++sl)
-    for (int s = 0; s < L; ++s)
-      for (int ln = 0; ln < 32; ++ln) {
-        const int64_t i = sl * 32 + ln;
-        if (i >= n_owned) continue;
-        if (s != diag[i] && s < card[i]) slots.push_back((int32_t)ef::sidx(i, s, (int)L));
-      }
   // boundary data (stepper.py:258-267): owned rows only
   std::vector<int8_t> bc_kind(NP, 0);
   std::vector<double> bc_n((size_t)D * NP, 0.0);
@@ -343,10 +334,6 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_params* prm, con
   EF_TRY(upload(h, &d_edges, edges));
   m.edges = d_edges;
   m.n_edges = (int64_t)edges.size();
-  int32_t* d_slots;
-  EF_TRY(upload(h, &d_slots, slots));
-  m.slots = d_slots;
-  m.n_slots = (int64_t)slots.size();
   m.slab = ef::make_fastdiv((uint32_t)(32 * L));
   m.col = d_col;
   m.tslot = d_tslot;
@@ -543,12 +530,9 @@ static int run_stage(ef_solver* h, const double* U, const double* U0, double* Uo
   ef::launch_low_order(D, h->lay, h->gas, U, h->w, sp, h->st);
   EF_TRY(mark(h, 4));
   if (h->passes > 0) {
-    ef::launch_slot_limiter(D, h->lay, h->gas, U, h->w, sp, 0, h->st);
+    ef::launch_limiter0(D, h->lay, h->gas, U, h->w, sp, h->st);
     EF_TRY(mark(h, 5));
-    for (int p = 0; p + 1 < h->passes; ++p) {
-      ef::launch_row_update(D, h->lay, h->gas, U, h->w, sp, p, h->st);
-      ef::launch_slot_limiter(D, h->lay, h->gas, U, h->w, sp, p + 1, h->st);
-    }
+    for (int p = 0; p + 1 < h->passes; ++p) ef::launch_pass(D, h->lay, h->gas, U, h->w, sp, p, h->st);
     EF_TRY(mark(h, 6));
   } else {
     EF_TRY(mark(h, 5));

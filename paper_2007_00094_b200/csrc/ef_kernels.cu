@@ -1,18 +1,20 @@
 // ef_kernels.cu — the sm_100a kernels of one forward-Euler stage.
 //
-// One thread owns one row (node); a warp owns one 32-row SELL slice, so every
-// per-slot load is a coalesced 256-byte line and neighbour gathers of the
-// structure-of-arrays state hit L1/L2 thanks to the Cuthill-McKee numbering.
+// Per-slot data is SELL-32 (slot-major inside 32-row slices) and per-node data
+// structure-of-arrays, so slot loads of consecutive rows coalesce and
+// neighbour gathers hit L1/L2 thanks to the Cuthill-McKee numbering.
 // Phase map (reference stepper.py):
-//   k_edge_visc  = step1 d_ij_low on the upper triangle, one thread per edge (:407-416)
-//   k_row_visc   = step1 IndicatorAccumulator (:417-425) + step2 _k_mirror and
-//                  _tau_local (:427-434, :66-70), one thread per row
-//   k_low_order  = step3 _k_low_order (+ tau = min(c_cfl tau_min, tau_max), :548)
-//   k_slot_limiter(q) = step4 (q = 0) / step5 limiter of pass q, one thread per
-//                  off-diagonal slot, P_ij rebuilt in registers   (:456-474, :485-491)
-//   k_row_update = step5 non-final limited update, one thread per row (:476-481)
-//   k_final      = step6 final pass + _k_boundary + _finish_step check
-//                  + SSP-RK3 combination + next stage's step0     (:493-504, :612-636, :399-405)
+//   k_edge_visc    = step1 d_ij_low on the upper triangle, one thread per edge (:407-416)
+//   k_row_visc     = step1 IndicatorAccumulator (:417-425) + step2 _k_mirror and
+//                    _tau_local (:427-434, :66-70)
+//   k_low_order    = step3 _k_low_order (+ tau = min(c_cfl tau_min, tau_max), :548)
+//   k_correction   = step4 _k_correction: P_ij rebuilt in registers + limiter (:456-474)
+//   k_limit_pass   = step5 non-final limited update + the next pass's limiter (:476-491)
+//   k_final        = step6 final pass + _k_boundary + _finish_step check
+//                    + SSP-RK3 combination + next stage's step0 (:493-504, :612-636, :399-405)
+// k_edge_visc is one thread per edge; the others one thread per owned row.
+// (A row-group variant -- G lanes per row, ordered sums from shared memory --
+// measured 40% slower on C2 and was dropped.)
 // P_ij is never stored: every pass rebuilds it from R, U, d, alpha and m_ij in
 // the same operation order (including the (1 - min l) rescales of earlier
 // passes), which is bit-identical and saves 2*nvar doubles per slot per pass.
@@ -350,39 +352,38 @@ __device__ __forceinline__ void build_P(const Layout& m, const Work& w, const do
   }
 }
 
-// One thread per off-diagonal slot of an owned row: rebuild P^(q)_ij and run
-// the limiter against the row's bounds (limiter.limiter_compute per lane,
-// stepper.py:469-474 for q = 0, :485-491 for q > 0).  Lanes are independent,
-// so the data-dependent Newton iterations of one slot no longer serialise a row.
 template <int D>
-__global__ void __launch_bounds__(TPB, EF_MINB) k_slot_limiter(Layout m, Gas g, const double* __restrict__ U,
-                                                               Work w, StageParams sp, int q) {
+__global__ void __launch_bounds__(TPB, EF_MINB) k_correction(Layout m, Gas g, const double* __restrict__ U,
+                                                    Work w, StageParams sp) {
   constexpr int NV = D + 2;
-  const int64_t e = blockIdx.x * (int64_t)TPB + threadIdx.x;
-  if (e >= m.n_slots) return;
-  const int64_t p = m.slots[e];
-  const int64_t i = (int64_t)fdiv((uint32_t)p, m.slab) * 32 + (p & 31);
-  const int64_t j = m.col[p];
+  const int64_t i = blockIdx.x * (int64_t)TPB + threadIdx.x;
+  if (i >= m.n_owned) return;
   const int64_t NP = m.NP;
+  const int L = m.L;
   const double tau = *w.tau;
-  const int card = m.card[i];
+  const int card = m.card[i], dg = m.diag[i];
   const double inv_mi = m.inv_m[i];
   const double factor = (tau * inv_mi) * (double)(card - 1);
   double Ui[NV], Ri[NV], Un[NV];
   load_node<NV>(U, NP, i, Ui);
   load_node<NV>(w.R, NP, i, Ri);
   load_node<NV>(w.Unext, NP, i, Un);
-  double P[NV];
-  build_P<D>(m, w, U, Ui, Ri, w.alpha[i], inv_mi, factor, p, j, q, P);
+  const double ai = w.alpha[i];
   const double rmin = w.bounds[i], rmax = w.bounds[NP + i], pmin = w.bounds[2 * NP + i];
-  w.l[q * NP * m.L + p] = limiter<D>(Un, P, rmin, rmax, pmin, sp.newton, g);
+  const int64_t base = sidx(i, 0, L);
+  for (int s = 0; s < card; ++s) {
+    if (s == dg) continue;
+    const int64_t p = base + (int64_t)s * 32;
+    const int64_t j = m.col[p];
+    double P[NV];
+    build_P<D>(m, w, U, Ui, Ri, ai, inv_mi, factor, p, j, 0, P);
+    w.l[p] = limiter<D>(Un, P, rmin, rmax, pmin, sp.newton, g);
+  }
 }
 
-// Non-final limited update (stepper.py:478-481): the ordered slot sum of
-// min(l_p, l_p^T) P^(p) for one row, then U_next_i += lam_i * upd.
 template <int D>
-__global__ void __launch_bounds__(TPB, EF_MINB) k_row_update(Layout m, Gas g, const double* __restrict__ U,
-                                                             Work w, StageParams sp, int pass) {
+__global__ void __launch_bounds__(TPB, EF_MINB) k_limit_pass(Layout m, Gas g, const double* __restrict__ U,
+                                                    Work w, StageParams sp, int pass) {
   constexpr int NV = D + 2;
   const int64_t i = blockIdx.x * (int64_t)TPB + threadIdx.x;
   if (i >= m.n_owned) return;
@@ -393,9 +394,10 @@ __global__ void __launch_bounds__(TPB, EF_MINB) k_row_update(Layout m, Gas g, co
   const int card = m.card[i], dg = m.diag[i];
   const double inv_mi = m.inv_m[i];
   const double factor = (tau * inv_mi) * (double)(card - 1);
-  double Ui[NV], Ri[NV];
+  double Ui[NV], Ri[NV], Un[NV];
   load_node<NV>(U, NP, i, Ui);
   load_node<NV>(w.R, NP, i, Ri);
+  load_node<NV>(w.Unext, NP, i, Un);
   const double ai = w.alpha[i];
   const int64_t base = sidx(i, 0, L);
   double upd[NV];
@@ -413,7 +415,19 @@ __global__ void __launch_bounds__(TPB, EF_MINB) k_row_update(Layout m, Gas g, co
   }
   const double lam = m.lam[i];
 #pragma unroll
-  for (int k = 0; k < NV; ++k) w.Unext[k * NP + i] = w.Unext[k * NP + i] + lam * upd[k];
+  for (int k = 0; k < NV; ++k) {
+    Un[k] = Un[k] + lam * upd[k];
+    w.Unext[k * NP + i] = Un[k];
+  }
+  const double rmin = w.bounds[i], rmax = w.bounds[NP + i], pmin = w.bounds[2 * NP + i];
+  for (int s = 0; s < card; ++s) {
+    if (s == dg) continue;
+    const int64_t p = base + (int64_t)s * 32;
+    const int64_t j = m.col[p];
+    double P[NV];
+    build_P<D>(m, w, U, Ui, Ri, ai, inv_mi, factor, p, j, pass + 1, P);
+    w.l[(pass + 1) * NPL + p] = limiter<D>(Un, P, rmin, rmax, pmin, sp.newton, g);
+  }
 }
 
 template <int D>
@@ -535,15 +549,15 @@ void launch_low_order(int dim, const Layout& m, const Gas& g, const double* U, W
                       StageParams sp, cudaStream_t st) {
   EF_DISPATCH(dim, k_low_order, grid_for(m.n_owned > 0 ? m.n_owned : 1), m, g, U, w, sp);
 }
-void launch_slot_limiter(int dim, const Layout& m, const Gas& g, const double* U, Work w,
-                         StageParams sp, int q, cudaStream_t st) {
-  if (m.n_slots == 0) return;
-  EF_DISPATCH(dim, k_slot_limiter, grid_for(m.n_slots), m, g, U, w, sp, q);
-}
-void launch_row_update(int dim, const Layout& m, const Gas& g, const double* U, Work w,
-                       StageParams sp, int pass, cudaStream_t st) {
+void launch_limiter0(int dim, const Layout& m, const Gas& g, const double* U, Work w,
+                     StageParams sp, cudaStream_t st) {
   if (m.n_owned == 0) return;
-  EF_DISPATCH(dim, k_row_update, grid_for(m.n_owned), m, g, U, w, sp, pass);
+  EF_DISPATCH(dim, k_correction, grid_for(m.n_owned), m, g, U, w, sp);
+}
+void launch_pass(int dim, const Layout& m, const Gas& g, const double* U, Work w,
+                 StageParams sp, int pass, cudaStream_t st) {
+  if (m.n_owned == 0) return;
+  EF_DISPATCH(dim, k_limit_pass, grid_for(m.n_owned), m, g, U, w, sp, pass);
 }
 void launch_final(int dim, const Layout& m, const Gas& g, const double* U, const double* U0,
                   double* Uout, Work w, StageParams sp, cudaStream_t st) {

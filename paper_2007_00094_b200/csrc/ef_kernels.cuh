@@ -61,8 +61,6 @@ struct Layout {
   const double* bc_n;    // [D][NP] slip normal
   const int32_t* edges;  // [n_edges] SELL positions of the upper slots of all local rows, ascending
   int64_t n_edges;
-  const int32_t* slots;  // [n_slots] SELL positions of the off-diagonal slots of owned rows, ascending
-  int64_t n_slots;
   FastDiv slab;          // division by 32 * L (SELL slice size)
   double farfield[5];
 };
@@ -110,12 +108,12 @@ void launch_row_visc(int dim, const Layout& m, const Gas& g, const double* U, Wo
                      bool want_tau, cudaStream_t st);
 void launch_low_order(int dim, const Layout& m, const Gas& g, const double* U, Work w,
                       StageParams sp, cudaStream_t st);
-// steps 4-5: l_q(i, s) = limiter(U_next_i, P^(q)_ij), one thread per off-diagonal slot
-void launch_slot_limiter(int dim, const Layout& m, const Gas& g, const double* U, Work w,
-                         StageParams sp, int q, cudaStream_t st);
-// step 5: U_next_i += lam_i * sum_s min(l_p, l_p^T) P^(p), one thread per owned row
-void launch_row_update(int dim, const Layout& m, const Gas& g, const double* U, Work w,
-                       StageParams sp, int pass, cudaStream_t st);
+// step4: l_0(i, s) = limiter(U^L_i, P^(0)_ij)
+void launch_limiter0(int dim, const Layout& m, const Gas& g, const double* U, Work w,
+                     StageParams sp, cudaStream_t st);
+// step5: non-final pass p (row update) fused with the limiter of pass p + 1
+void launch_pass(int dim, const Layout& m, const Gas& g, const double* U, Work w,
+                 StageParams sp, int pass, cudaStream_t st);
 void launch_final(int dim, const Layout& m, const Gas& g, const double* U, const double* U0,
                   double* Uout, Work w, StageParams sp, cudaStream_t st);
 void launch_pow(const double* x, double y, double* out, int64_t n, cudaStream_t st);
