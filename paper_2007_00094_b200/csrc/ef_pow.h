@@ -12,13 +12,15 @@
  * identical bits.  The host build is exported as `ef_pow_host` and installed
  * into the reference through `set_power_function` by the parity harness.
  *
- * Algorithm (own design, ~0.6 ulp max error measured against mpmath):
+ * Algorithm (own design, < 1.1 ulp max error measured against mpmath):
  *   x = 2^e * m, m in [sqrt(1/2), sqrt(2));  f = m - 1 (exact)
- *   log(m) = 2 atanh(s), s = f / (2 + f)  -- s carried as a double-double
+ *   log(m) = 2 atanh(s), s = f / (2 + f)  -- s carried as a double-double,
+ *     1/(2+f) by a division-free Newton iteration
  *   log(x) = e*ln2 + log(m)  as a double-double (hi, lo)
  *   z = y * log(x) as a double-double;  exp(z) = 2^k * exp(r),
  *   |r| <= ln2/2, exp(r) by a degree-14 Taylor polynomial.
- * No tables (divergent table lookups serialise on the GPU).
+ * Polynomials use Estrin's scheme (short dependency chains: the GPU kernels
+ * are latency-bound).  No tables (divergent lookups serialise on the GPU).
  *
  * Compiles as C99 (oracle) and as CUDA C++ (kernels, host library).
  */
@@ -85,23 +87,29 @@ EF_HD void ef_log_dd(double x, double* out_hi, double* out_lo) {
   double f = m - 1.0;               /* exact (Sterbenz) */
   double t_hi = 2.0 + f;
   double t_lo = (2.0 - t_hi) + f;   /* exact: |2| >= |f| */
-  double rt = 1.0 / t_hi;
+  /* 1 / t_hi without a division: quadratic Chebyshev guess on
+   * [2 - (1 - sqrt(1/2)), 1 + sqrt(2)] (rel. err 1.7e-3), then three Newton
+   * steps (2.7e-6, 7.5e-12, 5.6e-23).  Deterministic on host and device. */
+  double rt = ef_fma(ef_fma(0x1.deab9f5bac12fp-4, t_hi, -0x1.71e431e019c40p-1), t_hi, 0x1.7a4e362d364a6p+0);
+  rt = ef_fma(rt, ef_fma(-t_hi, rt, 1.0), rt);
+  rt = ef_fma(rt, ef_fma(-t_hi, rt, 1.0), rt);
+  rt = ef_fma(rt, ef_fma(-t_hi, rt, 1.0), rt);
   double s = f * rt;
   double r = ef_fma(-s, t_hi, f);
   r = r - s * t_lo;
   double s_lo = r * rt;             /* s + s_lo = f / (2 + f) to ~2^-104 */
   double z = s * s;
-  double p = 0x1.642c8590b2164p-4;  /* 2/23 */
-  p = ef_fma(p, z, 0x1.8618618618618p-4); /* 2/21 */
-  p = ef_fma(p, z, 0x1.af286bca1af28p-4); /* 2/19 */
-  p = ef_fma(p, z, 0x1.e1e1e1e1e1e1ep-4); /* 2/17 */
-  p = ef_fma(p, z, 0x1.1111111111111p-3); /* 2/15 */
-  p = ef_fma(p, z, 0x1.3b13b13b13b14p-3); /* 2/13 */
-  p = ef_fma(p, z, 0x1.745d1745d1746p-3); /* 2/11 */
-  p = ef_fma(p, z, 0x1.c71c71c71c71cp-3); /* 2/9 */
-  p = ef_fma(p, z, 0x1.2492492492492p-2); /* 2/7 */
-  p = ef_fma(p, z, 0x1.999999999999ap-2); /* 2/5 */
-  p = ef_fma(p, z, 0x1.5555555555555p-1); /* 2/3 */
+  /* 2 atanh(s) / s - 2 = sum_{k>=1} 2 z^k / (2k+1): Estrin on c_k = 2/(2k+3) */
+  double z2 = z * z, z4 = z2 * z2, z8 = z4 * z4;
+  double p01 = ef_fma(0x1.999999999999ap-2, z, 0x1.5555555555555p-1);  /* 2/5, 2/3 */
+  double p23 = ef_fma(0x1.c71c71c71c71cp-3, z, 0x1.2492492492492p-2);  /* 2/9, 2/7 */
+  double p45 = ef_fma(0x1.3b13b13b13b14p-3, z, 0x1.745d1745d1746p-3);  /* 2/13, 2/11 */
+  double p67 = ef_fma(0x1.e1e1e1e1e1e1ep-4, z, 0x1.1111111111111p-3);  /* 2/17, 2/15 */
+  double p89 = ef_fma(0x1.8618618618618p-4, z, 0x1.af286bca1af28p-4);  /* 2/21, 2/19 */
+  double q0 = ef_fma(p23, z2, p01);
+  double q1 = ef_fma(p67, z2, p45);
+  double q2 = ef_fma(0x1.642c8590b2164p-4, z2, p89);                   /* 2/23 */
+  double p = ef_fma(q2, z8, ef_fma(q1, z4, q0));
   double sz = s * z;
   double tail = ef_fma(sz, p, (2.0 * z) * s_lo);
   double hi0 = 2.0 * s;                   /* exact */
@@ -125,21 +133,21 @@ EF_HD double ef_exp_dd(double zh, double zl) {
   double r = ef_fma(-kd, EF_LN2_HI, zh);  /* exact (Sterbenz) */
   r = ef_fma(-kd, EF_LN2_LO, r);
   r = r + zl;
-  double q = 0x1.93974a8c07c9dp-37;       /* 1/14! */
-  q = ef_fma(q, r, 0x1.6124613a86d09p-33); /* 1/13! */
-  q = ef_fma(q, r, 0x1.1eed8eff8d898p-29); /* 1/12! */
-  q = ef_fma(q, r, 0x1.ae64567f544e4p-26); /* 1/11! */
-  q = ef_fma(q, r, 0x1.27e4fb7789f5cp-22); /* 1/10! */
-  q = ef_fma(q, r, 0x1.71de3a556c734p-19); /* 1/9! */
-  q = ef_fma(q, r, 0x1.a01a01a01a01ap-16); /* 1/8! */
-  q = ef_fma(q, r, 0x1.a01a01a01a01ap-13); /* 1/7! */
-  q = ef_fma(q, r, 0x1.6c16c16c16c17p-10); /* 1/6! */
-  q = ef_fma(q, r, 0x1.1111111111111p-7);  /* 1/5! */
-  q = ef_fma(q, r, 0x1.5555555555555p-5);  /* 1/4! */
-  q = ef_fma(q, r, 0x1.5555555555555p-3);  /* 1/3! */
-  q = ef_fma(q, r, 0.5);
-  double em1 = ef_fma(r * r, q, r);
-  double res = 1.0 + em1;
+  /* exp(r) - 1 - r = r^2 * Q(r), Q = sum_{k=2}^{14} r^(k-2) / k!, Estrin */
+  double r2 = r * r, r4 = r2 * r2, r8 = r4 * r4;
+  double a0 = ef_fma(0x1.5555555555555p-3, r, 0.5);                    /* 1/3!, 1/2! */
+  double a1 = ef_fma(0x1.1111111111111p-7, r, 0x1.5555555555555p-5);  /* 1/5!, 1/4! */
+  double a2 = ef_fma(0x1.a01a01a01a01ap-13, r, 0x1.6c16c16c16c17p-10); /* 1/7!, 1/6! */
+  double a3 = ef_fma(0x1.71de3a556c734p-19, r, 0x1.a01a01a01a01ap-16); /* 1/9!, 1/8! */
+  double a4 = ef_fma(0x1.ae64567f544e4p-26, r, 0x1.27e4fb7789f5cp-22); /* 1/11!, 1/10! */
+  double a5 = ef_fma(0x1.6124613a86d09p-33, r, 0x1.1eed8eff8d898p-29); /* 1/13!, 1/12! */
+  double b0 = ef_fma(a1, r2, a0);
+  double b1 = ef_fma(a3, r2, a2);
+  double b2 = ef_fma(a5, r2, a4);
+  double q = ef_fma(ef_fma(0x1.93974a8c07c9dp-37, r4, b2), r8, ef_fma(b1, r4, b0)); /* 1/14! */
+  double s1 = 1.0 + r;                    /* Fast2Sum: |1| >= |r| */
+  double e1 = (1.0 - s1) + r;
+  double res = s1 + ef_fma(r2, q, e1);    /* 1 + r + r^2 Q with one final rounding of note */
   if (k >= -1020 && k <= 1020) {
     return res * ef_from_bits((uint64_t)(k + 1023) << 52);
   }
