@@ -15,9 +15,9 @@
 // k_edge_visc is one thread per edge; the others one thread per owned row.
 // (A row-group variant -- G lanes per row, ordered sums from shared memory --
 // measured 40% slower on C2 and was dropped.)
-// P_ij is never stored: every pass rebuilds it from R, U, d, alpha and m_ij in
-// the same operation order (including the (1 - min l) rescales of earlier
-// passes), which is bit-identical and saves 2*nvar doubles per slot per pass.
+// Producers write transposed copies (d into the lower slot of row j, l_ij into
+// l^T of row j) so consumers stream their own row's slots instead of
+// gathering; P_ij is written once and rescaled in place per pass.
 #include "ef_kernels.cuh"
 
 namespace ef {
@@ -110,7 +110,12 @@ __global__ void __launch_bounds__(TPB, EF_MINB) k_edge_visc(Layout m, Gas g, con
     ct[a] = m.cT[a * NPL + p];
   }
   bool bad = false;
-  w.d[p] = d_ij_low<D>(Ui, Uj, cc, ct, g, bad);
+  const double dv = d_ij_low<D>(Ui, Uj, cc, ct, g, bad);
+  // d is symmetric by construction (riemann.py:139-142): the value is also
+  // the lower-triangle entry of row j, written straight to its slot (the
+  // reference's mirror, stepper.py:427-434, without a gather)
+  w.d[p] = dv;
+  w.d[sidx(j, m.tslot[p], m.L)] = dv;
   if (bad) atomicOr(w.err, ERR_PROJECT);
 }
 
@@ -179,12 +184,7 @@ __global__ void __launch_bounds__(TPB, EF_MINB) k_row_visc(Layout m, Gas g, cons
         for (int a = 0; a < D; ++a) t = t + (fj[k][a] - fi[k][a]) * cc[a];
         B[k] = B[k] + t;
       }
-      if (s < dg) {  // lower: d_ij = d_ji from the transpose position
-        const double x = d[sidx(j, m.tslot[p], L)];
-        d[p] = x;
-        return x;
-      }
-      return d[p];
+      return d[p];  // lower slots were filled by k_edge_visc
     };
     double res;
     if (L < 8) {  // numpy pairwise_sum, n < 8: sequential from +0
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(TPB, EF_MINB) k_low_order(Layout m, Gas g, con
 }
 
 // ---------------------------------------------------------------- steps 4-6
-// P_ij of slot (i, s) after `applied` limiter passes (stepper.py:460-468, :485).
+// P^(0)_ij of slot (i, s) (stepper.py:460-468); later passes rescale the stored P.
 template <int D>
 __device__ __forceinline__ void build_P(const Layout& m, const Work& w, const double* __restrict__ U,
                                         const double* Ui, const double* Ri, double ai, double inv_mi,
@@ -340,16 +340,7 @@ __device__ __forceinline__ void build_P(const Layout& m, const Work& w, const do
     const double K = ((b * w.R[k * NP + j]) - (bT * Ri[k])) + (dd * (U[k * NP + j] - Ui[k]));
     P[k] = factor * K;
   }
-  if (applied > 0) {
-    const int64_t NPL = NP * m.L;
-    const int64_t pt = sidx(j, m.tslot[p], m.L);
-    for (int q = 0; q < applied; ++q) {
-      const double ml = npmin(w.l[q * NPL + p], w.l[q * NPL + pt]);
-      const double f = 1.0 - ml;
-#pragma unroll
-      for (int k = 0; k < NV; ++k) P[k] = P[k] * f;
-    }
-  }
+  (void)applied;
 }
 
 template <int D>
@@ -377,7 +368,12 @@ __global__ void __launch_bounds__(TPB, EF_MINB) k_correction(Layout m, Gas g, co
     const int64_t j = m.col[p];
     double P[NV];
     build_P<D>(m, w, U, Ui, Ri, ai, inv_mi, factor, p, j, 0, P);
-    w.l[p] = limiter<D>(Un, P, rmin, rmax, pmin, sp.newton, g);
+    const int64_t NPL = NP * L;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) w.P[k * NPL + p] = P[k];
+    const double lv = limiter<D>(Un, P, rmin, rmax, pmin, sp.newton, g);
+    w.l[p] = lv;
+    w.lT[sidx(j, m.tslot[p], L)] = lv;  // l_ji of row j's slot for i
   }
 }
 
@@ -390,29 +386,29 @@ __global__ void __launch_bounds__(TPB, EF_MINB) k_limit_pass(Layout m, Gas g, co
   const int64_t NP = m.NP;
   const int L = m.L;
   const int64_t NPL = NP * L;
-  const double tau = *w.tau;
   const int card = m.card[i], dg = m.diag[i];
-  const double inv_mi = m.inv_m[i];
-  const double factor = (tau * inv_mi) * (double)(card - 1);
-  double Ui[NV], Ri[NV], Un[NV];
-  load_node<NV>(U, NP, i, Ui);
-  load_node<NV>(w.R, NP, i, Ri);
-  load_node<NV>(w.Unext, NP, i, Un);
-  const double ai = w.alpha[i];
   const int64_t base = sidx(i, 0, L);
+  const double* __restrict__ lp = w.l + pass * NPL;
+  const double* __restrict__ lpT = w.lT + pass * NPL;
   double upd[NV];
 #pragma unroll
   for (int k = 0; k < NV; ++k) upd[k] = 0.0;
+  // upd += min(l, l^T) P in slot order, then P <- (1 - min) P in place
+  // (stepper.py:478-485)
   for (int s = 0; s < card; ++s) {
     if (s == dg) continue;
     const int64_t p = base + (int64_t)s * 32;
-    const int64_t j = m.col[p];
-    double P[NV];
-    build_P<D>(m, w, U, Ui, Ri, ai, inv_mi, factor, p, j, pass, P);
-    const double ml = npmin(w.l[pass * NPL + p], w.l[pass * NPL + sidx(j, m.tslot[p], L)]);
+    const double ml = npmin(lp[p], lpT[p]);
+    const double f = 1.0 - ml;
 #pragma unroll
-    for (int k = 0; k < NV; ++k) upd[k] = upd[k] + ml * P[k];
+    for (int k = 0; k < NV; ++k) {
+      const double P = w.P[k * NPL + p];
+      upd[k] = upd[k] + ml * P;
+      w.P[k * NPL + p] = P * f;
+    }
   }
+  double Un[NV];
+  load_node<NV>(w.Unext, NP, i, Un);
   const double lam = m.lam[i];
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
@@ -420,13 +416,17 @@ __global__ void __launch_bounds__(TPB, EF_MINB) k_limit_pass(Layout m, Gas g, co
     w.Unext[k * NP + i] = Un[k];
   }
   const double rmin = w.bounds[i], rmax = w.bounds[NP + i], pmin = w.bounds[2 * NP + i];
+  double* __restrict__ ln = w.l + (pass + 1) * NPL;
+  double* __restrict__ lnT = w.lT + (pass + 1) * NPL;
   for (int s = 0; s < card; ++s) {
     if (s == dg) continue;
     const int64_t p = base + (int64_t)s * 32;
-    const int64_t j = m.col[p];
     double P[NV];
-    build_P<D>(m, w, U, Ui, Ri, ai, inv_mi, factor, p, j, pass + 1, P);
-    w.l[(pass + 1) * NPL + p] = limiter<D>(Un, P, rmin, rmax, pmin, sp.newton, g);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) P[k] = w.P[k * NPL + p];
+    const double lv = limiter<D>(Un, P, rmin, rmax, pmin, sp.newton, g);  // stepper.py:486-491
+    ln[p] = lv;
+    lnT[sidx(m.col[p], m.tslot[p], L)] = lv;
   }
 }
 
@@ -444,27 +444,19 @@ __global__ void __launch_bounds__(TPB, EF_MINB) k_final(Layout m, Gas g, const d
   load_node<NV>(w.Unext, NP, i, Un);
   if (sp.passes > 0) {
     const int pass = sp.passes - 1;
-    const double tau = *w.tau;
     const int card = m.card[i], dg = m.diag[i];
-    const double inv_mi = m.inv_m[i];
-    const double factor = (tau * inv_mi) * (double)(card - 1);
-    double Ui[NV], Ri[NV];
-    load_node<NV>(U, NP, i, Ui);
-    load_node<NV>(w.R, NP, i, Ri);
-    const double ai = w.alpha[i];
     const int64_t base = sidx(i, 0, L);
+    const double* __restrict__ lp = w.l + pass * NPL;
+    const double* __restrict__ lpT = w.lT + pass * NPL;
     double upd[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) upd[k] = 0.0;
     for (int s = 0; s < card; ++s) {
       if (s == dg) continue;
       const int64_t p = base + (int64_t)s * 32;
-      const int64_t j = m.col[p];
-      double P[NV];
-      build_P<D>(m, w, U, Ui, Ri, ai, inv_mi, factor, p, j, pass, P);
-      const double ml = npmin(w.l[pass * NPL + p], w.l[pass * NPL + sidx(j, m.tslot[p], L)]);
+      const double ml = npmin(lp[p], lpT[p]);
 #pragma unroll
-      for (int k = 0; k < NV; ++k) upd[k] = upd[k] + ml * P[k];
+      for (int k = 0; k < NV; ++k) upd[k] = upd[k] + ml * w.P[k * NPL + p];
     }
     const double lam = m.lam[i];
 #pragma unroll
