@@ -359,10 +359,9 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_params* prm, con
   EF_TRY(h->alloc(&w.bounds, (size_t)3 * NP));
   EF_TRY(h->alloc(&w.d, NPL));
   EF_TRY(h->alloc(&w.l, (size_t)std::max(1, h->passes) * NPL));
-  EF_TRY(h->alloc(&w.lT, (size_t)std::max(1, h->passes) * NPL));
   EF_TRY(h->alloc(&w.P, (size_t)NV * NPL));
   EF_CUDA(cudaMemset(w.P, 0, sizeof(double) * NV * NPL));
-  EF_CUDA(cudaMemset(w.lT, 0, sizeof(double) * std::max(1, h->passes) * NPL));
+
   EF_TRY(h->alloc(&w.tau_min_bits, 1));
   EF_TRY(h->alloc(&w.tau, 1));
   EF_TRY(h->alloc(&w.err, 1));

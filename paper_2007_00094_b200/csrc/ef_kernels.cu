@@ -15,14 +15,18 @@
 // k_edge_visc is one thread per edge; the others one thread per owned row.
 // (A row-group variant -- G lanes per row, ordered sums from shared memory --
 // measured 40% slower on C2 and was dropped.)
-// Producers write transposed copies (d into the lower slot of row j, l_ij into
-// l^T of row j) so consumers stream their own row's slots instead of
-// gathering; P_ij is written once and rescaled in place per pass.
+// k_edge_visc writes d_ij also into the lower slot of row j (d is symmetric),
+// so the row kernels stream their own slots; P_ij is written once by
+// k_correction and rescaled in place per pass (a transposed copy of l measured
+// slower: the producer's extra scattered store costs more than the gather).
 #include "ef_kernels.cuh"
 
 namespace ef {
 
-constexpr int TPB = 128;
+#ifndef EF_TPB
+#define EF_TPB 128
+#endif
+constexpr int TPB = EF_TPB;
 #ifndef EF_MINB
 #define EF_MINB 8  // resident blocks per SM requested from ptxas (64-register cap)
 #endif
@@ -371,9 +375,7 @@ __global__ void __launch_bounds__(TPB, EF_MINB) k_correction(Layout m, Gas g, co
     const int64_t NPL = NP * L;
 #pragma unroll
     for (int k = 0; k < NV; ++k) w.P[k * NPL + p] = P[k];
-    const double lv = limiter<D>(Un, P, rmin, rmax, pmin, sp.newton, g);
-    w.l[p] = lv;
-    w.lT[sidx(j, m.tslot[p], L)] = lv;  // l_ji of row j's slot for i
+    w.l[p] = limiter<D>(Un, P, rmin, rmax, pmin, sp.newton, g);
   }
 }
 
@@ -389,7 +391,6 @@ __global__ void __launch_bounds__(TPB, EF_MINB) k_limit_pass(Layout m, Gas g, co
   const int card = m.card[i], dg = m.diag[i];
   const int64_t base = sidx(i, 0, L);
   const double* __restrict__ lp = w.l + pass * NPL;
-  const double* __restrict__ lpT = w.lT + pass * NPL;
   double upd[NV];
 #pragma unroll
   for (int k = 0; k < NV; ++k) upd[k] = 0.0;
@@ -398,7 +399,7 @@ __global__ void __launch_bounds__(TPB, EF_MINB) k_limit_pass(Layout m, Gas g, co
   for (int s = 0; s < card; ++s) {
     if (s == dg) continue;
     const int64_t p = base + (int64_t)s * 32;
-    const double ml = npmin(lp[p], lpT[p]);
+    const double ml = npmin(lp[p], lp[sidx(m.col[p], m.tslot[p], L)]);
     const double f = 1.0 - ml;
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
@@ -417,16 +418,13 @@ __global__ void __launch_bounds__(TPB, EF_MINB) k_limit_pass(Layout m, Gas g, co
   }
   const double rmin = w.bounds[i], rmax = w.bounds[NP + i], pmin = w.bounds[2 * NP + i];
   double* __restrict__ ln = w.l + (pass + 1) * NPL;
-  double* __restrict__ lnT = w.lT + (pass + 1) * NPL;
   for (int s = 0; s < card; ++s) {
     if (s == dg) continue;
     const int64_t p = base + (int64_t)s * 32;
     double P[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) P[k] = w.P[k * NPL + p];
-    const double lv = limiter<D>(Un, P, rmin, rmax, pmin, sp.newton, g);  // stepper.py:486-491
-    ln[p] = lv;
-    lnT[sidx(m.col[p], m.tslot[p], L)] = lv;
+    ln[p] = limiter<D>(Un, P, rmin, rmax, pmin, sp.newton, g);  // stepper.py:486-491
   }
 }
 
@@ -447,14 +445,13 @@ __global__ void __launch_bounds__(TPB, EF_MINB) k_final(Layout m, Gas g, const d
     const int card = m.card[i], dg = m.diag[i];
     const int64_t base = sidx(i, 0, L);
     const double* __restrict__ lp = w.l + pass * NPL;
-    const double* __restrict__ lpT = w.lT + pass * NPL;
     double upd[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) upd[k] = 0.0;
     for (int s = 0; s < card; ++s) {
       if (s == dg) continue;
       const int64_t p = base + (int64_t)s * 32;
-      const double ml = npmin(lp[p], lpT[p]);
+      const double ml = npmin(lp[p], lp[sidx(m.col[p], m.tslot[p], L)]);
 #pragma unroll
       for (int k = 0; k < NV; ++k) upd[k] = upd[k] + ml * w.P[k * NPL + p];
     }

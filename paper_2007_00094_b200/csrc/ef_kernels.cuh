@@ -74,7 +74,6 @@ struct Work {
   double* bounds;    // [3][NP] rho_min, rho_max, phi_min
   double* d;         // [NP*L]
   double* l;         // [passes][NP*L]  l_ij of pass q
-  double* lT;        // [passes][NP*L]  l_ji of pass q at the (i, j) slot (written by row j)
   double* P;         // [NV][NP*L] correction fluxes P_ij, rescaled in place per pass
   unsigned long long* tau_min_bits;  // CFL min over owned rows
   double* tau;       // tau of the current RK step / Euler step
