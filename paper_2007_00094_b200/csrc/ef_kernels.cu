@@ -30,6 +30,9 @@ constexpr int TPB = EF_TPB;
 #ifndef EF_MINB
 #define EF_MINB 8  // resident blocks per SM requested from ptxas (64-register cap)
 #endif
+#ifndef EF_MINB_PASS
+#define EF_MINB_PASS 10  // k_limit_pass measured fastest at a 51-register cap
+#endif
 
 static inline unsigned grid_for(int64_t n) { return (unsigned)((n + TPB - 1) / TPB); }
 
@@ -380,7 +383,7 @@ __global__ void __launch_bounds__(TPB, EF_MINB) k_correction(Layout m, Gas g, co
 }
 
 template <int D>
-__global__ void __launch_bounds__(TPB, EF_MINB) k_limit_pass(Layout m, Gas g, const double* __restrict__ U,
+__global__ void __launch_bounds__(TPB, EF_MINB_PASS) k_limit_pass(Layout m, Gas g, const double* __restrict__ U,
                                                     Work w, StageParams sp, int pass) {
   constexpr int NV = D + 2;
   const int64_t i = blockIdx.x * (int64_t)TPB + threadIdx.x;

@@ -41,6 +41,7 @@ __all__ = [
     "mach3_disc",
     "sod_box",
     "periodic_fourier_box",
+    "periodic_box_matrices",
     "random_state",
     "make_config",
 ]
@@ -472,14 +473,65 @@ def sod_box(nx: int = 511, ny: int = 127, nz: int = 127, jitter: float = 0.2, se
     return ProblemSetup("c3-sod-box", mat, U0, bc, c_cfl=0.9, steps=steps, mesh=mesh)
 
 
+def periodic_box_matrices(n: int) -> PrecomputedMatrices:
+    """Q1 matrices of the uniform periodic n^3 hex mesh of the unit cube, built
+    from its translation invariance (every node has the same 27-point stencil
+    values) instead of a per-cell assembly -- O(n^3) memory and time, so the
+    262M-node C5 instance is feasible.  The values are those of `assemble_q1`
+    (same quadrature; the per-offset sums are taken over the 8 cells around a
+    node in a fixed order and m is symmetrised exactly)."""
+    if n < 3:
+        raise ValueError("periodic box needs n >= 3")
+    h = 1.0 / n
+    cell = Mesh(points=_CORNERS[3] * h, cells=np.arange(8)[None, :], dim=3)
+    loc = assemble_q1(cell)  # one cell: a dense 8x8 pattern
+    m_loc = np.zeros((8, 8))
+    c_loc = np.zeros((8, 8, 3))
+    for a in range(8):
+        for q in range(loc.indptr[a], loc.indptr[a + 1]):
+            m_loc[a, loc.indices[q]] = loc.m[q]
+            c_loc[a, loc.indices[q]] = loc.c[q]
+    corners = _CORNERS[3].astype(np.int64)
+    offs = np.array([(x, y, z) for x in (-1, 0, 1) for y in (-1, 0, 1) for z in (-1, 0, 1)])
+    m_off = np.zeros(27)
+    c_off = np.zeros((27, 3))
+    for k, o in enumerate(offs):
+        for a in range(8):  # node 0 is local vertex a of the cell with origin -corners[a]
+            b = np.flatnonzero((corners == corners[a] + o).all(axis=1))
+            if len(b):
+                m_off[k] += m_loc[a, b[0]]
+                c_off[k] += c_loc[a, b[0]]
+    mirror = np.array([np.flatnonzero((offs == -o).all(axis=1))[0] for o in offs])
+    m_sym = 0.5 * (m_off + m_off[mirror])
+    m_i = m_sym[0]
+    for k in range(1, 27):
+        m_i = m_i + m_sym[k]
+    N = n ** 3
+    ix, iy, iz = np.unravel_index(np.arange(N, dtype=np.int64), (n, n, n))
+    cols = np.empty((N, 27), dtype=np.int64)
+    for k, o in enumerate(offs):
+        cols[:, k] = (((ix + o[0]) % n) * n + (iy + o[1]) % n) * n + (iz + o[2]) % n
+    order = np.argsort(cols, axis=1, kind="stable")
+    cols = np.take_along_axis(cols, order, axis=1)
+    del ix, iy, iz
+    m = m_sym[order].ravel()
+    c = c_off[order].reshape(-1, 3)
+    del order
+    m_lumped = np.full(N, m_i)
+    return PrecomputedMatrices(n=N, dim=3, indptr=np.arange(0, 27 * N + 1, 27, dtype=np.int64),
+                               indices=cols.ravel(), m=m, c=c, beta=np.zeros(0), m_lumped=m_lumped,
+                               inv_m=1.0 / m_lumped)
+
+
 def periodic_fourier_box(n: int = 320, seed: int = 2007, gas: GasConstants = AIR,
                          steps: int = 50, modes: int = 8) -> ProblemSetup:
     """BASELINE C5: periodic n^3 hex mesh; rho, p in [0.5,1.5], |u| <= 1 from a
     sum of `modes` random low-frequency Fourier modes per field."""
-    mesh = box_mesh(n, n, n, periodic=(True, True, True))
-    mat = assemble_q1(mesh)
-    rep = np.zeros((mat.n, 3))
-    rep[mesh.reduced_index] = mesh.points
+    mat = periodic_box_matrices(n)
+    ix, iy, iz = np.unravel_index(np.arange(mat.n, dtype=np.int64), (n, n, n))
+    rep = np.column_stack([ix, iy, iz]) / float(n)
+    del ix, iy, iz
+    mesh = None
     rng = np.random.default_rng(seed)
     fields = []
     for _ in range(5):
@@ -519,4 +571,6 @@ def make_config(name: str, scale: str = "full", gas: GasConstants = AIR) -> Prob
         return sod_box(*((31, 7, 7) if small else (511, 127, 127)), gas=gas)
     if name == "c5":
         return periodic_fourier_box(12 if small else 320, gas=gas)
+    if name == "c5m":  # mid-size 3D instance for quick measurements
+        return periodic_fourier_box(12 if small else 160, gas=gas)
     raise ValueError(f"unknown config {name!r}")
