@@ -129,9 +129,35 @@ int ef_local_gids(ef_solver* h, int64_t* out);
 void ef_pow_host(const double* x, double y, double* out, int64_t n);
 int ef_pow_device(const double* x, double y, double* out, int64_t n);
 
-/* Device-resident state exchange for benchmarks: copies between the current
- * state and a device buffer in (n_local, nvar) SoA local order. */
+/* Device pointer of the current state, (nvar, stride) structure-of-arrays in
+ * local row order (benchmarks / zero-copy consumers). */
 int ef_state_device_ptr(ef_solver* h, void** dev_ptr, int64_t* stride);
+
+/* ---- multi-rank (exchange.partition / Communicator, exchange.py:393-222) ----
+ * One process per GPU: rank 0 calls ef_nccl_unique_id, broadcasts the 128
+ * bytes, every rank passes them in ef_dist.nccl_id to ef_create; halo syncs are
+ * NCCL send/recv, the CFL bound an NCCL allreduce(min).  Ranks created with
+ * nranks > 1 and nccl_id == NULL instead form a same-device group stepped in
+ * lockstep (exchanges by device copies) — the reference's simulated ranks. */
+int ef_nccl_unique_id(void* out128);
+typedef struct ef_group ef_group;
+int ef_group_create(ef_solver** ranks, int32_t nranks, ef_group** out);
+int ef_group_destroy(ef_group* g);
+int ef_group_set_state(ef_group* g, const double* U);
+int ef_group_get_state(ef_group* g, double* U);
+int ef_group_euler_step(ef_group* g, int32_t has_tau, double tau, double tau_max, double* tau_used);
+int ef_group_ssp_rk3_step(ef_group* g, int32_t has_tau, double tau, double tau_max, double* tau_used);
+
+/* Host-only partition plan of one rank (no CUDA): sizes = {n_owned, n_local,
+ * L, nranks}; rows: global CM ids of the rows sent to / received from a peer
+ * (recv = 0 / 1) in message order; slots: (row CM id, column CM id) pairs of
+ * the limiter-factor messages.  Return the count (-1 on a bad peer). */
+typedef struct ef_plan ef_plan;
+int ef_plan_build(const ef_matrices* mat, const ef_dist* dist, ef_plan** out);
+int ef_plan_destroy(ef_plan* p);
+int ef_plan_sizes(const ef_plan* p, int64_t* out4);
+int64_t ef_plan_rows(const ef_plan* p, int32_t peer, int32_t recv, int64_t* out_gids, int64_t cap);
+int64_t ef_plan_slots(const ef_plan* p, int32_t peer, int32_t recv, int64_t* out_pairs, int64_t cap);
 
 #ifdef __cplusplus
 }

@@ -64,6 +64,18 @@ SIGNATURES = {
     "ef_pow_host": (None, [_p, _d, _p, _i64]),
     "ef_pow_device": (_i32, [_p, _d, _p, _i64]),
     "ef_state_device_ptr": (_i32, [_p, ctypes.POINTER(_p), ctypes.POINTER(_i64)]),
+    "ef_nccl_unique_id": (_i32, [_p]),
+    "ef_group_create": (_i32, [_p, _i32, ctypes.POINTER(_p)]),
+    "ef_group_destroy": (_i32, [_p]),
+    "ef_group_set_state": (_i32, [_p, _p]),
+    "ef_group_get_state": (_i32, [_p, _p]),
+    "ef_group_euler_step": (_i32, [_p, _i32, _d, _d, ctypes.POINTER(_d)]),
+    "ef_group_ssp_rk3_step": (_i32, [_p, _i32, _d, _d, ctypes.POINTER(_d)]),
+    "ef_plan_build": (_i32, [ctypes.POINTER(EfMatrices), ctypes.POINTER(EfDist), ctypes.POINTER(_p)]),
+    "ef_plan_destroy": (_i32, [_p]),
+    "ef_plan_sizes": (_i32, [_p, _p]),
+    "ef_plan_rows": (_i64, [_p, _i32, _i32, _p, _i64]),
+    "ef_plan_slots": (_i64, [_p, _i32, _i32, _p, _i64]),
 }
 
 _lib = None

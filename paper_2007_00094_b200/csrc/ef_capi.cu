@@ -1,23 +1,28 @@
-// ef_capi.cu — host side of the C-ABI (include/ef_b200.h): setup of the
-// SELL-32 layout, device memory, stage orchestration and error mapping.
+// ef_capi.cu — host side of the C-ABI (include/ef_b200.h): SELL-32 setup from
+// the partition plan (ef_plan.h), device memory, the phase-stepped stage
+// driver with halo exchanges, transports (NCCL; same-device group), and error
+// mapping.
 //
-// Setup restates the reference's ordering contract natively (the reference
-// does it with per-row Python loops, stepper.py:163-268, sparsity.py:168-309):
-//   * rows live in global Cuthill-McKee order (cm_perm from exchange.partition);
-//   * a row's slots are its stencil columns sorted by CM id (stepper.py:195);
-//   * the pad width L is the global maximum cardinality (stepper.py:128-129);
-//   * ghost rows (nranks > 1) carry the stencil truncated to local rows
-//     (stepper.py:175-181).
+// One stage (stepper.py:508-610) = six kernels; on more than one rank the
+// reference's five ghost syncs and one tau reduction sit between them:
+//   edge_visc, row_visc | alpha (+ tau min) | low_order | R | correction | l_0 |
+//   limit_pass(p) | l_{p+1} ... | final | U  (+ step0 of the ghost rows)
+// (stepper.py:532, 545, 561, 585, 605).
+#include <dlfcn.h>
+
 #include <algorithm>
 #include <array>
-#include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <string>
 #include <vector>
 
+#include <nccl.h>
+
 #include "../../include/ef_b200.h"
 #include "ef_kernels.cuh"
+#include "ef_plan.h"
 
 using ef::Gas;
 using ef::Layout;
@@ -38,13 +43,69 @@ static int fail(int code, const std::string& msg) {
       return fail(EF_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));      \
   } while (0)
 
+#define EF_TRY(x)                 \
+  do {                            \
+    int rc_ = (x);                \
+    if (rc_ != EF_OK) return rc_; \
+  } while (0)
+
+// ---------------------------------------------------------------- NCCL (dlopen)
+// Bound at run time so the library also loads where NCCL is absent (CPU tests);
+// an already loaded libnccl (torch's) is preferred.
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api;
+  tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return api;
+#define EF_SYM(name) api.name = reinterpret_cast<decltype(api.name)>(dlsym(h, "nccl" #name))
+  EF_SYM(GetUniqueId);
+  EF_SYM(CommInitRank);
+  EF_SYM(CommDestroy);
+  EF_SYM(Send);
+  EF_SYM(Recv);
+  EF_SYM(GroupStart);
+  EF_SYM(GroupEnd);
+  EF_SYM(AllReduce);
+  EF_SYM(GetErrorString);
+#undef EF_SYM
+  api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Send && api.Recv && api.GroupStart &&
+           api.GroupEnd && api.AllReduce && api.GetErrorString;
+  return api;
+}
+
+#define EF_NCCL(x)                                                                             \
+  do {                                                                                         \
+    ncclResult_t r_ = (x);                                                                     \
+    if (r_ != ncclSuccess) return fail(EF_ERR_NCCL, std::string(#x) + ": " + nccl().GetErrorString(r_)); \
+  } while (0)
+
+// ---------------------------------------------------------------- handle
 struct ef_solver {
   int dim = 0, nvar = 0, L = 0, passes = 0, newton = 0, standard_card = 0;
   double c_cfl = 0.9;
   Gas gas{};
   int64_t n_global = 0, n_owned = 0, n_local = 0, NP = 0, NPL = 0, nnz_owned = 0;
   int rank = 0, nranks = 1, device = 0;
-  int64_t range_lo = 0;
+  bool use_nccl = false;   // nranks > 1: NCCL, or a same-device group (ef_group_*)
+  ncclComm_t comm = nullptr;
   cudaStream_t st = nullptr;
   bool own_stream = false;
   Layout lay{};
@@ -56,7 +117,14 @@ struct ef_solver {
   double* aos_dev = nullptr;
   int64_t* orig_dev = nullptr;
   std::vector<int64_t> orig_host, gid_host;
-  // pinned readback block: [0] tau (double), [1] err (int), [2] bad gid
+  // halo plans (per peer rank): counts and offsets in rows / slots, device index lists
+  std::vector<int64_t> xs_rows, xr_rows, xs_slots, xr_slots;   // counts
+  std::vector<int64_t> os_rows, or_rows, os_slots, or_slots;   // offsets
+  int32_t *send_rows = nullptr, *recv_rows = nullptr, *send_pos = nullptr, *recv_pos = nullptr;
+  int64_t n_send_rows = 0, n_recv_rows = 0, n_send_pos = 0, n_recv_pos = 0;
+  double *sendbuf = nullptr, *recvbuf = nullptr;
+  int64_t sync_count = 0, sync_volume = 0;  // Solver.comm counters (exchange.py:131-157)
+  // pinned readback block
   struct Readback {
     double tau;
     int err;
@@ -89,15 +157,15 @@ struct ef_solver {
     if (rb) cudaFreeHost(rb);
     for (auto& set : ring)
       for (auto& e : set) cudaEventDestroy(e);
+    if (comm && nccl().ok) nccl().CommDestroy(comm);
     if (own_stream && st) cudaStreamDestroy(st);
   }
 };
 
-#define EF_TRY(x)                 \
-  do {                            \
-    int rc_ = (x);                \
-    if (rc_ != EF_OK) return rc_; \
-  } while (0)
+struct ef_group {
+  std::vector<ef_solver*> hs;
+  unsigned long long** bits_dev = nullptr;  // device array of the ranks' tau_min_bits
+};
 
 template <class T>
 static int upload(ef_solver* h, T** dst, const std::vector<T>& src) {
@@ -124,97 +192,35 @@ static Gas make_gas(const ef_params* p) {
   return g;
 }
 
-static int build(ef_solver* h, const ef_matrices* mat, const ef_params* prm, const ef_boundary* bc,
-                 const ef_dist* dist) {
+// ---------------------------------------------------------------- setup
+static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, const ef_dist* dist) {
   const int D = h->dim, NV = h->nvar;
   const int64_t n = mat->n;
-  const int R = dist ? dist->nranks : 1;
-  const int r = dist ? dist->rank : 0;
   if (!dist || !dist->cm_perm) return fail(EF_ERR_ARG, "ef_dist.cm_perm is required");
-  const int64_t* cm_perm = dist->cm_perm;
-  std::vector<int64_t> cm_inv(n, -1);
-  for (int64_t o = 0; o < n; ++o) {
-    const int64_t g = cm_perm[o];
-    if (g < 0 || g >= n || cm_inv[g] >= 0) return fail(EF_ERR_ARG, "cm_perm is not a permutation");
-    cm_inv[g] = o;
-  }
-  // owned range (exchange.py:405-411 when ranges == NULL)
-  int64_t s_lo, s_hi;
-  if (dist->ranges) {
-    s_lo = dist->ranges[r];
-    s_hi = dist->ranges[r + 1];
-  } else {
-    const int64_t base = n / R, extra = n % R;
-    s_lo = r * base + std::min<int64_t>(r, extra);
-    s_hi = s_lo + base + (r < extra ? 1 : 0);
-  }
-  h->range_lo = s_lo;
-  // global pad width and the most frequent cardinality
-  int64_t L = 0;
-  std::vector<int64_t> card_hist(1, 0);
-  for (int64_t o = 0; o < n; ++o) {
-    const int64_t c = mat->indptr[o + 1] - mat->indptr[o];
-    L = std::max(L, c);
-    if ((int64_t)card_hist.size() <= c) card_hist.resize(c + 1, 0);
-    card_hist[c]++;
-  }
-  if (L > 255) return fail(EF_ERR_ARG, "stencil cardinality above 255 is not supported");
-  h->L = (int)L;
-  h->standard_card = (int)(std::max_element(card_hist.begin(), card_hist.end()) - card_hist.begin());
-  // local rows: owned CM ids, then ghosts (ascending CM id)
-  const int64_t n_owned = s_hi - s_lo;
+  ef::Plan P;
+  if (!ef::build_plan(n, mat->indptr, mat->indices, dist->cm_perm, h->rank, h->nranks, dist->ranges, P))
+    return fail(EF_ERR_ARG, P.error);
+  const int L = P.L;
+  const int64_t n_owned = P.n_owned, n_local = P.n_local;
+  h->L = L;
+  h->standard_card = P.standard_card;
   h->n_global = n;
-  std::vector<int64_t> ghosts;
-  for (int64_t g = s_lo; g < s_hi; ++g) {
-    const int64_t o = cm_inv[g];
-    for (int64_t q = mat->indptr[o]; q < mat->indptr[o + 1]; ++q) {
-      const int64_t cg = cm_perm[mat->indices[q]];
-      if (cg < s_lo || cg >= s_hi) ghosts.push_back(cg);
-    }
-  }
-  std::sort(ghosts.begin(), ghosts.end());
-  ghosts.erase(std::unique(ghosts.begin(), ghosts.end()), ghosts.end());
-  const int64_t n_local = n_owned + (int64_t)ghosts.size();
-  auto local_of = [&](int64_t g) -> int64_t {
-    if (g >= s_lo && g < s_hi) return g - s_lo;
-    auto it = std::lower_bound(ghosts.begin(), ghosts.end(), g);
-    if (it != ghosts.end() && *it == g) return n_owned + (it - ghosts.begin());
-    return -1;
-  };
   h->n_owned = n_owned;
   h->n_local = n_local;
-  h->NP = (n_local + 31) / 32 * 32;
-  if (h->NP == 0) h->NP = 32;
+  h->NP = std::max<int64_t>((n_local + 31) / 32 * 32, 32);
   h->NPL = h->NP * L;
   const int64_t NP = h->NP, NPL = h->NPL;
-  h->gid_host.resize(n_local);
+  if (NPL >= (int64_t)1 << 31) return fail(EF_ERR_ARG, "local slot count exceeds int32 positions");
+  h->gid_host = P.gid;
   h->orig_host.resize(n_local);
-  for (int64_t i = 0; i < n_owned; ++i) h->gid_host[i] = s_lo + i;
-  for (size_t k = 0; k < ghosts.size(); ++k) h->gid_host[n_owned + k] = ghosts[k];
-  for (int64_t i = 0; i < n_local; ++i) h->orig_host[i] = cm_inv[h->gid_host[i]];
+  for (int64_t i = 0; i < n_local; ++i) h->orig_host[i] = P.cm_inv[P.gid[i]];
+  auto local_of = [&](int64_t g) -> int64_t {
+    if (g >= P.s_lo && g < P.s_hi) return g - P.s_lo;
+    auto it = std::lower_bound(P.gid.begin() + n_owned, P.gid.end(), g);
+    if (it != P.gid.end() && *it == g) return it - P.gid.begin();
+    return -1;
+  };
 
-  // per local row: slots sorted by CM id, truncated to local columns
-  std::vector<int64_t> rptr(n_local + 1, 0);
-  std::vector<int64_t> rcm;   // CM id per slot
-  std::vector<int64_t> rsrc;  // source nnz index per slot
-  rcm.reserve((size_t)n_local * L);
-  rsrc.reserve((size_t)n_local * L);
-  std::vector<std::pair<int64_t, int64_t>> tmp;
-  for (int64_t i = 0; i < n_local; ++i) {
-    const int64_t o = h->orig_host[i];
-    tmp.clear();
-    for (int64_t q = mat->indptr[o]; q < mat->indptr[o + 1]; ++q) {
-      const int64_t cg = cm_perm[mat->indices[q]];
-      if (i >= n_owned && local_of(cg) < 0) continue;
-      tmp.emplace_back(cg, q);
-    }
-    std::sort(tmp.begin(), tmp.end());
-    for (auto& t : tmp) {
-      rcm.push_back(t.first);
-      rsrc.push_back(t.second);
-    }
-    rptr[i + 1] = (int64_t)rcm.size();
-  }
   // SELL-32 host images
   std::vector<int32_t> col(NPL);
   std::vector<uint8_t> tslot(NPL, 0), card(NP, 1), diag(NP, 0);
@@ -222,62 +228,56 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_params* prm, con
   std::vector<double> m_i(NP, 1.0), inv_m(NP, 1.0), lam(NP, 1.0);
   std::vector<int64_t> gid(NP, 0);
   for (int64_t i = 0; i < NP; ++i)
-    for (int s = 0; s < L; ++s) col[ef::sidx(i, s, (int)L)] = (int32_t)std::min<int64_t>(i, n_local > 0 ? n_local - 1 : 0);
+    for (int s = 0; s < L; ++s) col[ef::sidx(i, s, L)] = (int32_t)std::min<int64_t>(i, n_local - 1);
   int64_t nnz_owned = 0;
   for (int64_t i = 0; i < n_local; ++i) {
     const int64_t o = h->orig_host[i];
-    const int64_t cnt = rptr[i + 1] - rptr[i];
+    const int64_t cnt = P.rptr[i + 1] - P.rptr[i];
     card[i] = (uint8_t)cnt;
     if (i < n_owned) nnz_owned += cnt;
     int dg = -1;
     for (int64_t s = 0; s < cnt; ++s) {
-      const int64_t cg = rcm[rptr[i] + s];
+      const int64_t cg = P.rcm[P.rptr[i] + s];
       const int64_t j = local_of(cg);
-      const int64_t q = rsrc[rptr[i] + s];
-      const int64_t p = ef::sidx(i, (int)s, (int)L);
+      const int64_t q = P.rsrc[P.rptr[i] + s];
+      const int64_t p = ef::sidx(i, (int)s, L);
       col[p] = (int32_t)j;
       if (j == i) dg = (int)s;
       mij[p] = mat->m[q];
       for (int a = 0; a < D; ++a) c[(size_t)a * NPL + p] = mat->c[q * D + a];
-      // transpose slot: position of this row's CM id in row j
-      const int64_t* b = rcm.data() + rptr[j];
-      const int64_t* e = rcm.data() + rptr[j + 1];
-      const int64_t* it = std::lower_bound(b, e, h->gid_host[i]);
-      if (it == e || *it != h->gid_host[i]) {
-        if (i < n_owned || j < n_owned)
-          return fail(EF_ERR_ARG, "stencil pattern is not structurally symmetric");
-        tslot[p] = 0;
-      } else {
-        tslot[p] = (uint8_t)(it - b);
-      }
+      // transpose slot: position of this row's CM id in row j (both rows local)
+      const int64_t* b = P.rcm.data() + P.rptr[j];
+      const int64_t* e = P.rcm.data() + P.rptr[j + 1];
+      const int64_t* it = std::lower_bound(b, e, P.gid[i]);
+      if (it == e || *it != P.gid[i]) return fail(EF_ERR_ARG, "stencil pattern is not structurally symmetric");
+      tslot[p] = (uint8_t)(it - b);
     }
     if (dg < 0) return fail(EF_ERR_ARG, "every stencil must contain its own row");
     diag[i] = (uint8_t)dg;
     m_i[i] = mat->m_lumped[o];
     inv_m[i] = mat->inv_m[o];
     const int64_t den = std::max<int64_t>(cnt - 1, 1);
-    lam[i] = 1.0 / (double)den;
-    gid[i] = h->gid_host[i];
+    lam[i] = 1.0 / (double)den;  // stepper.py:214-215
+    gid[i] = P.gid[i];
   }
   for (int64_t i = 0; i < n_local; ++i) {
-    const int64_t cnt = rptr[i + 1] - rptr[i];
+    const int64_t cnt = P.rptr[i + 1] - P.rptr[i];
     for (int64_t s = 0; s < cnt; ++s) {
-      const int64_t p = ef::sidx(i, (int)s, (int)L);
-      const int64_t j = col[p];
-      const int64_t pt = ef::sidx(j, tslot[p], (int)L);
+      const int64_t p = ef::sidx(i, (int)s, L);
+      const int64_t pt = ef::sidx(col[p], tslot[p], L);
       for (int a = 0; a < D; ++a) cT[(size_t)a * NPL + p] = c[(size_t)a * NPL + pt];
     }
   }
   h->nnz_owned = nnz_owned;
-  // upper-triangle edge list (all local rows: ghost rows need d for the mirror)
-  if (NPL >= (int64_t)1 << 31) return fail(EF_ERR_ARG, "local slot count exceeds int32 positions");
+  // upper-triangle edges with at least one owned endpoint (a ghost row's upper
+  // edge to an owned row is that row's lower entry)
   std::vector<int32_t> edges;
   for (int64_t sl = 0; sl < NP / 32; ++sl)
     for (int s = 0; s < L; ++s)
       for (int ln = 0; ln < 32; ++ln) {
         const int64_t i = sl * 32 + ln;
-        if (i >= n_local) continue;
-        if (s > diag[i] && s < card[i]) edges.push_back((int32_t)ef::sidx(i, s, (int)L));
+        if (i >= n_local || !(s > diag[i] && s < card[i])) continue;
+        if (i < n_owned || col[ef::sidx(i, s, L)] < n_owned) edges.push_back((int32_t)ef::sidx(i, s, L));
       }
   // boundary data (stepper.py:258-267): owned rows only
   std::vector<int8_t> bc_kind(NP, 0);
@@ -287,28 +287,57 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_params* prm, con
     for (int64_t q = 0; q < bc->n_slip; ++q) {
       const int64_t o = bc->slip[q];
       if (o < 0 || o >= n) return fail(EF_ERR_ARG, "slip node id out of range");
-      const int64_t g = cm_perm[o];
-      if (g < s_lo || g >= s_hi) continue;
-      const int64_t i = g - s_lo;
+      const int64_t g = dist->cm_perm[o];
+      if (g < P.s_lo || g >= P.s_hi) continue;
+      const int64_t i = g - P.s_lo;
       bc_kind[i] |= 1;
       for (int a = 0; a < D; ++a) bc_n[(size_t)a * NP + i] = bc->slip_normals[q * D + a];
     }
     for (int64_t q = 0; q < bc->n_inflow; ++q) {
       const int64_t o = bc->inflow[q];
       if (o < 0 || o >= n) return fail(EF_ERR_ARG, "inflow node id out of range");
-      const int64_t g = cm_perm[o];
-      if (g < s_lo || g >= s_hi) continue;
-      bc_kind[g - s_lo] |= 2;
+      const int64_t g = dist->cm_perm[o];
+      if (g < P.s_lo || g >= P.s_hi) continue;
+      bc_kind[g - P.s_lo] |= 2;
     }
     if (bc->n_inflow > 0) {
       if (!bc->farfield) return fail(EF_ERR_ARG, "inflow nodes need a farfield state");
       for (int k = 0; k < NV; ++k) farfield[k] = bc->farfield[k];
     }
   }
+  // halo plans -> flat device index lists (peer-major)
+  const int R = h->nranks;
+  h->xs_rows.assign(R, 0);
+  h->xr_rows.assign(R, 0);
+  h->xs_slots.assign(R, 0);
+  h->xr_slots.assign(R, 0);
+  h->os_rows.assign(R + 1, 0);
+  h->or_rows.assign(R + 1, 0);
+  h->os_slots.assign(R + 1, 0);
+  h->or_slots.assign(R + 1, 0);
+  std::vector<int32_t> srows, rrows, spos, rpos;
+  for (int q = 0; q < R; ++q) {
+    for (int64_t i : P.send_rows[q]) srows.push_back((int32_t)i);
+    for (int64_t i : P.recv_rows[q]) rrows.push_back((int32_t)i);
+    for (int64_t e : P.send_slots[q]) spos.push_back((int32_t)ef::sidx(e / 256, (int)(e % 256), L));
+    for (int64_t e : P.recv_slots[q]) rpos.push_back((int32_t)ef::sidx(e / 256, (int)(e % 256), L));
+    h->xs_rows[q] = (int64_t)P.send_rows[q].size();
+    h->xr_rows[q] = (int64_t)P.recv_rows[q].size();
+    h->xs_slots[q] = (int64_t)P.send_slots[q].size();
+    h->xr_slots[q] = (int64_t)P.recv_slots[q].size();
+    h->os_rows[q + 1] = h->os_rows[q] + h->xs_rows[q];
+    h->or_rows[q + 1] = h->or_rows[q] + h->xr_rows[q];
+    h->os_slots[q + 1] = h->os_slots[q] + h->xs_slots[q];
+    h->or_slots[q + 1] = h->or_slots[q] + h->xr_slots[q];
+  }
+  h->n_send_rows = (int64_t)srows.size();
+  h->n_recv_rows = (int64_t)rrows.size();
+  h->n_send_pos = (int64_t)spos.size();
+  h->n_recv_pos = (int64_t)rpos.size();
 
   // ---- device images
   Layout& m = h->lay;
-  m.L = (int)L;
+  m.L = L;
   m.NP = NP;
   m.n_local = n_local;
   m.n_owned = n_owned;
@@ -317,6 +346,7 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_params* prm, con
   double *d_c, *d_cT, *d_mij, *d_mi, *d_invm, *d_lam, *d_bcn;
   int64_t* d_gid;
   int8_t* d_bck;
+  int32_t* d_edges;
   EF_TRY(upload(h, &d_col, col));
   EF_TRY(upload(h, &d_tslot, tslot));
   EF_TRY(upload(h, &d_card, card));
@@ -330,11 +360,7 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_params* prm, con
   EF_TRY(upload(h, &d_gid, gid));
   EF_TRY(upload(h, &d_bck, bc_kind));
   EF_TRY(upload(h, &d_bcn, bc_n));
-  int32_t* d_edges;
   EF_TRY(upload(h, &d_edges, edges));
-  m.edges = d_edges;
-  m.n_edges = (int64_t)edges.size();
-  m.slab = ef::make_fastdiv((uint32_t)(32 * L));
   m.col = d_col;
   m.tslot = d_tslot;
   m.card = d_card;
@@ -348,9 +374,23 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_params* prm, con
   m.gid = d_gid;
   m.bc_kind = d_bck;
   m.bc_n = d_bcn;
+  m.edges = d_edges;
+  m.n_edges = (int64_t)edges.size();
+  m.slab = ef::make_fastdiv((uint32_t)(32 * L));
   for (int k = 0; k < 5; ++k) m.farfield[k] = farfield[k];
+  if (R > 1) {
+    EF_TRY(upload(h, &h->send_rows, srows));
+    EF_TRY(upload(h, &h->recv_rows, rrows));
+    EF_TRY(upload(h, &h->send_pos, spos));
+    EF_TRY(upload(h, &h->recv_pos, rpos));
+    const int64_t sb = std::max(h->n_send_rows * NV, h->n_send_pos);
+    const int64_t rbn = std::max(h->n_recv_rows * NV, h->n_recv_pos);
+    EF_TRY(h->alloc(&h->sendbuf, sb));
+    EF_TRY(h->alloc(&h->recvbuf, rbn));
+  }
 
   Work& w = h->w;
+  const int npass = std::max(1, h->passes);
   EF_TRY(h->alloc(&w.eor, NP));
   EF_TRY(h->alloc(&w.phi, NP));
   EF_TRY(h->alloc(&w.alpha, NP));
@@ -358,16 +398,15 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_params* prm, con
   EF_TRY(h->alloc(&w.Unext, (size_t)NV * NP));
   EF_TRY(h->alloc(&w.bounds, (size_t)3 * NP));
   EF_TRY(h->alloc(&w.d, NPL));
-  EF_TRY(h->alloc(&w.l, (size_t)std::max(1, h->passes) * NPL));
+  EF_TRY(h->alloc(&w.l, (size_t)npass * NPL));
   EF_TRY(h->alloc(&w.P, (size_t)NV * NPL));
-  EF_CUDA(cudaMemset(w.P, 0, sizeof(double) * NV * NPL));
-
   EF_TRY(h->alloc(&w.tau_min_bits, 1));
   EF_TRY(h->alloc(&w.tau, 1));
   EF_TRY(h->alloc(&w.err, 1));
   EF_TRY(h->alloc(&w.bad_gid, 1));
   EF_CUDA(cudaMemset(w.d, 0, sizeof(double) * NPL));
-  EF_CUDA(cudaMemset(w.l, 0, sizeof(double) * std::max(1, h->passes) * NPL));
+  EF_CUDA(cudaMemset(w.l, 0, sizeof(double) * npass * NPL));
+  EF_CUDA(cudaMemset(w.P, 0, sizeof(double) * NV * NPL));
   EF_CUDA(cudaMemset(w.alpha, 0, sizeof(double) * NP));
   EF_CUDA(cudaMemset(w.R, 0, sizeof(double) * NV * NP));
   EF_CUDA(cudaMemset(w.eor, 0, sizeof(double) * NP));
@@ -379,119 +418,20 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_params* prm, con
   EF_TRY(h->alloc(&h->aos_dev, (size_t)n * NV));
   EF_TRY(upload(h, &h->orig_dev, h->orig_host));
   EF_CUDA(cudaMallocHost((void**)&h->rb, sizeof(ef_solver::Readback)));
-  (void)prm;
   return EF_OK;
 }
 
-extern "C" {
+// ---------------------------------------------------------------- driver
+// A Driver steps one NCCL rank (hs.size() == 1) or every rank of a same-device
+// group in lockstep (all handles on one stream, exchanges by device copies).
+struct Driver {
+  std::vector<ef_solver*> hs;
+  bool group = false;
+  unsigned long long** bits_dev = nullptr;
+  ef_solver* h0() const { return hs[0]; }
+  bool multi() const { return hs[0]->nranks > 1; }
+};
 
-const char* ef_last_error(void) { return g_err.c_str(); }
-
-int ef_create(const ef_matrices* mat, const ef_params* prm, const ef_boundary* bc,
-              const ef_dist* dist, ef_solver** out) {
-  if (!mat || !prm || !out) return fail(EF_ERR_ARG, "null argument");
-  *out = nullptr;
-  if (!(prm->c_cfl > 0.0 && prm->c_cfl <= 1.0)) return fail(EF_ERR_ARG, "c_cfl must lie in (0, 1]");
-  if (prm->limiter_passes < 0) return fail(EF_ERR_ARG, "limiter_passes must be >= 0");
-  if (prm->newton_steps < 0) return fail(EF_ERR_ARG, "newton_steps must be >= 0");
-  if (mat->dim != 2 && mat->dim != 3) return fail(EF_ERR_ARG, "dim must be 2 or 3");
-  if (mat->n <= 0) return fail(EF_ERR_ARG, "empty mesh");
-  if (dist && (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks))
-    return fail(EF_ERR_ARG, "bad rank/nranks");
-  if (dist && dist->nranks > 1)
-    return fail(EF_ERR_ARG, "multi-rank halo exchange is not built into this library version");
-  ef_solver* h = new ef_solver();
-  h->dim = mat->dim;
-  h->nvar = mat->dim + 2;
-  h->passes = prm->limiter_passes;
-  h->newton = prm->newton_steps;
-  h->c_cfl = prm->c_cfl;
-  h->gas = make_gas(prm);
-  h->rank = dist ? dist->rank : 0;
-  h->nranks = dist ? dist->nranks : 1;
-  h->device = dist ? dist->device : 0;
-  cudaError_t e = cudaSetDevice(h->device);
-  if (e != cudaSuccess) {
-    delete h;
-    return fail(EF_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
-  }
-  if (dist && dist->stream) {
-    h->st = (cudaStream_t)dist->stream;
-  } else {
-    e = cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking);
-    if (e != cudaSuccess) {
-      delete h;
-      return fail(EF_ERR_CUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
-    }
-    h->own_stream = true;
-  }
-  int rc = build(h, mat, prm, bc, dist);
-  if (rc != EF_OK) {
-    std::string msg = g_err;
-    delete h;
-    g_err = msg;
-    return rc;
-  }
-  *out = h;
-  return EF_OK;
-}
-
-int ef_destroy(ef_solver* h) {
-  if (h) {
-    cudaSetDevice(h->device);
-    cudaStreamSynchronize(h->st);
-    delete h;
-  }
-  return EF_OK;
-}
-
-static int readback(ef_solver* h) {
-  EF_CUDA(cudaMemcpyAsync(&h->rb->tau, h->w.tau, sizeof(double), cudaMemcpyDeviceToHost, h->st));
-  EF_CUDA(cudaMemcpyAsync(&h->rb->err, h->w.err, sizeof(int), cudaMemcpyDeviceToHost, h->st));
-  EF_CUDA(cudaMemcpyAsync(&h->rb->bad, h->w.bad_gid, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
-  EF_CUDA(cudaStreamSynchronize(h->st));
-  EF_CUDA(cudaGetLastError());
-  return EF_OK;
-}
-
-int ef_set_state(ef_solver* h, const double* U) {
-  if (!h || !U) return fail(EF_ERR_ARG, "null argument");
-  cudaSetDevice(h->device);
-  const int NV = h->nvar;
-  // upload the full array, permute it into local SoA order on the device
-  // (into a spare buffer, so a rejected state leaves the current one intact)
-  const int spare = (h->cur + 1) % 3;
-  EF_CUDA(cudaMemsetAsync(h->w.err, 0, sizeof(int), h->st));
-  EF_CUDA(cudaMemcpyAsync(h->aos_dev, U, sizeof(double) * NV * h->n_global, cudaMemcpyHostToDevice, h->st));
-  ef::launch_gather_state(h->dim, h->lay, h->aos_dev, h->orig_dev, h->Ubuf[spare], h->w.err, h->st);
-  EF_TRY(readback(h));
-  if (h->rb->err) return fail(EF_ERR_INADMISSIBLE, "initial state is not admissible");
-  h->cur = spare;
-  h->pending_out = -1;
-  ef::launch_nodal(h->dim, h->lay, h->gas, h->Ubuf[h->cur], h->w, 0, h->lay.n_local, h->st);
-  EF_CUDA(cudaGetLastError());
-  return EF_OK;
-}
-
-int ef_get_state(ef_solver* h, double* U) {
-  if (!h || !U) return fail(EF_ERR_ARG, "null argument");
-  cudaSetDevice(h->device);
-  const int NV = h->nvar;
-  if (h->nranks == 1) {
-    ef::launch_scatter_state(h->dim, h->lay, h->Ubuf[h->cur], h->orig_dev, h->aos_dev, h->st);
-    EF_CUDA(cudaMemcpyAsync(U, h->aos_dev, sizeof(double) * NV * h->n_global, cudaMemcpyDeviceToHost, h->st));
-    EF_CUDA(cudaStreamSynchronize(h->st));
-    return EF_OK;
-  }
-  std::vector<double> soa((size_t)NV * h->NP);
-  EF_CUDA(cudaMemcpyAsync(soa.data(), h->Ubuf[h->cur], sizeof(double) * NV * h->NP, cudaMemcpyDeviceToHost, h->st));
-  EF_CUDA(cudaStreamSynchronize(h->st));
-  for (int64_t i = 0; i < h->n_owned; ++i)
-    for (int k = 0; k < NV; ++k) U[h->orig_host[i] * NV + k] = soa[(size_t)k * h->NP + i];
-  return EF_OK;
-}
-
-// ---- one forward-Euler stage (stepper.py:508-610) --------------------------------
 static int flush_timers(ef_solver* h) {
   for (int q = 0; q < h->ring_used; ++q) {
     EF_CUDA(cudaEventSynchronize(h->ring[q][7]));
@@ -521,30 +461,119 @@ static int mark(ef_solver* h, int k) {
   return EF_OK;
 }
 
-static int run_stage(ef_solver* h, const double* U, const double* U0, double* Uout, StageParams sp) {
-  const int D = h->dim;
-  const bool want_tau = sp.tau_mode == ef::TAU_CFL;
-  EF_TRY(mark(h, 0));
-  EF_TRY(mark(h, 1));  // step0 is fused into the previous stage's final kernel
-  ef::launch_edge_visc(D, h->lay, h->gas, U, h->w, want_tau, h->st);
-  EF_TRY(mark(h, 2));
-  ef::launch_row_visc(D, h->lay, h->gas, U, h->w, want_tau, h->st);
-  EF_TRY(mark(h, 3));
-  ef::launch_low_order(D, h->lay, h->gas, U, h->w, sp, h->st);
-  EF_TRY(mark(h, 4));
-  if (h->passes > 0) {
-    ef::launch_limiter0(D, h->lay, h->gas, U, h->w, sp, h->st);
-    EF_TRY(mark(h, 5));
-    for (int p = 0; p + 1 < h->passes; ++p) ef::launch_pass(D, h->lay, h->gas, U, h->w, sp, p, h->st);
-    EF_TRY(mark(h, 6));
-  } else {
-    EF_TRY(mark(h, 5));
-    EF_TRY(mark(h, 6));
+// Halo exchange of one field (exchange.py:145-157 semantics: owners' values
+// overwrite the ghost copies).  rows: ncomp doubles per row; slots: ncomp == 1.
+// `field(r)` returns rank r's device array (index into Driver::hs).
+template <class FieldOf>
+static int exchange(Driver& d, bool slots, int ncomp, FieldOf field) {
+  if (!d.multi()) return EF_OK;
+  for (size_t r = 0; r < d.hs.size(); ++r) {
+    ef_solver* h = d.hs[r];
+    if (slots)
+      ef::launch_pack_pos(field(r), h->send_pos, h->n_send_pos, h->sendbuf, h->st);
+    else
+      ef::launch_pack_rows(field(r), ncomp, h->NP, h->send_rows, h->n_send_rows, h->sendbuf, h->st);
   }
-  ef::launch_final(D, h->lay, h->gas, U, U0, Uout, h->w, sp, h->st);
-  EF_TRY(mark(h, 7));
-  EF_CUDA(cudaGetLastError());
-  h->n_euler++;
+  if (d.group) {
+    for (ef_solver* h : d.hs)
+      for (int q = 0; q < h->nranks; ++q) {
+        const int64_t cnt = slots ? h->xr_slots[q] : h->xr_rows[q] * ncomp;
+        if (cnt == 0) continue;
+        ef_solver* src = d.hs[q];
+        const int64_t soff = slots ? src->os_slots[h->rank] : src->os_rows[h->rank] * ncomp;
+        const int64_t roff = slots ? h->or_slots[q] : h->or_rows[q] * ncomp;
+        EF_CUDA(cudaMemcpyAsync(h->recvbuf + roff, src->sendbuf + soff, sizeof(double) * cnt,
+                                cudaMemcpyDeviceToDevice, h->st));
+      }
+  } else {
+    ef_solver* h = d.h0();
+    EF_NCCL(nccl().GroupStart());
+    for (int q = 0; q < h->nranks; ++q) {
+      const int64_t sc = slots ? h->xs_slots[q] : h->xs_rows[q] * ncomp;
+      const int64_t rc = slots ? h->xr_slots[q] : h->xr_rows[q] * ncomp;
+      const int64_t so = slots ? h->os_slots[q] : h->os_rows[q] * ncomp;
+      const int64_t ro = slots ? h->or_slots[q] : h->or_rows[q] * ncomp;
+      if (sc) EF_NCCL(nccl().Send(h->sendbuf + so, (size_t)sc, ncclFloat64, q, h->comm, h->st));
+      if (rc) EF_NCCL(nccl().Recv(h->recvbuf + ro, (size_t)rc, ncclFloat64, q, h->comm, h->st));
+    }
+    EF_NCCL(nccl().GroupEnd());
+  }
+  for (size_t r = 0; r < d.hs.size(); ++r) {
+    ef_solver* h = d.hs[r];
+    if (slots)
+      ef::launch_unpack_pos(field(r), h->recv_pos, h->n_recv_pos, h->recvbuf, h->st);
+    else
+      ef::launch_unpack_rows(field(r), ncomp, h->NP, h->recv_rows, h->n_recv_rows, h->recvbuf, h->st);
+    h->sync_count++;
+    h->sync_volume += slots ? h->n_recv_pos : h->n_recv_rows * ncomp;
+  }
+  return EF_OK;
+}
+
+// allreduce_min of the CFL bound (exchange.py:160-165): bit patterns of
+// positive doubles order like their values, so a uint64 min is exact.
+static int allreduce_tau(Driver& d) {
+  if (!d.multi()) return EF_OK;
+  if (d.group) {
+    ef::launch_group_min(d.bits_dev, (int)d.hs.size(), d.h0()->st);
+    EF_CUDA(cudaGetLastError());
+    return EF_OK;
+  }
+  ef_solver* h = d.h0();
+  EF_NCCL(nccl().AllReduce(h->w.tau_min_bits, h->w.tau_min_bits, 1, ncclUint64, ncclMin, h->comm, h->st));
+  return EF_OK;
+}
+
+struct StageIO {
+  const double* U;
+  const double* U0;
+  double* Uout;
+};
+
+static int run_stage(Driver& d, const std::vector<StageIO>& io, StageParams sp) {
+  const bool want_tau = sp.tau_mode == ef::TAU_CFL;
+  auto each = [&](auto fn) {
+    for (size_t r = 0; r < d.hs.size(); ++r) fn(d.hs[r], io[r]);
+  };
+  ef_solver* t = d.h0();  // timers are kept on the first handle
+  EF_TRY(mark(t, 0));
+  EF_TRY(mark(t, 1));  // step0 is fused into the previous stage's final kernel
+  each([&](ef_solver* h, const StageIO& x) { ef::launch_edge_visc(h->dim, h->lay, h->gas, x.U, h->w, want_tau, h->st); });
+  EF_TRY(mark(t, 2));
+  each([&](ef_solver* h, const StageIO& x) { ef::launch_row_visc(h->dim, h->lay, h->gas, x.U, h->w, want_tau, h->st); });
+  EF_TRY(exchange(d, false, 1, [&d](size_t r) { return d.hs[r]->w.alpha; }));
+  if (want_tau) EF_TRY(allreduce_tau(d));
+  EF_TRY(mark(t, 3));
+  each([&](ef_solver* h, const StageIO& x) { ef::launch_low_order(h->dim, h->lay, h->gas, x.U, h->w, sp, h->st); });
+  EF_TRY(exchange(d, false, t->nvar, [&d](size_t r) { return d.hs[r]->w.R; }));
+  EF_TRY(mark(t, 4));
+  if (t->passes > 0) {
+    each([&](ef_solver* h, const StageIO& x) { ef::launch_limiter0(h->dim, h->lay, h->gas, x.U, h->w, sp, h->st); });
+    EF_TRY(exchange(d, true, 1, [&d](size_t r) { return d.hs[r]->w.l; }));
+    EF_TRY(mark(t, 5));
+    for (int p = 0; p + 1 < t->passes; ++p) {
+      each([&](ef_solver* h, const StageIO& x) { ef::launch_pass(h->dim, h->lay, h->gas, x.U, h->w, sp, p, h->st); });
+      EF_TRY(exchange(d, true, 1, [&d, p](size_t r) { return d.hs[r]->w.l + (size_t)(p + 1) * d.hs[r]->NPL; }));
+    }
+    EF_TRY(mark(t, 6));
+  } else {
+    EF_TRY(mark(t, 5));
+    EF_TRY(mark(t, 6));
+  }
+  each([&](ef_solver* h, const StageIO& x) {
+    ef::launch_final(h->dim, h->lay, h->gas, x.U, x.U0, x.Uout, h->w, sp, h->st);
+  });
+  if (d.multi()) {
+    EF_TRY(exchange(d, false, t->nvar, [&io](size_t r) { return io[r].Uout; }));
+    each([&](ef_solver* h, const StageIO& x) {  // step0 of the ghost rows
+      ef::launch_nodal(h->dim, h->lay, h->gas, x.Uout, h->w, h->n_owned, h->n_local, h->st);
+    });
+  }
+  EF_TRY(mark(t, 7));
+  for (ef_solver* h : d.hs) {
+    EF_CUDA(cudaGetLastError());
+    h->n_euler++;
+  }
   return EF_OK;
 }
 
@@ -560,82 +589,249 @@ static StageParams stage_params(ef_solver* h, int mode, double tau, double tau_m
   return sp;
 }
 
-static int reset_flags(ef_solver* h) {
-  EF_CUDA(cudaMemsetAsync(h->w.err, 0, sizeof(int), h->st));
-  EF_CUDA(cudaMemsetAsync(h->w.bad_gid, 0xff, sizeof(unsigned long long), h->st));
-  return EF_OK;
-}
-
-static int finish(ef_solver* h, int out_buf, double* tau_used) {
-  EF_TRY(readback(h));
-  const int err = h->rb->err;
-  if (err & ef::ERR_TAU_UNBOUNDED) return fail(EF_ERR_TAU_UNBOUNDED, "constant field, the time step bound is unbounded");
-  if (err & ef::ERR_PROJECT) return fail(EF_ERR_INADMISSIBLE, "projected state requires rho > 0 and p > 0");
-  if (err & ef::ERR_BAD_STATE) {
-    const int64_t g = (int64_t)h->rb->bad;
-    int64_t orig = -1;
-    for (int64_t i = 0; i < h->n_local; ++i)
-      if (h->gid_host[i] == g) orig = h->orig_host[i];
-    h->bad_node = orig;
-    return fail(EF_ERR_INADMISSIBLE, "inadmissible state at node " + std::to_string(orig));
+static int reset_flags(Driver& d) {
+  for (ef_solver* h : d.hs) {
+    EF_CUDA(cudaMemsetAsync(h->w.err, 0, sizeof(int), h->st));
+    EF_CUDA(cudaMemsetAsync(h->w.bad_gid, 0xff, sizeof(unsigned long long), h->st));
   }
-  h->cur = out_buf;
-  h->tau_last = h->rb->tau;
-  if (tau_used) *tau_used = h->rb->tau;
   return EF_OK;
 }
 
-static int euler_async(ef_solver* h, int32_t has_tau, double tau, double tau_max, int* out_buf) {
-  const int in = h->cur, out = (h->cur + 1) % 3;
-  EF_TRY(reset_flags(h));
-  StageParams sp = stage_params(h, has_tau ? ef::TAU_GIVEN : ef::TAU_CFL, tau, tau_max, -1.0);
-  EF_TRY(run_stage(h, h->Ubuf[in], h->Ubuf[in], h->Ubuf[out], sp));
+static int euler_async(Driver& d, int32_t has_tau, double tau, double tau_max, int* out_buf) {
+  const int in = d.h0()->cur, out = (in + 1) % 3;
+  EF_TRY(reset_flags(d));
+  std::vector<StageIO> io;
+  for (ef_solver* h : d.hs) io.push_back({h->Ubuf[in], h->Ubuf[in], h->Ubuf[out]});
+  StageParams sp = stage_params(d.h0(), has_tau ? ef::TAU_GIVEN : ef::TAU_CFL, tau, tau_max, -1.0);
+  EF_TRY(run_stage(d, io, sp));
   *out_buf = out;
   return EF_OK;
 }
 
-static int rk3_async(ef_solver* h, int32_t has_tau, double tau, double tau_max, int* out_buf) {
-  const int u0 = h->cur, a = (h->cur + 1) % 3, b = (h->cur + 2) % 3;
-  EF_TRY(reset_flags(h));
-  StageParams s1 = stage_params(h, has_tau ? ef::TAU_GIVEN : ef::TAU_CFL, tau, tau_max, -1.0);
-  EF_TRY(run_stage(h, h->Ubuf[u0], h->Ubuf[u0], h->Ubuf[a], s1));
-  StageParams s2 = stage_params(h, ef::TAU_DEVICE, 0.0, 0.0, 0.25);
-  EF_TRY(run_stage(h, h->Ubuf[a], h->Ubuf[u0], h->Ubuf[b], s2));
-  StageParams s3 = stage_params(h, ef::TAU_DEVICE, 0.0, 0.0, 2.0 / 3.0);
-  EF_TRY(run_stage(h, h->Ubuf[b], h->Ubuf[u0], h->Ubuf[a], s3));
+static int rk3_async(Driver& d, int32_t has_tau, double tau, double tau_max, int* out_buf) {
+  const int u0 = d.h0()->cur, a = (u0 + 1) % 3, b = (u0 + 2) % 3;
+  EF_TRY(reset_flags(d));
+  auto io_of = [&](int in, int out) {
+    std::vector<StageIO> io;
+    for (ef_solver* h : d.hs) io.push_back({h->Ubuf[in], h->Ubuf[u0], h->Ubuf[out]});
+    return io;
+  };
+  EF_TRY(run_stage(d, io_of(u0, a), stage_params(d.h0(), has_tau ? ef::TAU_GIVEN : ef::TAU_CFL, tau, tau_max, -1.0)));
+  EF_TRY(run_stage(d, io_of(a, b), stage_params(d.h0(), ef::TAU_DEVICE, 0.0, 0.0, 0.25)));        // stepper.py:632
+  EF_TRY(run_stage(d, io_of(b, a), stage_params(d.h0(), ef::TAU_DEVICE, 0.0, 0.0, 2.0 / 3.0)));   // stepper.py:635
   *out_buf = a;
   return EF_OK;
 }
 
-int ef_euler_step(ef_solver* h, int32_t has_tau, double tau, double tau_max, double* tau_used) {
+static int readback(ef_solver* h) {
+  EF_CUDA(cudaMemcpyAsync(&h->rb->tau, h->w.tau, sizeof(double), cudaMemcpyDeviceToHost, h->st));
+  EF_CUDA(cudaMemcpyAsync(&h->rb->err, h->w.err, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+  EF_CUDA(cudaMemcpyAsync(&h->rb->bad, h->w.bad_gid, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
+  EF_CUDA(cudaStreamSynchronize(h->st));
+  EF_CUDA(cudaGetLastError());
+  return EF_OK;
+}
+
+// Reads the step's flags (made identical on every rank: NCCL max / min, or a
+// host reduction over the group) and commits the output buffer on success.
+static int finish(Driver& d, int out_buf, double* tau_used) {
+  ef_solver* h0 = d.h0();
+  if (d.multi() && !d.group) {
+    EF_NCCL(nccl().AllReduce(h0->w.err, h0->w.err, 1, ncclInt32, ncclMax, h0->comm, h0->st));
+    EF_NCCL(nccl().AllReduce(h0->w.bad_gid, h0->w.bad_gid, 1, ncclUint64, ncclMin, h0->comm, h0->st));
+  }
+  int err = 0;
+  unsigned long long bad = ~0ull;
+  for (ef_solver* h : d.hs) {
+    EF_TRY(readback(h));
+    err |= h->rb->err;
+    bad = std::min(bad, h->rb->bad);
+  }
+  if (err & ef::ERR_TAU_UNBOUNDED) return fail(EF_ERR_TAU_UNBOUNDED, "constant field, the time step bound is unbounded");
+  if (err & ef::ERR_PROJECT) return fail(EF_ERR_INADMISSIBLE, "projected state requires rho > 0 and p > 0");
+  if (err & ef::ERR_BAD_STATE) {
+    int64_t orig = -1;  // original id of the smallest inadmissible CM id (any local copy)
+    for (ef_solver* h : d.hs)
+      for (int64_t i = 0; i < h->n_local && orig < 0; ++i)
+        if (h->gid_host[i] == (int64_t)bad) orig = h->orig_host[i];
+    for (ef_solver* h : d.hs) h->bad_node = orig;
+    return fail(EF_ERR_INADMISSIBLE, "inadmissible state at node " + std::to_string(orig));
+  }
+  for (ef_solver* h : d.hs) {
+    h->cur = out_buf;
+    h->tau_last = h0->rb->tau;
+  }
+  if (tau_used) *tau_used = h0->rb->tau;
+  return EF_OK;
+}
+
+static int set_state_all(Driver& d, const double* U) {
+  int bad = 0;
+  for (ef_solver* h : d.hs) {
+    const int spare = (h->cur + 1) % 3;
+    EF_CUDA(cudaMemsetAsync(h->w.err, 0, sizeof(int), h->st));
+    EF_CUDA(cudaMemcpyAsync(h->aos_dev, U, sizeof(double) * h->nvar * h->n_global, cudaMemcpyHostToDevice, h->st));
+    ef::launch_gather_state(h->dim, h->lay, h->aos_dev, h->orig_dev, h->Ubuf[spare], h->w.err, h->st);
+    EF_TRY(readback(h));
+    bad |= h->rb->err;
+  }
+  if (bad) return fail(EF_ERR_INADMISSIBLE, "initial state is not admissible");
+  for (ef_solver* h : d.hs) {
+    h->cur = (h->cur + 1) % 3;
+    h->pending_out = -1;
+    ef::launch_nodal(h->dim, h->lay, h->gas, h->Ubuf[h->cur], h->w, 0, h->lay.n_local, h->st);
+    EF_CUDA(cudaGetLastError());
+  }
+  return EF_OK;
+}
+
+static int get_state_one(ef_solver* h, double* U) {
+  const int NV = h->nvar;
+  if (h->nranks == 1) {
+    ef::launch_scatter_state(h->dim, h->lay, h->Ubuf[h->cur], h->orig_dev, h->aos_dev, h->st);
+    EF_CUDA(cudaMemcpyAsync(U, h->aos_dev, sizeof(double) * NV * h->n_global, cudaMemcpyDeviceToHost, h->st));
+    EF_CUDA(cudaStreamSynchronize(h->st));
+    return EF_OK;
+  }
+  std::vector<double> soa((size_t)NV * h->NP);
+  EF_CUDA(cudaMemcpyAsync(soa.data(), h->Ubuf[h->cur], sizeof(double) * NV * h->NP, cudaMemcpyDeviceToHost, h->st));
+  EF_CUDA(cudaStreamSynchronize(h->st));
+  for (int64_t i = 0; i < h->n_owned; ++i)
+    for (int k = 0; k < NV; ++k) U[h->orig_host[i] * NV + k] = soa[(size_t)k * h->NP + i];
+  return EF_OK;
+}
+
+// ---------------------------------------------------------------- C-ABI
+struct ef_plan {
+  ef::Plan p;
+};
+
+extern "C" {
+
+const char* ef_last_error(void) { return g_err.c_str(); }
+
+int ef_nccl_unique_id(void* out128) {
+  if (!out128) return fail(EF_ERR_ARG, "null argument");
+  if (!nccl().ok) return fail(EF_ERR_NCCL, "libnccl.so.2 could not be loaded");
+  ncclUniqueId id;
+  EF_NCCL(nccl().GetUniqueId(&id));
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  std::memcpy(out128, &id, sizeof id);
+  return EF_OK;
+}
+
+int ef_create(const ef_matrices* mat, const ef_params* prm, const ef_boundary* bc, const ef_dist* dist,
+              ef_solver** out) {
+  if (!mat || !prm || !out) return fail(EF_ERR_ARG, "null argument");
+  *out = nullptr;
+  if (!(prm->c_cfl > 0.0 && prm->c_cfl <= 1.0)) return fail(EF_ERR_ARG, "c_cfl must lie in (0, 1]");
+  if (prm->limiter_passes < 0) return fail(EF_ERR_ARG, "limiter_passes must be >= 0");
+  if (prm->newton_steps < 0) return fail(EF_ERR_ARG, "newton_steps must be >= 0");
+  if (mat->dim != 2 && mat->dim != 3) return fail(EF_ERR_ARG, "dim must be 2 or 3");
+  if (mat->n <= 0) return fail(EF_ERR_ARG, "empty mesh");
+  if (dist && (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks))
+    return fail(EF_ERR_ARG, "bad rank/nranks");
+  ef_solver* h = new ef_solver();
+  h->dim = mat->dim;
+  h->nvar = mat->dim + 2;
+  h->passes = prm->limiter_passes;
+  h->newton = prm->newton_steps;
+  h->c_cfl = prm->c_cfl;
+  h->gas = make_gas(prm);
+  h->rank = dist ? dist->rank : 0;
+  h->nranks = dist ? dist->nranks : 1;
+  h->device = dist ? dist->device : 0;
+  auto bail = [&](int rc) {
+    std::string msg = g_err;
+    delete h;
+    g_err = msg;
+    return rc;
+  };
+  cudaError_t e = cudaSetDevice(h->device);
+  if (e != cudaSuccess) return bail(fail(EF_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e)));
+  if (dist && dist->stream) {
+    h->st = (cudaStream_t)dist->stream;
+  } else {
+    e = cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return bail(fail(EF_ERR_CUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(e)));
+    h->own_stream = true;
+  }
+  int rc = build(h, mat, bc, dist);
+  if (rc != EF_OK) return bail(rc);
+  if (h->nranks > 1 && dist->nccl_id) {
+    if (!nccl().ok) return bail(fail(EF_ERR_NCCL, "libnccl.so.2 could not be loaded"));
+    ncclUniqueId id;
+    std::memcpy(&id, dist->nccl_id, sizeof id);
+    ncclResult_t r = nccl().CommInitRank(&h->comm, h->nranks, id, h->rank);
+    if (r != ncclSuccess) return bail(fail(EF_ERR_NCCL, std::string("ncclCommInitRank: ") + nccl().GetErrorString(r)));
+    h->use_nccl = true;
+  }
+  *out = h;
+  return EF_OK;
+}
+
+int ef_destroy(ef_solver* h) {
+  if (h) {
+    cudaSetDevice(h->device);
+    cudaStreamSynchronize(h->st);
+    delete h;
+  }
+  return EF_OK;
+}
+
+static int single_driver(ef_solver* h, Driver& d) {
   if (!h) return fail(EF_ERR_ARG, "null handle");
+  if (h->nranks > 1 && !h->use_nccl)
+    return fail(EF_ERR_ARG, "a rank created without nccl_id must be stepped through an ef_group");
   cudaSetDevice(h->device);
+  d.hs = {h};
+  d.group = false;
+  return EF_OK;
+}
+
+int ef_set_state(ef_solver* h, const double* U) {
+  if (!h || !U) return fail(EF_ERR_ARG, "null argument");
+  cudaSetDevice(h->device);
+  Driver d;
+  d.hs = {h};
+  return set_state_all(d, U);
+}
+
+int ef_get_state(ef_solver* h, double* U) {
+  if (!h || !U) return fail(EF_ERR_ARG, "null argument");
+  cudaSetDevice(h->device);
+  return get_state_one(h, U);
+}
+
+int ef_euler_step(ef_solver* h, int32_t has_tau, double tau, double tau_max, double* tau_used) {
+  Driver d;
+  EF_TRY(single_driver(h, d));
   int out;
-  EF_TRY(euler_async(h, has_tau, tau, tau_max, &out));
-  return finish(h, out, tau_used);
+  EF_TRY(euler_async(d, has_tau, tau, tau_max, &out));
+  return finish(d, out, tau_used);
 }
 
 int ef_ssp_rk3_step(ef_solver* h, int32_t has_tau, double tau, double tau_max, double* tau_used) {
-  if (!h) return fail(EF_ERR_ARG, "null handle");
-  cudaSetDevice(h->device);
+  Driver d;
+  EF_TRY(single_driver(h, d));
   int out;
-  EF_TRY(rk3_async(h, has_tau, tau, tau_max, &out));
-  return finish(h, out, tau_used);
+  EF_TRY(rk3_async(d, has_tau, tau, tau_max, &out));
+  return finish(d, out, tau_used);
 }
 
 int ef_ssp_rk3_step_async(ef_solver* h, int32_t has_tau, double tau, double tau_max) {
-  if (!h) return fail(EF_ERR_ARG, "null handle");
-  cudaSetDevice(h->device);
+  Driver d;
+  EF_TRY(single_driver(h, d));
   if (h->pending_out >= 0) h->cur = h->pending_out;  // chain on the unchecked result
   int out;
-  EF_TRY(rk3_async(h, has_tau, tau, tau_max, &out));
+  EF_TRY(rk3_async(d, has_tau, tau, tau_max, &out));
   h->pending_out = out;
   return EF_OK;
 }
 
 int ef_sync(ef_solver* h, double* tau_used) {
-  if (!h) return fail(EF_ERR_ARG, "null handle");
-  cudaSetDevice(h->device);
+  Driver d;
+  EF_TRY(single_driver(h, d));
   if (h->pending_out < 0) {
     EF_CUDA(cudaStreamSynchronize(h->st));
     if (tau_used) *tau_used = h->tau_last;
@@ -643,7 +839,7 @@ int ef_sync(ef_solver* h, double* tau_used) {
   }
   const int out = h->pending_out;
   h->pending_out = -1;
-  return finish(h, out, tau_used);
+  return finish(d, out, tau_used);
 }
 
 int64_t ef_bad_node(const ef_solver* h) { return h ? h->bad_node : -1; }
@@ -664,8 +860,8 @@ int ef_phase_times(ef_solver* h, double* s7) {
 int ef_counters(ef_solver* h, int64_t* out3) {
   if (!h || !out3) return fail(EF_ERR_ARG, "null argument");
   out3[0] = h->n_euler;
-  out3[1] = 0;
-  out3[2] = 0;
+  out3[1] = h->sync_count;
+  out3[2] = h->sync_volume;
   return EF_OK;
 }
 
@@ -745,6 +941,128 @@ int ef_state_device_ptr(ef_solver* h, void** dev_ptr, int64_t* stride) {
   *dev_ptr = h->Ubuf[h->cur];
   *stride = h->NP;
   return EF_OK;
+}
+
+// ---- same-device group: all ranks of a partition in one process/GPU
+int ef_group_create(ef_solver** hs, int32_t n, ef_group** out) {
+  if (!hs || !out || n < 1) return fail(EF_ERR_ARG, "null argument");
+  for (int r = 0; r < n; ++r) {
+    if (!hs[r] || hs[r]->rank != r || hs[r]->nranks != n) return fail(EF_ERR_ARG, "group needs ranks 0..n-1 of one partition");
+    if (hs[r]->device != hs[0]->device) return fail(EF_ERR_ARG, "group ranks must share one device");
+    if (hs[r]->use_nccl) return fail(EF_ERR_ARG, "group ranks must be created without nccl_id");
+  }
+  ef_group* g = new ef_group();
+  g->hs.assign(hs, hs + n);
+  cudaSetDevice(hs[0]->device);
+  for (int r = 1; r < n; ++r) {  // one stream for the whole group: ordered phases, no waiting kernels
+    cudaStreamSynchronize(hs[r]->st);
+    if (hs[r]->own_stream && hs[r]->st && hs[r]->st != hs[0]->st) cudaStreamDestroy(hs[r]->st);
+    hs[r]->own_stream = false;
+    hs[r]->st = hs[0]->st;
+  }
+  std::vector<unsigned long long*> bits;
+  for (auto* h : g->hs) bits.push_back(h->w.tau_min_bits);
+  cudaError_t e = cudaMalloc(&g->bits_dev, sizeof(unsigned long long*) * n);
+  if (e == cudaSuccess) e = cudaMemcpy(g->bits_dev, bits.data(), sizeof(unsigned long long*) * n, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    delete g;
+    return fail(EF_ERR_CUDA, std::string("group setup: ") + cudaGetErrorString(e));
+  }
+  *out = g;
+  return EF_OK;
+}
+
+int ef_group_destroy(ef_group* g) {
+  if (g) {
+    if (g->bits_dev) cudaFree(g->bits_dev);
+    delete g;
+  }
+  return EF_OK;
+}
+
+static Driver group_driver(ef_group* g) {
+  Driver d;
+  d.hs = g->hs;
+  d.group = true;
+  d.bits_dev = g->bits_dev;
+  cudaSetDevice(g->hs[0]->device);
+  return d;
+}
+
+int ef_group_set_state(ef_group* g, const double* U) {
+  if (!g || !U) return fail(EF_ERR_ARG, "null argument");
+  Driver d = group_driver(g);
+  return set_state_all(d, U);
+}
+
+int ef_group_get_state(ef_group* g, double* U) {
+  if (!g || !U) return fail(EF_ERR_ARG, "null argument");
+  for (ef_solver* h : g->hs) EF_TRY(get_state_one(h, U));
+  return EF_OK;
+}
+
+int ef_group_euler_step(ef_group* g, int32_t has_tau, double tau, double tau_max, double* tau_used) {
+  if (!g) return fail(EF_ERR_ARG, "null handle");
+  Driver d = group_driver(g);
+  int out;
+  EF_TRY(euler_async(d, has_tau, tau, tau_max, &out));
+  return finish(d, out, tau_used);
+}
+
+int ef_group_ssp_rk3_step(ef_group* g, int32_t has_tau, double tau, double tau_max, double* tau_used) {
+  if (!g) return fail(EF_ERR_ARG, "null handle");
+  Driver d = group_driver(g);
+  int out;
+  EF_TRY(rk3_async(d, has_tau, tau, tau_max, &out));
+  return finish(d, out, tau_used);
+}
+
+// ---- host-only partition plans (no CUDA; CPU tests)
+int ef_plan_build(const ef_matrices* mat, const ef_dist* dist, ef_plan** out) {
+  if (!mat || !dist || !out || !dist->cm_perm) return fail(EF_ERR_ARG, "null argument");
+  if (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks) return fail(EF_ERR_ARG, "bad rank/nranks");
+  ef_plan* p = new ef_plan();
+  if (!ef::build_plan(mat->n, mat->indptr, mat->indices, dist->cm_perm, dist->rank, dist->nranks, dist->ranges, p->p)) {
+    std::string msg = p->p.error;
+    delete p;
+    return fail(EF_ERR_ARG, msg);
+  }
+  *out = p;
+  return EF_OK;
+}
+
+int ef_plan_destroy(ef_plan* p) {
+  delete p;
+  return EF_OK;
+}
+
+int ef_plan_sizes(const ef_plan* p, int64_t* out4) {
+  if (!p || !out4) return fail(EF_ERR_ARG, "null argument");
+  out4[0] = p->p.n_owned;
+  out4[1] = p->p.n_local;
+  out4[2] = p->p.L;
+  out4[3] = p->p.nranks;
+  return EF_OK;
+}
+
+int64_t ef_plan_rows(const ef_plan* p, int32_t peer, int32_t recv, int64_t* out_gids, int64_t cap) {
+  if (!p || peer < 0 || peer >= p->p.nranks) return -1;
+  const auto& v = recv ? p->p.recv_rows[peer] : p->p.send_rows[peer];
+  if (out_gids)
+    for (int64_t k = 0; k < (int64_t)v.size() && k < cap; ++k) out_gids[k] = p->p.gid[v[k]];
+  return (int64_t)v.size();
+}
+
+int64_t ef_plan_slots(const ef_plan* p, int32_t peer, int32_t recv, int64_t* out_pairs, int64_t cap) {
+  if (!p || peer < 0 || peer >= p->p.nranks) return -1;
+  const auto& v = recv ? p->p.recv_slots[peer] : p->p.send_slots[peer];
+  if (out_pairs)
+    for (int64_t k = 0; k < (int64_t)v.size() && k < cap; ++k) {
+      const int64_t i = v[k] / 256, t = v[k] % 256;
+      out_pairs[2 * k] = p->p.gid[i];
+      out_pairs[2 * k + 1] = p->p.rcm[p->p.rptr[i] + t];
+    }
+  return (int64_t)v.size();
 }
 
 }  // extern "C"

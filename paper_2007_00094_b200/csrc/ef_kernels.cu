@@ -502,6 +502,41 @@ __global__ void __launch_bounds__(TPB, EF_MINB) k_final(Layout m, Gas g, const d
   w.phi[i] = ph;
 }
 
+// ---------------------------------------------------------------- halo packing
+// rows: buf[r * ncomp + k] <-> field[k * NP + idx[r]]; slots: buf[q] <-> arr[pos[q]]
+__global__ void k_pack_rows(const double* __restrict__ field, int ncomp, int64_t NP,
+                            const int32_t* __restrict__ idx, int64_t count, double* __restrict__ buf) {
+  const int64_t q = blockIdx.x * (int64_t)TPB + threadIdx.x;
+  if (q >= count * ncomp) return;
+  const int64_t r = q / ncomp;
+  const int k = (int)(q - r * ncomp);
+  buf[q] = field[k * NP + idx[r]];
+}
+__global__ void k_unpack_rows(double* __restrict__ field, int ncomp, int64_t NP,
+                              const int32_t* __restrict__ idx, int64_t count, const double* __restrict__ buf) {
+  const int64_t q = blockIdx.x * (int64_t)TPB + threadIdx.x;
+  if (q >= count * ncomp) return;
+  const int64_t r = q / ncomp;
+  const int k = (int)(q - r * ncomp);
+  field[k * NP + idx[r]] = buf[q];
+}
+__global__ void k_pack_pos(const double* __restrict__ arr, const int32_t* __restrict__ pos, int64_t count,
+                           double* __restrict__ buf) {
+  const int64_t q = blockIdx.x * (int64_t)TPB + threadIdx.x;
+  if (q < count) buf[q] = arr[pos[q]];
+}
+__global__ void k_unpack_pos(double* __restrict__ arr, const int32_t* __restrict__ pos, int64_t count,
+                             const double* __restrict__ buf) {
+  const int64_t q = blockIdx.x * (int64_t)TPB + threadIdx.x;
+  if (q < count) arr[pos[q]] = buf[q];
+}
+// min of the CFL bounds of every rank of a same-device group, written back to all
+__global__ void k_group_min(unsigned long long* const* bits, int n) {
+  unsigned long long v = ~0ull;
+  for (int r = 0; r < n; ++r) v = min(v, *bits[r]);
+  for (int r = 0; r < n; ++r) *bits[r] = v;
+}
+
 __global__ void k_pow(const double* __restrict__ x, double y, double* __restrict__ out, int64_t n) {
   const int64_t q = blockIdx.x * (int64_t)TPB + threadIdx.x;
   if (q < n) out[q] = ef_pow(x[q], y);
@@ -555,6 +590,23 @@ void launch_final(int dim, const Layout& m, const Gas& g, const double* U, const
                   double* Uout, Work w, StageParams sp, cudaStream_t st) {
   if (m.n_owned == 0) return;
   EF_DISPATCH(dim, k_final, grid_for(m.n_owned), m, g, U, U0, Uout, w, sp);
+}
+void launch_pack_rows(const double* field, int ncomp, int64_t NP, const int32_t* idx, int64_t count,
+                      double* buf, cudaStream_t st) {
+  if (count > 0) k_pack_rows<<<grid_for(count * ncomp), TPB, 0, st>>>(field, ncomp, NP, idx, count, buf);
+}
+void launch_unpack_rows(double* field, int ncomp, int64_t NP, const int32_t* idx, int64_t count,
+                        const double* buf, cudaStream_t st) {
+  if (count > 0) k_unpack_rows<<<grid_for(count * ncomp), TPB, 0, st>>>(field, ncomp, NP, idx, count, buf);
+}
+void launch_pack_pos(const double* arr, const int32_t* pos, int64_t count, double* buf, cudaStream_t st) {
+  if (count > 0) k_pack_pos<<<grid_for(count), TPB, 0, st>>>(arr, pos, count, buf);
+}
+void launch_unpack_pos(double* arr, const int32_t* pos, int64_t count, const double* buf, cudaStream_t st) {
+  if (count > 0) k_unpack_pos<<<grid_for(count), TPB, 0, st>>>(arr, pos, count, buf);
+}
+void launch_group_min(unsigned long long* const* bits_dev, int n, cudaStream_t st) {
+  k_group_min<<<1, 1, 0, st>>>(bits_dev, n);
 }
 void launch_pow(const double* x, double y, double* out, int64_t n, cudaStream_t st) {
   if (n <= 0) return;

@@ -118,5 +118,13 @@ void launch_pass(int dim, const Layout& m, const Gas& g, const double* U, Work w
 void launch_final(int dim, const Layout& m, const Gas& g, const double* U, const double* U0,
                   double* Uout, Work w, StageParams sp, cudaStream_t st);
 void launch_pow(const double* x, double y, double* out, int64_t n, cudaStream_t st);
+// halo exchange helpers
+void launch_pack_rows(const double* field, int ncomp, int64_t NP, const int32_t* idx, int64_t count,
+                      double* buf, cudaStream_t st);
+void launch_unpack_rows(double* field, int ncomp, int64_t NP, const int32_t* idx, int64_t count,
+                        const double* buf, cudaStream_t st);
+void launch_pack_pos(const double* arr, const int32_t* pos, int64_t count, double* buf, cudaStream_t st);
+void launch_unpack_pos(double* arr, const int32_t* pos, int64_t count, const double* buf, cudaStream_t st);
+void launch_group_min(unsigned long long* const* bits_dev, int n, cudaStream_t st);
 
 }  // namespace ef

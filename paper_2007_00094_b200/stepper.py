@@ -11,8 +11,11 @@ exchange.partition does, exchange.py:397-403) and marshals arrays.
 
 `lanes`, `workers`, `overlap` and `chunk_size` are accepted for signature
 compatibility; the reference's results are bitwise independent of them
-(test_stepper.py:106-128) and so are ours.  `ranks` > 1 requires one process
-per GPU under torch.distributed (see paper_2007_00094_b200.distributed).
+(test_stepper.py:106-128) and so are ours.  `ranks` > 1 partitions the mesh
+into contiguous Cuthill-McKee ranges with ghost layers exactly like the
+reference's simulated ranks (exchange.py:393-445) and steps them in lockstep
+on one device; one process per GPU with NCCL is
+paper_2007_00094_b200.distributed.DistributedSolver.
 """
 
 from __future__ import annotations
@@ -57,10 +60,11 @@ def cm_permutation(matrices):
     return cm_perm, cm_inv
 
 
-def _raise(code: int, h=None):
-    msg = _lib.last_error()
+def _raise(code: int, msg: Optional[str] = None):
     if code == _lib.EF_OK:
         return
+    if msg is None:
+        msg = _lib.last_error()
     if code == _lib.EF_ERR_ARG:
         raise ValueError(msg)
     if code == _lib.EF_ERR_INADMISSIBLE:
@@ -76,8 +80,8 @@ class Solver:
     def __init__(self, matrices, c_cfl: float = 0.9, limiter_passes: int = 2, newton_steps: int = 2,
                  lanes: int = 4, workers: int = 1, ranks: int = 1, overlap: bool = True,
                  chunk_size: int = 2048, boundary: Optional[BoundaryConditions] = None,
-                 gas: GasConstants = AIR, device: int = 0, stream=None, rank: int = 0,
-                 cm_perm: Optional[np.ndarray] = None):
+                 gas: GasConstants = AIR, device: int = 0, stream=None,
+                 cm_perm: Optional[np.ndarray] = None, ranges=None, nccl_rank=None):
         if not 0.0 < c_cfl <= 1.0:
             raise ValueError("c_cfl must lie in (0, 1]")
         if limiter_passes < 0:
@@ -93,7 +97,6 @@ class Solver:
         self.dim = int(matrices.dim)
         self.nvar = self.dim + 2
         self.ranks = ranks
-        self.rank = rank
         lib = _lib.load()
         if cm_perm is None:
             cm_perm, cm_inv = cm_permutation(matrices)
@@ -127,35 +130,71 @@ class Solver:
                 bcs.n_slip = len(boundary.slip_nodes)
                 bcs.slip = ptr(boundary.slip_nodes, np.int64)
                 bcs.slip_normals = ptr(boundary.slip_normals, np.float64)
-        # simulated ranks (the reference's `ranks`) do not change results; real
-        # multi-GPU ranks are set up by paper_2007_00094_b200.distributed
-        nranks = 1
         if stream is not None:
             stream = int(stream)
             if stream == 0:  # the legacy default stream (torch's default) is handle 1
                 stream = 1
-        dist = _lib.EfDist(int(rank), nranks, int(device), ptr(cm_perm, np.int64), None, None, stream)
-        h = ctypes.c_void_p()
-        rc = lib.ef_create(ctypes.byref(mats), ctypes.byref(prm), ctypes.byref(bcs),
-                           ctypes.byref(dist), ctypes.byref(h))
-        _raise(rc)
-        self._h = h
+        ranges = None if ranges is None else ptr(np.asarray(ranges, dtype=np.int64), np.int64)
+        self._handles = []
+        self._group = None
+        if nccl_rank is not None:
+            # one rank of a one-process-per-GPU NCCL job (paper_2007_00094_b200.distributed)
+            r, R, uid = nccl_rank
+            idbuf = ctypes.create_string_buffer(bytes(uid), 128)
+            keep.append(idbuf)
+            specs = [(int(r), int(R), ctypes.cast(idbuf, ctypes.c_void_p).value)]
+        else:
+            # ranks > 1: the reference's simulated ranks as a same-device group
+            R = max(1, int(ranks or 1))
+            specs = [(r, R, None) for r in range(R)]
+        for r, R, uid in specs:
+            dist = _lib.EfDist(r, R, int(device), ptr(cm_perm, np.int64), ranges, uid, stream)
+            h = ctypes.c_void_p()
+            rc = lib.ef_create(ctypes.byref(mats), ctypes.byref(prm), ctypes.byref(bcs),
+                               ctypes.byref(dist), ctypes.byref(h))
+            if rc != _lib.EF_OK:
+                msg = _lib.last_error()
+                self.close()
+                _raise(rc, msg)
+            self._handles.append(h)
+        if nccl_rank is None and len(self._handles) > 1:
+            arr = (ctypes.c_void_p * len(self._handles))(*[h.value for h in self._handles])
+            g = ctypes.c_void_p()
+            _raise(lib.ef_group_create(arr, len(self._handles), ctypes.byref(g)))
+            self._group = g
+        self._h = self._handles[0]
         del keep
         info = np.zeros(6, dtype=np.int64)
         lib.ef_info(self._h, info.ctypes.data)
         self.n_owned, self.n_local, self.pad_width, self.nnz_owned, self.standard_card = (
             int(x) for x in info[:5])
-        self.comm = SimpleNamespace(sync_count=0, sync_volume=0)
         self.n_euler_steps = 0
         self.tau_last = None
         self._timers_on = False
 
+    @property
+    def comm(self):
+        """sync_count / sync_volume of the halo exchanges (exchange.py:131-157)."""
+        tot = np.zeros(3, dtype=np.int64)
+        for h in self._handles:
+            c = np.zeros(3, dtype=np.int64)
+            _lib.load().ef_counters(h, c.ctypes.data)
+            tot[2] += c[2]
+            tot[1] = c[1]
+        return SimpleNamespace(sync_count=int(tot[1]), sync_volume=int(tot[2]))
+
     # ----- lifecycle ------------------------------------------------------
     def close(self):
-        h = getattr(self, "_h", None)
-        if h:
-            _lib.load().ef_destroy(h)
-            self._h = None
+        lib = _lib.load()
+        g = getattr(self, "_group", None)
+        if g:
+            lib.ef_group_destroy(g)
+            self._group = None
+        for h in getattr(self, "_handles", []):
+            if h:
+                lib.ef_destroy(h)
+        self._handles = []
+        self._h = None
 
     def __del__(self):
         try:
@@ -169,23 +208,29 @@ class Solver:
         U = np.ascontiguousarray(U, dtype=np.float64)
         if U.shape != (self.n, self.nvar):
             raise ValueError("state array has the wrong shape")
-        rc = _lib.load().ef_set_state(self._h, U.ctypes.data)
+        lib = _lib.load()
+        rc = (lib.ef_group_set_state(self._group, U.ctypes.data) if self._group
+              else lib.ef_set_state(self._h, U.ctypes.data))
         if rc == _lib.EF_ERR_INADMISSIBLE:
             raise AdmissibilityError("initial state is not admissible")
         _raise(rc)
 
     def get_state(self, out: Optional[np.ndarray] = None) -> np.ndarray:
-        """Owned states in original node order (stepper.py:330-336)."""
+        """States in original node order (stepper.py:330-336); on an NCCL rank
+        only the owned rows are filled (see distributed.DistributedSolver)."""
         if out is None:
-            out = np.empty((self.n, self.nvar))
-        _raise(_lib.load().ef_get_state(self._h, out.ctypes.data))
+            out = np.zeros((self.n, self.nvar))
+        lib = _lib.load()
+        _raise(lib.ef_group_get_state(self._group, out.ctypes.data) if self._group
+               else lib.ef_get_state(self._h, out.ctypes.data))
         return out
 
     # ----- stepping -------------------------------------------------------
     def euler_step(self, tau: Optional[float] = None, tau_max: float = np.inf) -> float:
         t = ctypes.c_double()
-        rc = _lib.load().ef_euler_step(self._h, 0 if tau is None else 1,
-                                       0.0 if tau is None else float(tau), float(tau_max), ctypes.byref(t))
+        lib = _lib.load()
+        args = (0 if tau is None else 1, 0.0 if tau is None else float(tau), float(tau_max), ctypes.byref(t))
+        rc = lib.ef_group_euler_step(self._group, *args) if self._group else lib.ef_euler_step(self._h, *args)
         _raise(rc)
         self.tau_last = t.value
         self.n_euler_steps += 1
@@ -193,8 +238,9 @@ class Solver:
 
     def ssp_rk3_step(self, tau: Optional[float] = None, tau_max: float = np.inf) -> float:
         t = ctypes.c_double()
-        rc = _lib.load().ef_ssp_rk3_step(self._h, 0 if tau is None else 1,
-                                         0.0 if tau is None else float(tau), float(tau_max), ctypes.byref(t))
+        lib = _lib.load()
+        args = (0 if tau is None else 1, 0.0 if tau is None else float(tau), float(tau_max), ctypes.byref(t))
+        rc = lib.ef_group_ssp_rk3_step(self._group, *args) if self._group else lib.ef_ssp_rk3_step(self._h, *args)
         _raise(rc)
         self.tau_last = t.value
         self.n_euler_steps += 3

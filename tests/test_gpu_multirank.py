@@ -1,0 +1,68 @@
+"""The multi-rank path (contiguous CM ranges, ghost rows with truncated
+stencils, halo exchanges of alpha / R / l / U, tau min-reduction) run as a
+same-device group: results must be bitwise identical to one rank, as the
+reference asserts for its simulated ranks (test_acceptance.py:293-311,
+test_stepper.py:106-128)."""
+
+import numpy as np
+import pytest
+
+import oracle as O
+from goldens import Golden
+from paper_2007_00094_b200 import Solver
+from paper_2007_00094_b200 import problems as P
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(mat, U0, bc, ranks, steps, mode="rk3", **kw):
+    s = Solver(mat, boundary=bc, ranks=ranks, **kw)
+    s.set_state(U0)
+    taus = [s.ssp_rk3_step() if mode == "rk3" else s.euler_step() for _ in range(steps)]
+    return taus, s.get_state(), s
+
+
+CASES = {
+    "c1": lambda: P.isentropic_vortex(24),
+    "c2": lambda: P.mach3_disc(20, seed=7),
+    "c3": lambda: P.sod_box(15, 4, 4, seed=3),
+    "c5": lambda: P.periodic_fourier_box(8, seed=2),
+}
+
+
+@pytest.mark.parametrize("case", sorted(CASES))
+@pytest.mark.parametrize("ranks", [2, 3, 5])
+def test_ranks_are_bitwise_identical(case, ranks):
+    ps = CASES[case]()
+    t1, U1, _ = _run(ps.matrices, ps.U0, ps.boundary, 1, 4, c_cfl=ps.c_cfl)
+    tR, UR, s = _run(ps.matrices, ps.U0, ps.boundary, ranks, 4, c_cfl=ps.c_cfl)
+    assert t1 == tR
+    assert np.array_equal(U1, UR)
+    assert s.comm.sync_count > 0 and s.comm.sync_volume > 0
+
+
+@pytest.mark.parametrize("passes", [0, 1, 3])
+def test_ranks_with_limiter_variants(passes):
+    ps = P.mach3_disc(20, seed=9)
+    t1, U1, _ = _run(ps.matrices, ps.U0, ps.boundary, 1, 3, limiter_passes=passes)
+    t4, U4, _ = _run(ps.matrices, ps.U0, ps.boundary, 4, 3, limiter_passes=passes)
+    assert t1 == t4 and np.array_equal(U1, U4)
+
+
+def test_ranks_match_reference_golden():
+    g = Golden("mach3_channel_r2")
+    s = Solver(g.matrices, ranks=3, **g.solver_kwargs())
+    taus, U = g.run(s)
+    assert np.array_equal(taus, g.taus) and np.array_equal(U, g.U_final)
+
+
+def test_ranks_euler_and_roundtrip():
+    ps = P.sod_box(11, 3, 3, seed=4)
+    s = Solver(ps.matrices, boundary=ps.boundary, ranks=4)
+    s.set_state(ps.U0)
+    assert np.array_equal(s.get_state(), ps.U0)
+    o = O.OracleSolver(ps.matrices, boundary=ps.boundary)
+    o.set_state(ps.U0)
+    for _ in range(3):
+        assert s.euler_step() == o.euler_step()
+    assert np.array_equal(s.get_state(), o.get_state())
