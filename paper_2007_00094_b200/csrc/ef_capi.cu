@@ -773,8 +773,9 @@ int ef_create(const ef_matrices* mat, const ef_params* prm, const ef_boundary* b
 int ef_destroy(ef_solver* h) {
   if (h) {
     cudaSetDevice(h->device);
-    cudaStreamSynchronize(h->st);
+    if (h->own_stream) cudaStreamSynchronize(h->st);  // a group rank borrows rank 0's stream
     delete h;
+    cudaGetLastError();  // teardown errors must not surface in a later call
   }
   return EF_OK;
 }
@@ -974,8 +975,11 @@ int ef_group_create(ef_solver** hs, int32_t n, ef_group** out) {
 
 int ef_group_destroy(ef_group* g) {
   if (g) {
+    cudaSetDevice(g->hs[0]->device);
+    cudaStreamSynchronize(g->hs[0]->st);
     if (g->bits_dev) cudaFree(g->bits_dev);
     delete g;
+    cudaGetLastError();
   }
   return EF_OK;
 }

@@ -190,7 +190,7 @@ class Solver:
         if g:
             lib.ef_group_destroy(g)
             self._group = None
-        for h in getattr(self, "_handles", []):
+        for h in reversed(getattr(self, "_handles", [])):  # rank 0 owns a group's stream: last
             if h:
                 lib.ef_destroy(h)
         self._handles = []
