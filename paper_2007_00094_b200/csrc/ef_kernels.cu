@@ -155,22 +155,11 @@ __global__ void __launch_bounds__(TPB, EF_MINB) k_row_visc(Layout m, Gas g, cons
     double fi[NV][D];
     flux<D>(Ui, g, fi);
     const double eor_i = w.eor[i];
-    double ep[NV];
-    {
-      const double re = Ui[0] * internal_energy<D>(Ui);
-      if (re <= 0.0) bad = true;
-      const double scale = dpow(re, g.neg_g_gp1_inv) * g.gp1_inv;  // physics.py:143
-      ep[0] = scale * Ui[D + 1];
-#pragma unroll
-      for (int a = 0; a < D; ++a) ep[1 + a] = (-scale) * Ui[1 + a];
-      ep[D + 1] = scale * Ui[0];
-    }
     double A = 0.0, B[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) B[k] = 0.0;
-    double* __restrict__ d = w.d;
-    auto v = [&](int s) -> double {
-      if (s == dg || s >= card) return 0.0;  // j == i and pads add exact zeros
+    for (int s = 0; s < card; ++s) {  // indicator: sequential over slots
+      if (s == dg) continue;  // j == i contributes exact zeros
       const int64_t p = base + (int64_t)s * 32;
       const int64_t j = m.col[p];
       double Uj[NV];
@@ -191,7 +180,12 @@ __global__ void __launch_bounds__(TPB, EF_MINB) k_row_visc(Layout m, Gas g, cons
         for (int a = 0; a < D; ++a) t = t + (fj[k][a] - fi[k][a]) * cc[a];
         B[k] = B[k] + t;
       }
-      return d[p];  // lower slots were filled by k_edge_visc
+    }
+    // d row sum over the L padded slots (lower slots were filled by k_edge_visc)
+    double* __restrict__ d = w.d;
+    auto v = [&](int s) -> double {
+      if (s == dg || s >= card) return 0.0;
+      return d[base + (int64_t)s * 32];
     };
     double res;
     if (L < 8) {  // numpy pairwise_sum, n < 8: sequential from +0
@@ -212,6 +206,17 @@ __global__ void __launch_bounds__(TPB, EF_MINB) k_row_visc(Layout m, Gas g, cons
     const double dii = -res;
     d[base + (int64_t)dg * 32] = dii;
     if (want_tau && dii < 0.0) cand = m.m_i[i] / (-2.0 * dii);
+    // IndicatorAccumulator.reset (harten_entropy_derivative, physics.py:133-148)
+    double ep[NV];
+    {
+      const double re = Ui[0] * internal_energy<D>(Ui);
+      if (re <= 0.0) bad = true;
+      const double scale = dpow(re, g.neg_g_gp1_inv) * g.gp1_inv;  // physics.py:143
+      ep[0] = scale * Ui[D + 1];
+#pragma unroll
+      for (int a = 0; a < D; ++a) ep[1 + a] = (-scale) * Ui[1 + a];
+      ep[D + 1] = scale * Ui[0];
+    }
     // IndicatorAccumulator.result, indicator.py:63-73
     double eb = 0.0;
 #pragma unroll
