@@ -224,7 +224,7 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
   // SELL-32 host images
   std::vector<int32_t> col(NPL);
   std::vector<uint8_t> tslot(NPL, 0), card(NP, 1), diag(NP, 0);
-  std::vector<double> c((size_t)D * NPL, 0.0), cT((size_t)D * NPL, 0.0), mij(NPL, 0.0);
+  std::vector<double> c((size_t)D * NPL, 0.0), mij(NPL, 0.0);
   std::vector<double> m_i(NP, 1.0), inv_m(NP, 1.0), lam(NP, 1.0);
   std::vector<int64_t> gid(NP, 0);
   for (int64_t i = 0; i < NP; ++i)
@@ -260,14 +260,6 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
     lam[i] = 1.0 / (double)den;  // stepper.py:214-215
     gid[i] = P.gid[i];
   }
-  for (int64_t i = 0; i < n_local; ++i) {
-    const int64_t cnt = P.rptr[i + 1] - P.rptr[i];
-    for (int64_t s = 0; s < cnt; ++s) {
-      const int64_t p = ef::sidx(i, (int)s, L);
-      const int64_t pt = ef::sidx(col[p], tslot[p], L);
-      for (int a = 0; a < D; ++a) cT[(size_t)a * NPL + p] = c[(size_t)a * NPL + pt];
-    }
-  }
   h->nnz_owned = nnz_owned;
   // upper-triangle edges with at least one owned endpoint (a ghost row's upper
   // edge to an owned row is that row's lower entry)
@@ -279,6 +271,27 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
         if (i >= n_local || !(s > diag[i] && s < card[i])) continue;
         if (i < n_owned || col[ef::sidx(i, s, L)] < n_owned) edges.push_back((int32_t)ef::sidx(i, s, L));
       }
+  // static edge geometry (riemann.py:131-136): n = c / |c|, |c| = sqrt(R1(c*c)),
+  // for c_ij and c_ji, evaluated with the reference's operation order
+  const int64_t NE = (int64_t)edges.size();
+  std::vector<double> egeo((size_t)2 * (D + 1) * std::max<int64_t>(NE, 1), 0.0);
+  for (int64_t e = 0; e < NE; ++e) {
+    const int64_t p = edges[e];
+    const int64_t pt = ef::sidx(col[p], tslot[p], L);
+    for (int dir = 0; dir < 2; ++dir) {
+      const int64_t q = dir ? pt : p;
+      volatile double ss = 0.0;  // ((0 + c0^2) + c1^2) + c2^2, no contraction
+      for (int a = 0; a < D; ++a) {
+        volatile double sq = c[(size_t)a * NPL + q] * c[(size_t)a * NPL + q];
+        ss = ss + sq;
+      }
+      const double nrm = std::sqrt((double)ss);
+      const int base = dir * (D + 1);
+      for (int a = 0; a < D; ++a)
+        egeo[(size_t)(base + a) * NE + e] = nrm > 0.0 ? c[(size_t)a * NPL + q] / nrm : (a == 0 ? 1.0 : 0.0);
+      egeo[(size_t)(base + D) * NE + e] = nrm;
+    }
+  }
   // boundary data (stepper.py:258-267): owned rows only
   std::vector<int8_t> bc_kind(NP, 0);
   std::vector<double> bc_n((size_t)D * NP, 0.0);
@@ -343,7 +356,7 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
   m.n_owned = n_owned;
   int32_t* d_col;
   uint8_t *d_tslot, *d_card, *d_diag;
-  double *d_c, *d_cT, *d_mij, *d_mi, *d_invm, *d_lam, *d_bcn;
+  double *d_c, *d_egeo, *d_mij, *d_mi, *d_invm, *d_lam, *d_bcn;
   int64_t* d_gid;
   int8_t* d_bck;
   int32_t* d_edges;
@@ -352,7 +365,7 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
   EF_TRY(upload(h, &d_card, card));
   EF_TRY(upload(h, &d_diag, diag));
   EF_TRY(upload(h, &d_c, c));
-  EF_TRY(upload(h, &d_cT, cT));
+  EF_TRY(upload(h, &d_egeo, egeo));
   EF_TRY(upload(h, &d_mij, mij));
   EF_TRY(upload(h, &d_mi, m_i));
   EF_TRY(upload(h, &d_invm, inv_m));
@@ -366,7 +379,7 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
   m.card = d_card;
   m.diag = d_diag;
   m.c = d_c;
-  m.cT = d_cT;
+  m.egeo = d_egeo;
   m.mij = d_mij;
   m.m_i = d_mi;
   m.inv_m = d_invm;

@@ -107,17 +107,18 @@ __global__ void __launch_bounds__(TPB, EF_MINB) k_edge_visc(Layout m, Gas g, con
   const int64_t p = m.edges[e];
   const int64_t i = (int64_t)fdiv((uint32_t)p, m.slab) * 32 + (p & 31);
   const int64_t j = m.col[p];
-  const int64_t NP = m.NP, NPL = NP * m.L;
-  double Ui[NV], Uj[NV], cc[D], ct[D];
+  const int64_t NP = m.NP, NE = m.n_edges;
+  double Ui[NV], Uj[NV], nij[D], nji[D];
   load_node<NV>(U, NP, i, Ui);
   load_node<NV>(U, NP, j, Uj);
 #pragma unroll
   for (int a = 0; a < D; ++a) {
-    cc[a] = m.c[a * NPL + p];
-    ct[a] = m.cT[a * NPL + p];
+    nij[a] = m.egeo[a * NE + e];
+    nji[a] = m.egeo[(D + 1 + a) * NE + e];
   }
+  const double norm_ij = m.egeo[D * NE + e], norm_ji = m.egeo[(2 * D + 1) * NE + e];
   bool bad = false;
-  const double dv = d_ij_low<D>(Ui, Uj, cc, ct, g, bad);
+  const double dv = d_ij_geo<D>(Ui, Uj, nij, norm_ij, nji, norm_ji, g, bad);
   // d is symmetric by construction (riemann.py:139-142): the value is also
   // the lower-triangle entry of row j, written straight to its slot (the
   // reference's mirror, stepper.py:427-434, without a gather)

@@ -51,7 +51,7 @@ struct Layout {
   const uint8_t* card;   // [NP] valid slots in the (possibly truncated) stencil
   const uint8_t* diag;   // [NP] slot of the diagonal
   const double* c;       // [D][NP*L]  c_ij
-  const double* cT;      // [D][NP*L]  c_ji
+  const double* egeo;    // [2(D+1)][n_edges]  n_ij, |c_ij|, n_ji, |c_ji| per upper edge
   const double* mij;     // [NP*L]     consistent mass m_ij
   const double* m_i;     // [NP] lumped mass
   const double* inv_m;   // [NP]
