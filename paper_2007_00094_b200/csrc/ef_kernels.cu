@@ -27,12 +27,18 @@ namespace ef {
 #define EF_TPB 128
 #endif
 constexpr int TPB = EF_TPB;
+// Resident blocks per SM requested from ptxas (i.e. the register cap) per
+// kernel and dimension, measured on B200 (C2 2D, 160^3 periodic 3D): these
+// kernels are latency-bound, so occupancy usually beats spill-free code.
 #ifndef EF_MINB
-#define EF_MINB 8  // resident blocks per SM requested from ptxas (64-register cap)
+#define EF_MINB 8
 #endif
-#ifndef EF_MINB_PASS
-#define EF_MINB_PASS 10  // k_limit_pass measured fastest at a 51-register cap
-#endif
+#define EF_MINB_EDGE(D) 8
+#define EF_MINB_ROW(D) ((D) == 3 ? 5 : EF_MINB)
+#define EF_MINB_LOW(D) ((D) == 3 ? 5 : EF_MINB)
+#define EF_MINB_CORR(D) ((D) == 3 ? 6 : EF_MINB)
+#define EF_MINB_PASS(D) 10
+#define EF_MINB_FINAL(D) ((D) == 3 ? 6 : EF_MINB)
 
 static inline unsigned grid_for(int64_t n) { return (unsigned)((n + TPB - 1) / TPB); }
 
@@ -98,7 +104,7 @@ __global__ void k_nodal(Layout m, Gas g, const double* __restrict__ U, Work w, i
 // positions in ascending order, so a warp reads 32 consecutive positions of
 // one slot row (coalesced) and the row / slot are recovered from the position.
 template <int D>
-__global__ void __launch_bounds__(TPB, EF_MINB) k_edge_visc(Layout m, Gas g, const double* __restrict__ U,
+__global__ void __launch_bounds__(TPB, EF_MINB_EDGE(D)) k_edge_visc(Layout m, Gas g, const double* __restrict__ U,
                                                    Work w, int reset_tau) {
   constexpr int NV = D + 2;
   const int64_t e = blockIdx.x * (int64_t)TPB + threadIdx.x;
@@ -139,7 +145,7 @@ __device__ __forceinline__ double warp_min(double v) {
 // mirror of the lower triangle with d_ii = -(numpy pairwise row sum)
 // (_k_mirror, stepper.py:427-434) and the CFL bound (_tau_local, :66-70).
 template <int D>
-__global__ void __launch_bounds__(TPB, EF_MINB) k_row_visc(Layout m, Gas g, const double* __restrict__ U,
+__global__ void __launch_bounds__(TPB, EF_MINB_ROW(D)) k_row_visc(Layout m, Gas g, const double* __restrict__ U,
                                                   Work w, int want_tau) {
   constexpr int NV = D + 2;
   const int64_t i = blockIdx.x * (int64_t)TPB + threadIdx.x;
@@ -265,7 +271,7 @@ __device__ __forceinline__ double stage_tau(const Work& w, const StageParams& sp
 }
 
 template <int D>
-__global__ void __launch_bounds__(TPB, EF_MINB) k_low_order(Layout m, Gas g, const double* __restrict__ U,
+__global__ void __launch_bounds__(TPB, EF_MINB_LOW(D)) k_low_order(Layout m, Gas g, const double* __restrict__ U,
                                                    Work w, StageParams sp) {
   constexpr int NV = D + 2;
   const double tau = stage_tau(w, sp);
@@ -357,7 +363,7 @@ __device__ __forceinline__ void build_P(const Layout& m, const Work& w, const do
 }
 
 template <int D>
-__global__ void __launch_bounds__(TPB, EF_MINB) k_correction(Layout m, Gas g, const double* __restrict__ U,
+__global__ void __launch_bounds__(TPB, EF_MINB_CORR(D)) k_correction(Layout m, Gas g, const double* __restrict__ U,
                                                     Work w, StageParams sp) {
   constexpr int NV = D + 2;
   const int64_t i = blockIdx.x * (int64_t)TPB + threadIdx.x;
@@ -389,7 +395,7 @@ __global__ void __launch_bounds__(TPB, EF_MINB) k_correction(Layout m, Gas g, co
 }
 
 template <int D>
-__global__ void __launch_bounds__(TPB, EF_MINB_PASS) k_limit_pass(Layout m, Gas g, const double* __restrict__ U,
+__global__ void __launch_bounds__(TPB, EF_MINB_PASS(D)) k_limit_pass(Layout m, Gas g, const double* __restrict__ U,
                                                     Work w, StageParams sp, int pass) {
   constexpr int NV = D + 2;
   const int64_t i = blockIdx.x * (int64_t)TPB + threadIdx.x;
@@ -438,7 +444,7 @@ __global__ void __launch_bounds__(TPB, EF_MINB_PASS) k_limit_pass(Layout m, Gas 
 }
 
 template <int D>
-__global__ void __launch_bounds__(TPB, EF_MINB) k_final(Layout m, Gas g, const double* __restrict__ U,
+__global__ void __launch_bounds__(TPB, EF_MINB_FINAL(D)) k_final(Layout m, Gas g, const double* __restrict__ U,
                                                const double* __restrict__ U0, double* __restrict__ Uout,
                                                Work w, StageParams sp) {
   constexpr int NV = D + 2;
