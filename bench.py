@@ -228,9 +228,15 @@ def run_ours(args, rank, world, local_rank):
     achieved = phase_bytes[dom] / per_launch[dom] / 1e9
     stage_bytes = 8.0 * stage_doubles_per_nnz(dim, card, passes) * nnz
     stage_s = (ms * 1e-3) / (3 * args.steps)
+    traffic = None  # dram read + write bytes per launch from the committed ncu --set full capture
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            traffic = json.load(fh).get(args.config, {}).get(KERNEL_OF_PHASE[dom], {}).get("traffic_bytes")
+    except Exception:
+        traffic = None
     roofline = {
         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-        "traffic": None, "kernel": KERNEL_OF_PHASE[dom], "phase": dom,
+        "traffic": traffic, "kernel": KERNEL_OF_PHASE[dom], "phase": dom,
         "kernel_ms": per_launch[dom] * 1e3, "algorithmic_bytes_per_launch": phase_bytes[dom],
         "peak_kind": peak_kind,
         "phase_ms": {k: round(v * 1e3, 4) for k, v in per_launch.items()},
