@@ -210,7 +210,8 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
   h->NP = std::max<int64_t>((n_local + 31) / 32 * 32, 32);
   h->NPL = h->NP * L;
   const int64_t NP = h->NP, NPL = h->NPL;
-  if (NPL >= (int64_t)1 << 31) return fail(EF_ERR_ARG, "local slot count exceeds int32 positions");
+  if (NPL >= (int64_t)1 << 31 || (int64_t)NV * NP >= (int64_t)1 << 31)
+    return fail(EF_ERR_ARG, "local rows/slots exceed 32-bit indexing (use more ranks)");
   h->gid_host = P.gid;
   h->orig_host.resize(n_local);
   for (int64_t i = 0; i < n_local; ++i) h->orig_host[i] = P.cm_inv[P.gid[i]];

@@ -39,8 +39,28 @@ constexpr int TPB = EF_TPB;
 #define EF_MINB_CORR(D) ((D) == 3 ? 6 : EF_MINB)
 #define EF_MINB_PASS(D) 10
 #define EF_MINB_FINAL(D) ((D) == 3 ? 6 : EF_MINB)
+// unroll factors of the per-row slot loops (lets ptxas hoist later slots' loads)
+#define EF_STR(x) #x
+#define EF_PRAGMA(x) _Pragma(EF_STR(x))
+#ifndef EF_UNROLL_N
+#define EF_UNROLL_N 1
+#endif
+#define EF_UNROLL_ROW EF_PRAGMA(unroll(D == 2 ? 2 : 1))
+#define EF_UNROLL_LOW EF_PRAGMA(unroll EF_UNROLL_N)
+#define EF_UNROLL_CORR EF_PRAGMA(unroll EF_UNROLL_N)
+#define EF_UNROLL_PASS1 EF_PRAGMA(unroll EF_UNROLL_N)
+#define EF_UNROLL_PASS2 EF_PRAGMA(unroll EF_UNROLL_N)
+#define EF_UNROLL_FINAL EF_PRAGMA(unroll EF_UNROLL_N)
 
 static inline unsigned grid_for(int64_t n) { return (unsigned)((n + TPB - 1) / TPB); }
+
+__device__ __forceinline__ int sidx32(int i, int s, int L) { return (i >> 5) * (32 * L) + s * 32 + (i & 31); }
+
+template <int NV>
+__device__ __forceinline__ void load_node(const double* __restrict__ U, int NP, int i, double* out) {
+#pragma unroll
+  for (int k = 0; k < NV; ++k) out[k] = U[k * NP + i];
+}
 
 template <int NV>
 __device__ __forceinline__ void load_node(const double* __restrict__ U, int64_t NP, int64_t i,
@@ -107,29 +127,29 @@ template <int D>
 __global__ void __launch_bounds__(TPB, EF_MINB_EDGE(D)) k_edge_visc(Layout m, Gas g, const double* __restrict__ U,
                                                    Work w, int reset_tau) {
   constexpr int NV = D + 2;
-  const int64_t e = blockIdx.x * (int64_t)TPB + threadIdx.x;
+  const int e = blockIdx.x * TPB + threadIdx.x;
   if (reset_tau && e == 0) *w.tau_min_bits = 0x7ff0000000000000ULL;
   if (e >= m.n_edges) return;
-  const int64_t p = m.edges[e];
-  const int64_t i = (int64_t)fdiv((uint32_t)p, m.slab) * 32 + (p & 31);
-  const int64_t j = m.col[p];
-  const int64_t NP = m.NP, NE = m.n_edges;
+  const int p = m.edges[e];
+  const int i = (int)fdiv((uint32_t)p, m.slab) * 32 + (p & 31);
+  const int j = m.col[p];
+  const int NP = (int)m.NP, NE = (int)m.n_edges;
   double Ui[NV], Uj[NV], nij[D], nji[D];
   load_node<NV>(U, NP, i, Ui);
   load_node<NV>(U, NP, j, Uj);
 #pragma unroll
   for (int a = 0; a < D; ++a) {
-    nij[a] = m.egeo[a * NE + e];
-    nji[a] = m.egeo[(D + 1 + a) * NE + e];
+    nij[a] = m.egeo[(size_t)a * NE + e];
+    nji[a] = m.egeo[(size_t)(D + 1 + a) * NE + e];
   }
-  const double norm_ij = m.egeo[D * NE + e], norm_ji = m.egeo[(2 * D + 1) * NE + e];
+  const double norm_ij = m.egeo[(size_t)D * NE + e], norm_ji = m.egeo[(size_t)(2 * D + 1) * NE + e];
   bool bad = false;
   const double dv = d_ij_geo<D>(Ui, Uj, nij, norm_ij, nji, norm_ji, g, bad);
   // d is symmetric by construction (riemann.py:139-142): the value is also
   // the lower-triangle entry of row j, written straight to its slot (the
   // reference's mirror, stepper.py:427-434, without a gather)
   w.d[p] = dv;
-  w.d[sidx(j, m.tslot[p], m.L)] = dv;
+  w.d[sidx32(j, m.tslot[p], m.L)] = dv;
   if (bad) atomicOr(w.err, ERR_PROJECT);
 }
 
@@ -148,15 +168,15 @@ template <int D>
 __global__ void __launch_bounds__(TPB, EF_MINB_ROW(D)) k_row_visc(Layout m, Gas g, const double* __restrict__ U,
                                                   Work w, int want_tau) {
   constexpr int NV = D + 2;
-  const int64_t i = blockIdx.x * (int64_t)TPB + threadIdx.x;
+  const int i = blockIdx.x * TPB + threadIdx.x;
   double cand = __longlong_as_double(0x7ff0000000000000LL);
   bool bad = false;
   if (i < m.n_owned) {
-    const int64_t NP = m.NP;
+    const int NP = (int)m.NP;
     const int L = m.L;
-    const int64_t NPL = NP * L;
+    const int NPL = NP * L;
     const int card = m.card[i], dg = m.diag[i];
-    const int64_t base = sidx(i, 0, L);
+    const int base = sidx32(i, 0, L);
     double Ui[NV];
     load_node<NV>(U, NP, i, Ui);
     double fi[NV][D];
@@ -165,15 +185,16 @@ __global__ void __launch_bounds__(TPB, EF_MINB_ROW(D)) k_row_visc(Layout m, Gas 
     double A = 0.0, B[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) B[k] = 0.0;
+    EF_UNROLL_ROW
     for (int s = 0; s < card; ++s) {  // indicator: sequential over slots
       if (s == dg) continue;  // j == i contributes exact zeros
-      const int64_t p = base + (int64_t)s * 32;
-      const int64_t j = m.col[p];
+      const int p = base + s * 32;
+      const int j = m.col[p];
       double Uj[NV];
       load_node<NV>(U, NP, j, Uj);
       double cc[D];
 #pragma unroll
-      for (int a = 0; a < D; ++a) cc[a] = m.c[a * NPL + p];
+      for (int a = 0; a < D; ++a) cc[a] = m.c[(size_t)a * NPL + p];
       double mc = 0.0;
 #pragma unroll
       for (int a = 0; a < D; ++a) mc = mc + Uj[1 + a] * cc[a];
@@ -192,7 +213,7 @@ __global__ void __launch_bounds__(TPB, EF_MINB_ROW(D)) k_row_visc(Layout m, Gas 
     double* __restrict__ d = w.d;
     auto v = [&](int s) -> double {
       if (s == dg || s >= card) return 0.0;
-      return d[base + (int64_t)s * 32];
+      return d[base + s * 32];
     };
     double res;
     if (L < 8) {  // numpy pairwise_sum, n < 8: sequential from +0
@@ -211,7 +232,7 @@ __global__ void __launch_bounds__(TPB, EF_MINB_ROW(D)) k_row_visc(Layout m, Gas 
       for (int s = Lm; s < L; ++s) res = res + v(s);
     }
     const double dii = -res;
-    d[base + (int64_t)dg * 32] = dii;
+    d[base + dg * 32] = dii;
     if (want_tau && dii < 0.0) cand = m.m_i[i] / (-2.0 * dii);
     // IndicatorAccumulator.reset (harten_entropy_derivative, physics.py:133-148)
     double ep[NV];
@@ -275,7 +296,7 @@ __global__ void __launch_bounds__(TPB, EF_MINB_LOW(D)) k_low_order(Layout m, Gas
                                                    Work w, StageParams sp) {
   constexpr int NV = D + 2;
   const double tau = stage_tau(w, sp);
-  const int64_t i = blockIdx.x * (int64_t)TPB + threadIdx.x;
+  const int i = blockIdx.x * TPB + threadIdx.x;
   if (i == 0 && sp.tau_mode != TAU_DEVICE) {
     *w.tau = tau;
     if (sp.tau_mode == TAU_CFL &&
@@ -283,9 +304,9 @@ __global__ void __launch_bounds__(TPB, EF_MINB_LOW(D)) k_low_order(Layout m, Gas
       atomicOr(w.err, ERR_TAU_UNBOUNDED);
   }
   if (i >= m.n_owned) return;
-  const int64_t NP = m.NP;
+  const int NP = (int)m.NP;
   const int L = m.L;
-  const int64_t NPL = NP * L;
+  const int NPL = NP * L;
   double Ui[NV];
   load_node<NV>(U, NP, i, Ui);
   double fi[NV][D];
@@ -297,18 +318,19 @@ __global__ void __launch_bounds__(TPB, EF_MINB_LOW(D)) k_low_order(Layout m, Gas
   // the diagonal (and every pad) yields the bar state U_i and phi_i exactly
   double rmin = Ui[0], rmax = Ui[0], pmin = w.phi[i];
   const int card = m.card[i], dg = m.diag[i];
-  const int64_t base = sidx(i, 0, L);
+  const int base = sidx32(i, 0, L);
+  EF_UNROLL_LOW
   for (int s = 0; s < card; ++s) {
     if (s == dg) continue;
-    const int64_t p = base + (int64_t)s * 32;
-    const int64_t j = m.col[p];
+    const int p = base + s * 32;
+    const int j = m.col[p];
     double Uj[NV];
     load_node<NV>(U, NP, j, Uj);
     double fj[NV][D];
     flux<D>(Uj, g, fj);
     double cc[D];
 #pragma unroll
-    for (int a = 0; a < D; ++a) cc[a] = m.c[a * NPL + p];
+    for (int a = 0; a < D; ++a) cc[a] = m.c[(size_t)a * NPL + p];
     const double dv = w.d[p];
     const double dH = dv * (0.5 * (ai + w.alpha[j]));
     double ubar = 0.0;
@@ -345,9 +367,9 @@ __global__ void __launch_bounds__(TPB, EF_MINB_LOW(D)) k_low_order(Layout m, Gas
 template <int D>
 __device__ __forceinline__ void build_P(const Layout& m, const Work& w, const double* __restrict__ U,
                                         const double* Ui, const double* Ri, double ai, double inv_mi,
-                                        double factor, int64_t p, int64_t j, int applied, double* P) {
+                                        double factor, int p, int j, int applied, double* P) {
   constexpr int NV = D + 2;
-  const int64_t NP = m.NP;
+  const int NP = (int)m.NP;
   const double dv = w.d[p];
   const double dH = dv * (0.5 * (ai + w.alpha[j]));
   const double mm = m.mij[p];
@@ -366,9 +388,9 @@ template <int D>
 __global__ void __launch_bounds__(TPB, EF_MINB_CORR(D)) k_correction(Layout m, Gas g, const double* __restrict__ U,
                                                     Work w, StageParams sp) {
   constexpr int NV = D + 2;
-  const int64_t i = blockIdx.x * (int64_t)TPB + threadIdx.x;
+  const int i = blockIdx.x * TPB + threadIdx.x;
   if (i >= m.n_owned) return;
-  const int64_t NP = m.NP;
+  const int NP = (int)m.NP;
   const int L = m.L;
   const double tau = *w.tau;
   const int card = m.card[i], dg = m.diag[i];
@@ -380,16 +402,17 @@ __global__ void __launch_bounds__(TPB, EF_MINB_CORR(D)) k_correction(Layout m, G
   load_node<NV>(w.Unext, NP, i, Un);
   const double ai = w.alpha[i];
   const double rmin = w.bounds[i], rmax = w.bounds[NP + i], pmin = w.bounds[2 * NP + i];
-  const int64_t base = sidx(i, 0, L);
+  const int base = sidx32(i, 0, L);
+  EF_UNROLL_CORR
   for (int s = 0; s < card; ++s) {
     if (s == dg) continue;
-    const int64_t p = base + (int64_t)s * 32;
-    const int64_t j = m.col[p];
+    const int p = base + s * 32;
+    const int j = m.col[p];
     double P[NV];
     build_P<D>(m, w, U, Ui, Ri, ai, inv_mi, factor, p, j, 0, P);
-    const int64_t NPL = NP * L;
+    const int NPL = NP * L;
 #pragma unroll
-    for (int k = 0; k < NV; ++k) w.P[k * NPL + p] = P[k];
+    for (int k = 0; k < NV; ++k) w.P[(size_t)k * NPL + p] = P[k];
     w.l[p] = limiter<D>(Un, P, rmin, rmax, pmin, sp.newton, g);
   }
 }
@@ -398,29 +421,30 @@ template <int D>
 __global__ void __launch_bounds__(TPB, EF_MINB_PASS(D)) k_limit_pass(Layout m, Gas g, const double* __restrict__ U,
                                                     Work w, StageParams sp, int pass) {
   constexpr int NV = D + 2;
-  const int64_t i = blockIdx.x * (int64_t)TPB + threadIdx.x;
+  const int i = blockIdx.x * TPB + threadIdx.x;
   if (i >= m.n_owned) return;
-  const int64_t NP = m.NP;
+  const int NP = (int)m.NP;
   const int L = m.L;
-  const int64_t NPL = NP * L;
+  const int NPL = NP * L;
   const int card = m.card[i], dg = m.diag[i];
-  const int64_t base = sidx(i, 0, L);
-  const double* __restrict__ lp = w.l + pass * NPL;
+  const int base = sidx32(i, 0, L);
+  const double* __restrict__ lp = w.l + (size_t)pass * NPL;
   double upd[NV];
 #pragma unroll
   for (int k = 0; k < NV; ++k) upd[k] = 0.0;
   // upd += min(l, l^T) P in slot order, then P <- (1 - min) P in place
   // (stepper.py:478-485)
+  EF_UNROLL_PASS1
   for (int s = 0; s < card; ++s) {
     if (s == dg) continue;
-    const int64_t p = base + (int64_t)s * 32;
-    const double ml = npmin(lp[p], lp[sidx(m.col[p], m.tslot[p], L)]);
+    const int p = base + s * 32;
+    const double ml = npmin(lp[p], lp[sidx32(m.col[p], m.tslot[p], L)]);
     const double f = 1.0 - ml;
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
-      const double P = w.P[k * NPL + p];
+      const double P = w.P[(size_t)k * NPL + p];
       upd[k] = upd[k] + ml * P;
-      w.P[k * NPL + p] = P * f;
+      w.P[(size_t)k * NPL + p] = P * f;
     }
   }
   double Un[NV];
@@ -432,13 +456,14 @@ __global__ void __launch_bounds__(TPB, EF_MINB_PASS(D)) k_limit_pass(Layout m, G
     w.Unext[k * NP + i] = Un[k];
   }
   const double rmin = w.bounds[i], rmax = w.bounds[NP + i], pmin = w.bounds[2 * NP + i];
-  double* __restrict__ ln = w.l + (pass + 1) * NPL;
+  double* __restrict__ ln = w.l + (size_t)(pass + 1) * NPL;
+  EF_UNROLL_PASS2
   for (int s = 0; s < card; ++s) {
     if (s == dg) continue;
-    const int64_t p = base + (int64_t)s * 32;
+    const int p = base + s * 32;
     double P[NV];
 #pragma unroll
-    for (int k = 0; k < NV; ++k) P[k] = w.P[k * NPL + p];
+    for (int k = 0; k < NV; ++k) P[k] = w.P[(size_t)k * NPL + p];
     ln[p] = limiter<D>(Un, P, rmin, rmax, pmin, sp.newton, g);  // stepper.py:486-491
   }
 }
@@ -448,27 +473,28 @@ __global__ void __launch_bounds__(TPB, EF_MINB_FINAL(D)) k_final(Layout m, Gas g
                                                const double* __restrict__ U0, double* __restrict__ Uout,
                                                Work w, StageParams sp) {
   constexpr int NV = D + 2;
-  const int64_t i = blockIdx.x * (int64_t)TPB + threadIdx.x;
+  const int i = blockIdx.x * TPB + threadIdx.x;
   if (i >= m.n_owned) return;
-  const int64_t NP = m.NP;
+  const int NP = (int)m.NP;
   const int L = m.L;
-  const int64_t NPL = NP * L;
+  const int NPL = NP * L;
   double Un[NV];
   load_node<NV>(w.Unext, NP, i, Un);
   if (sp.passes > 0) {
     const int pass = sp.passes - 1;
     const int card = m.card[i], dg = m.diag[i];
-    const int64_t base = sidx(i, 0, L);
-    const double* __restrict__ lp = w.l + pass * NPL;
+    const int base = sidx32(i, 0, L);
+    const double* __restrict__ lp = w.l + (size_t)pass * NPL;
     double upd[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) upd[k] = 0.0;
+    EF_UNROLL_FINAL
     for (int s = 0; s < card; ++s) {
       if (s == dg) continue;
-      const int64_t p = base + (int64_t)s * 32;
-      const double ml = npmin(lp[p], lp[sidx(m.col[p], m.tslot[p], L)]);
+      const int p = base + s * 32;
+      const double ml = npmin(lp[p], lp[sidx32(m.col[p], m.tslot[p], L)]);
 #pragma unroll
-      for (int k = 0; k < NV; ++k) upd[k] = upd[k] + ml * w.P[k * NPL + p];
+      for (int k = 0; k < NV; ++k) upd[k] = upd[k] + ml * w.P[(size_t)k * NPL + p];
     }
     const double lam = m.lam[i];
 #pragma unroll
