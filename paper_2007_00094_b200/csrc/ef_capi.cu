@@ -224,7 +224,7 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
 
   // SELL-32 host images
   std::vector<int32_t> col(NPL);
-  std::vector<uint8_t> tslot(NPL, 0), card(NP, 1), diag(NP, 0);
+  std::vector<uint8_t> tslot(NPL, 0), card(NP, 1), cardf(NP, 1), diag(NP, 0);
   std::vector<double> c((size_t)D * NPL, 0.0), mij(NPL, 0.0);
   std::vector<double> m_i(NP, 1.0), inv_m(NP, 1.0), lam(NP, 1.0);
   std::vector<int64_t> gid(NP, 0);
@@ -255,6 +255,7 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
     }
     if (dg < 0) return fail(EF_ERR_ARG, "every stencil must contain its own row");
     diag[i] = (uint8_t)dg;
+    cardf[i] = (uint8_t)(mat->indptr[o + 1] - mat->indptr[o]);
     m_i[i] = mat->m_lumped[o];
     inv_m[i] = mat->inv_m[o];
     const int64_t den = std::max<int64_t>(cnt - 1, 1);
@@ -356,7 +357,7 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
   m.n_local = n_local;
   m.n_owned = n_owned;
   int32_t* d_col;
-  uint8_t *d_tslot, *d_card, *d_diag;
+  uint8_t *d_tslot, *d_card, *d_cardf, *d_diag;
   double *d_c, *d_egeo, *d_mij, *d_mi, *d_invm, *d_lam, *d_bcn;
   int64_t* d_gid;
   int8_t* d_bck;
@@ -364,6 +365,7 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
   EF_TRY(upload(h, &d_col, col));
   EF_TRY(upload(h, &d_tslot, tslot));
   EF_TRY(upload(h, &d_card, card));
+  EF_TRY(upload(h, &d_cardf, cardf));
   EF_TRY(upload(h, &d_diag, diag));
   EF_TRY(upload(h, &d_c, c));
   EF_TRY(upload(h, &d_egeo, egeo));
@@ -378,6 +380,7 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
   m.col = d_col;
   m.tslot = d_tslot;
   m.card = d_card;
+  m.cardf = d_cardf;
   m.diag = d_diag;
   m.c = d_c;
   m.egeo = d_egeo;
@@ -404,7 +407,6 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
   }
 
   Work& w = h->w;
-  const int npass = std::max(1, h->passes);
   EF_TRY(h->alloc(&w.eor, NP));
   EF_TRY(h->alloc(&w.phi, NP));
   EF_TRY(h->alloc(&w.alpha, NP));
@@ -412,14 +414,14 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
   EF_TRY(h->alloc(&w.Unext, (size_t)NV * NP));
   EF_TRY(h->alloc(&w.bounds, (size_t)3 * NP));
   EF_TRY(h->alloc(&w.d, NPL));
-  EF_TRY(h->alloc(&w.l, (size_t)npass * NPL));
+  EF_TRY(h->alloc(&w.ml, NPL));
   EF_TRY(h->alloc(&w.P, (size_t)NV * NPL));
   EF_TRY(h->alloc(&w.tau_min_bits, 1));
   EF_TRY(h->alloc(&w.tau, 1));
   EF_TRY(h->alloc(&w.err, 1));
   EF_TRY(h->alloc(&w.bad_gid, 1));
   EF_CUDA(cudaMemset(w.d, 0, sizeof(double) * NPL));
-  EF_CUDA(cudaMemset(w.l, 0, sizeof(double) * npass * NPL));
+  EF_CUDA(cudaMemset(w.ml, 0, sizeof(double) * NPL));
   EF_CUDA(cudaMemset(w.P, 0, sizeof(double) * NV * NPL));
   EF_CUDA(cudaMemset(w.alpha, 0, sizeof(double) * NP));
   EF_CUDA(cudaMemset(w.R, 0, sizeof(double) * NV * NP));
@@ -559,15 +561,20 @@ static int run_stage(Driver& d, const std::vector<StageIO>& io, StageParams sp) 
   if (want_tau) EF_TRY(allreduce_tau(d));
   EF_TRY(mark(t, 3));
   each([&](ef_solver* h, const StageIO& x) { ef::launch_low_order(h->dim, h->lay, h->gas, x.U, h->w, sp, h->st); });
+  // ghost rows: R for P, U^L and bounds for their own limiter side
   EF_TRY(exchange(d, false, t->nvar, [&d](size_t r) { return d.hs[r]->w.R; }));
+  if (t->passes > 0) {
+    EF_TRY(exchange(d, false, t->nvar, [&d](size_t r) { return d.hs[r]->w.Unext; }));
+    EF_TRY(exchange(d, false, 3, [&d](size_t r) { return d.hs[r]->w.bounds; }));
+  }
   EF_TRY(mark(t, 4));
   if (t->passes > 0) {
-    each([&](ef_solver* h, const StageIO& x) { ef::launch_limiter0(h->dim, h->lay, h->gas, x.U, h->w, sp, h->st); });
-    EF_TRY(exchange(d, true, 1, [&d](size_t r) { return d.hs[r]->w.l; }));
+    each([&](ef_solver* h, const StageIO& x) { ef::launch_edge_lim(h->dim, h->lay, h->gas, x.U, h->w, sp, 0, h->st); });
     EF_TRY(mark(t, 5));
     for (int p = 0; p + 1 < t->passes; ++p) {
-      each([&](ef_solver* h, const StageIO& x) { ef::launch_pass(h->dim, h->lay, h->gas, x.U, h->w, sp, p, h->st); });
-      EF_TRY(exchange(d, true, 1, [&d, p](size_t r) { return d.hs[r]->w.l + (size_t)(p + 1) * d.hs[r]->NPL; }));
+      each([&](ef_solver* h, const StageIO& x) { ef::launch_row_upd(h->dim, h->lay, h->gas, x.U, h->w, sp, h->st); });
+      EF_TRY(exchange(d, false, t->nvar, [&d](size_t r) { return d.hs[r]->w.Unext; }));
+      each([&](ef_solver* h, const StageIO& x) { ef::launch_edge_lim(h->dim, h->lay, h->gas, x.U, h->w, sp, p + 1, h->st); });
     }
     EF_TRY(mark(t, 6));
   } else {
@@ -922,9 +929,9 @@ int ef_debug_fetch(ef_solver* h, int32_t which, int32_t which_pass, double* out)
     case 1: return node_field(h->w.alpha, 1);
     case 2: return node_field(h->w.R, NV);
     case 3: return node_field(h->w.bounds, 3);
-    case 4:
-      if (which_pass < 0 || which_pass >= std::max(1, h->passes)) return fail(EF_ERR_ARG, "bad pass");
-      return slot_field(h->w.l + (size_t)which_pass * NPL);
+    case 4:  // min(l_ij, l_ji) of the last limiter pass
+      (void)which_pass;
+      return slot_field(h->w.ml);
     case 5: return node_field(h->w.eor, 1);
     case 6: return node_field(h->w.phi, 1);
     case 7: return node_field(h->Ubuf[h->cur], NV);

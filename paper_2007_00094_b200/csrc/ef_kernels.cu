@@ -8,17 +8,18 @@
 //   k_row_visc     = step1 IndicatorAccumulator (:417-425) + step2 _k_mirror and
 //                    _tau_local (:427-434, :66-70)
 //   k_low_order    = step3 _k_low_order (+ tau = min(c_cfl tau_min, tau_max), :548)
-//   k_correction   = step4 _k_correction: P_ij rebuilt in registers + limiter (:456-474)
-//   k_limit_pass   = step5 non-final limited update + the next pass's limiter (:476-491)
+//   k_edge_lim(q)  = step4 (q = 0: P_ij, P_ji built from R, U, d, alpha, m) and the
+//                    limiter of pass q for both rows of an edge + min(l_ij, l_ji)
+//                    (:456-474, :478-479, :485-491), one thread per edge
+//   k_row_upd      = step5 non-final limited update (:480-481), one thread per row
 //   k_final        = step6 final pass + _k_boundary + _finish_step check
 //                    + SSP-RK3 combination + next stage's step0 (:493-504, :612-636, :399-405)
 // k_edge_visc is one thread per edge; the others one thread per owned row.
 // (A row-group variant -- G lanes per row, ordered sums from shared memory --
 // measured 40% slower on C2 and was dropped.)
-// k_edge_visc writes d_ij also into the lower slot of row j (d is symmetric),
-// so the row kernels stream their own slots; P_ij is written once by
-// k_correction and rescaled in place per pass (a transposed copy of l measured
-// slower: the producer's extra scattered store costs more than the gather).
+// k_edge_visc writes d_ij also into the lower slot of row j (d is symmetric)
+// and k_edge_lim writes P and min(l_ij, l_ji) to both rows of an edge, so the
+// row kernels stream their own slots instead of gathering transposes.
 #include "ef_kernels.cuh"
 
 namespace ef {
@@ -36,8 +37,17 @@ constexpr int TPB = EF_TPB;
 #define EF_MINB_EDGE(D) 8
 #define EF_MINB_ROW(D) ((D) == 3 ? 5 : EF_MINB)
 #define EF_MINB_LOW(D) ((D) == 3 ? 5 : EF_MINB)
-#define EF_MINB_CORR(D) ((D) == 3 ? 6 : EF_MINB)
-#define EF_MINB_PASS(D) 10
+#ifndef EF_MINB_ELIM2
+#define EF_MINB_ELIM2 EF_MINB
+#endif
+#ifndef EF_MINB_ELIM3
+#define EF_MINB_ELIM3 6
+#endif
+#define EF_MINB_ELIM(D) ((D) == 3 ? EF_MINB_ELIM3 : EF_MINB_ELIM2)
+#ifndef EF_MINB_UPD
+#define EF_MINB_UPD 10
+#endif
+#define EF_MINB_PASS(D) EF_MINB_UPD
 #define EF_MINB_FINAL(D) ((D) == 3 ? 6 : EF_MINB)
 // unroll factors of the per-row slot loops (lets ptxas hoist later slots' loads)
 #define EF_STR(x) #x
@@ -47,9 +57,7 @@ constexpr int TPB = EF_TPB;
 #endif
 #define EF_UNROLL_ROW EF_PRAGMA(unroll(D == 2 ? 2 : 1))
 #define EF_UNROLL_LOW EF_PRAGMA(unroll EF_UNROLL_N)
-#define EF_UNROLL_CORR EF_PRAGMA(unroll EF_UNROLL_N)
 #define EF_UNROLL_PASS1 EF_PRAGMA(unroll EF_UNROLL_N)
-#define EF_UNROLL_PASS2 EF_PRAGMA(unroll EF_UNROLL_N)
 #define EF_UNROLL_FINAL EF_PRAGMA(unroll EF_UNROLL_N)
 
 static inline unsigned grid_for(int64_t n) { return (unsigned)((n + TPB - 1) / TPB); }
@@ -363,109 +371,97 @@ __global__ void __launch_bounds__(TPB, EF_MINB_LOW(D)) k_low_order(Layout m, Gas
 }
 
 // ---------------------------------------------------------------- steps 4-6
-// P^(0)_ij of slot (i, s) (stepper.py:460-468); later passes rescale the stored P.
+// Edge-parallel limiter.  For an edge (i, j) the correction fluxes of both
+// rows, P_ij (row i, stepper.py:460-468) and P_ji (row j), their limiter
+// factors l_ij = limiter(U^L_i, P_ij, bounds_i) and l_ji (limiter.py:149-193)
+// and the symmetric factor min(l_ij, l_ji) (stepper.py:478-479) are formed by
+// ONE thread, which writes P and min(l) to both rows' slots.  Later passes
+// rescale P <- (1 - min l) P per side (stepper.py:485) and re-limit.  The row
+// kernels then only stream their own slots.  Every operation is the
+// reference's, in its order; each side uses its own m_ij / m_ji, alpha sum and
+// factor, so nothing assumes symmetry that the inputs might not have.
 template <int D>
-__device__ __forceinline__ void build_P(const Layout& m, const Work& w, const double* __restrict__ U,
-                                        const double* Ui, const double* Ri, double ai, double inv_mi,
-                                        double factor, int p, int j, int applied, double* P) {
+__global__ void __launch_bounds__(TPB, EF_MINB_ELIM(D)) k_edge_lim(Layout m, Gas g, const double* __restrict__ U,
+                                                                 Work w, StageParams sp, int q) {
   constexpr int NV = D + 2;
+  const int e = blockIdx.x * TPB + threadIdx.x;
+  if (e >= m.n_edges) return;
+  const int p = m.edges[e];
+  const int i = (int)fdiv((uint32_t)p, m.slab) * 32 + (p & 31);
+  const int j = m.col[p];
+  const int pt = sidx32(j, m.tslot[p], m.L);
   const int NP = (int)m.NP;
-  const double dv = w.d[p];
-  const double dH = dv * (0.5 * (ai + w.alpha[j]));
-  const double mm = m.mij[p];
-  const double b = 0.0 - mm * m.inv_m[j];   // b_ij  = delta_ij - m_ij / m_j
-  const double bT = 0.0 - mm * inv_mi;      // b_ji  = delta_ij - m_ij / m_i
-  const double dd = dH - dv;
+  const size_t NPL = (size_t)NP * m.L;
+  double Pi[NV], Pj[NV];
+  if (q == 0) {
+    const double tau = *w.tau;
+    const double imi = m.inv_m[i], imj = m.inv_m[j];
+    const double fi = (tau * imi) * (double)(m.cardf[i] - 1);  // stepper.py:467 (full card)
+    const double fj = (tau * imj) * (double)(m.cardf[j] - 1);
+    const double ai = w.alpha[i], aj = w.alpha[j];
+    const double dv = w.d[p];  // == d at pt (d is symmetric by construction)
+    const double dHi = dv * (0.5 * (ai + aj));
+    const double dHj = dv * (0.5 * (aj + ai));
+    const double mij = m.mij[p], mji = m.mij[pt];
+    const double bi = 0.0 - mij * imj, bTi = 0.0 - mij * imi;  // b_slot / bT_slot, stepper.py:234-236
+    const double bj = 0.0 - mji * imi, bTj = 0.0 - mji * imj;
+    const double ddi = dHi - dv, ddj = dHj - dv;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const double Uik = U[k * NP + i], Ujk = U[k * NP + j];
+      const double Rik = w.R[k * NP + i], Rjk = w.R[k * NP + j];
+      Pi[k] = fi * (((bi * Rjk) - (bTi * Rik)) + (ddi * (Ujk - Uik)));
+      Pj[k] = fj * (((bj * Rik) - (bTj * Rjk)) + (ddj * (Uik - Ujk)));
+    }
+  } else {
+    const double gi = 1.0 - w.ml[p], gj = 1.0 - w.ml[pt];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      Pi[k] = w.P[(size_t)k * NPL + p] * gi;
+      Pj[k] = w.P[(size_t)k * NPL + pt] * gj;
+    }
+  }
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
-    const double K = ((b * w.R[k * NP + j]) - (bT * Ri[k])) + (dd * (U[k * NP + j] - Ui[k]));
-    P[k] = factor * K;
+    w.P[(size_t)k * NPL + p] = Pi[k];
+    w.P[(size_t)k * NPL + pt] = Pj[k];
   }
-  (void)applied;
-}
-
-template <int D>
-__global__ void __launch_bounds__(TPB, EF_MINB_CORR(D)) k_correction(Layout m, Gas g, const double* __restrict__ U,
-                                                    Work w, StageParams sp) {
-  constexpr int NV = D + 2;
-  const int i = blockIdx.x * TPB + threadIdx.x;
-  if (i >= m.n_owned) return;
-  const int NP = (int)m.NP;
-  const int L = m.L;
-  const double tau = *w.tau;
-  const int card = m.card[i], dg = m.diag[i];
-  const double inv_mi = m.inv_m[i];
-  const double factor = (tau * inv_mi) * (double)(card - 1);
-  double Ui[NV], Ri[NV], Un[NV];
-  load_node<NV>(U, NP, i, Ui);
-  load_node<NV>(w.R, NP, i, Ri);
+  double Un[NV];
   load_node<NV>(w.Unext, NP, i, Un);
-  const double ai = w.alpha[i];
-  const double rmin = w.bounds[i], rmax = w.bounds[NP + i], pmin = w.bounds[2 * NP + i];
-  const int base = sidx32(i, 0, L);
-  EF_UNROLL_CORR
-  for (int s = 0; s < card; ++s) {
-    if (s == dg) continue;
-    const int p = base + s * 32;
-    const int j = m.col[p];
-    double P[NV];
-    build_P<D>(m, w, U, Ui, Ri, ai, inv_mi, factor, p, j, 0, P);
-    const int NPL = NP * L;
-#pragma unroll
-    for (int k = 0; k < NV; ++k) w.P[(size_t)k * NPL + p] = P[k];
-    w.l[p] = limiter<D>(Un, P, rmin, rmax, pmin, sp.newton, g);
-  }
+  const double li = limiter<D>(Un, Pi, w.bounds[i], w.bounds[NP + i], w.bounds[2 * NP + i], sp.newton, g);
+  load_node<NV>(w.Unext, NP, j, Un);
+  const double lj = limiter<D>(Un, Pj, w.bounds[j], w.bounds[NP + j], w.bounds[2 * NP + j], sp.newton, g);
+  w.ml[p] = npmin(li, lj);   // row i: np.minimum(l_ij, l_ji)
+  w.ml[pt] = npmin(lj, li);  // row j: np.minimum(l_ji, l_ij)
 }
 
+// step5 (non-final pass): U_next_i += lam_i * sum_s min(l) P in slot order
+// (stepper.py:478-481); the rescale of P belongs to the next k_edge_lim.
 template <int D>
-__global__ void __launch_bounds__(TPB, EF_MINB_PASS(D)) k_limit_pass(Layout m, Gas g, const double* __restrict__ U,
-                                                    Work w, StageParams sp, int pass) {
+__global__ void __launch_bounds__(TPB, EF_MINB_PASS(D)) k_row_upd(Layout m, Gas g, const double* __restrict__ U,
+                                                                Work w, StageParams sp) {
   constexpr int NV = D + 2;
   const int i = blockIdx.x * TPB + threadIdx.x;
   if (i >= m.n_owned) return;
   const int NP = (int)m.NP;
   const int L = m.L;
-  const int NPL = NP * L;
+  const size_t NPL = (size_t)NP * L;
   const int card = m.card[i], dg = m.diag[i];
   const int base = sidx32(i, 0, L);
-  const double* __restrict__ lp = w.l + (size_t)pass * NPL;
   double upd[NV];
 #pragma unroll
   for (int k = 0; k < NV; ++k) upd[k] = 0.0;
-  // upd += min(l, l^T) P in slot order, then P <- (1 - min) P in place
-  // (stepper.py:478-485)
   EF_UNROLL_PASS1
   for (int s = 0; s < card; ++s) {
     if (s == dg) continue;
     const int p = base + s * 32;
-    const double ml = npmin(lp[p], lp[sidx32(m.col[p], m.tslot[p], L)]);
-    const double f = 1.0 - ml;
+    const double ml = w.ml[p];
 #pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      const double P = w.P[(size_t)k * NPL + p];
-      upd[k] = upd[k] + ml * P;
-      w.P[(size_t)k * NPL + p] = P * f;
-    }
+    for (int k = 0; k < NV; ++k) upd[k] = upd[k] + ml * w.P[(size_t)k * NPL + p];
   }
-  double Un[NV];
-  load_node<NV>(w.Unext, NP, i, Un);
   const double lam = m.lam[i];
 #pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    Un[k] = Un[k] + lam * upd[k];
-    w.Unext[k * NP + i] = Un[k];
-  }
-  const double rmin = w.bounds[i], rmax = w.bounds[NP + i], pmin = w.bounds[2 * NP + i];
-  double* __restrict__ ln = w.l + (size_t)(pass + 1) * NPL;
-  EF_UNROLL_PASS2
-  for (int s = 0; s < card; ++s) {
-    if (s == dg) continue;
-    const int p = base + s * 32;
-    double P[NV];
-#pragma unroll
-    for (int k = 0; k < NV; ++k) P[k] = w.P[(size_t)k * NPL + p];
-    ln[p] = limiter<D>(Un, P, rmin, rmax, pmin, sp.newton, g);  // stepper.py:486-491
-  }
+  for (int k = 0; k < NV; ++k) w.Unext[k * NP + i] = w.Unext[k * NP + i] + lam * upd[k];
 }
 
 template <int D>
@@ -477,14 +473,12 @@ __global__ void __launch_bounds__(TPB, EF_MINB_FINAL(D)) k_final(Layout m, Gas g
   if (i >= m.n_owned) return;
   const int NP = (int)m.NP;
   const int L = m.L;
-  const int NPL = NP * L;
+  const size_t NPL = (size_t)NP * L;
   double Un[NV];
   load_node<NV>(w.Unext, NP, i, Un);
   if (sp.passes > 0) {
-    const int pass = sp.passes - 1;
     const int card = m.card[i], dg = m.diag[i];
     const int base = sidx32(i, 0, L);
-    const double* __restrict__ lp = w.l + (size_t)pass * NPL;
     double upd[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) upd[k] = 0.0;
@@ -492,7 +486,7 @@ __global__ void __launch_bounds__(TPB, EF_MINB_FINAL(D)) k_final(Layout m, Gas g
     for (int s = 0; s < card; ++s) {
       if (s == dg) continue;
       const int p = base + s * 32;
-      const double ml = npmin(lp[p], lp[sidx32(m.col[p], m.tslot[p], L)]);
+      const double ml = w.ml[p];
 #pragma unroll
       for (int k = 0; k < NV; ++k) upd[k] = upd[k] + ml * w.P[(size_t)k * NPL + p];
     }
@@ -614,15 +608,15 @@ void launch_low_order(int dim, const Layout& m, const Gas& g, const double* U, W
                       StageParams sp, cudaStream_t st) {
   EF_DISPATCH(dim, k_low_order, grid_for(m.n_owned > 0 ? m.n_owned : 1), m, g, U, w, sp);
 }
-void launch_limiter0(int dim, const Layout& m, const Gas& g, const double* U, Work w,
-                     StageParams sp, cudaStream_t st) {
-  if (m.n_owned == 0) return;
-  EF_DISPATCH(dim, k_correction, grid_for(m.n_owned), m, g, U, w, sp);
+void launch_edge_lim(int dim, const Layout& m, const Gas& g, const double* U, Work w,
+                     StageParams sp, int q, cudaStream_t st) {
+  if (m.n_edges == 0) return;
+  EF_DISPATCH(dim, k_edge_lim, grid_for(m.n_edges), m, g, U, w, sp, q);
 }
-void launch_pass(int dim, const Layout& m, const Gas& g, const double* U, Work w,
-                 StageParams sp, int pass, cudaStream_t st) {
+void launch_row_upd(int dim, const Layout& m, const Gas& g, const double* U, Work w,
+                    StageParams sp, cudaStream_t st) {
   if (m.n_owned == 0) return;
-  EF_DISPATCH(dim, k_limit_pass, grid_for(m.n_owned), m, g, U, w, sp, pass);
+  EF_DISPATCH(dim, k_row_upd, grid_for(m.n_owned), m, g, U, w, sp);
 }
 void launch_final(int dim, const Layout& m, const Gas& g, const double* U, const double* U0,
                   double* Uout, Work w, StageParams sp, cudaStream_t st) {

@@ -49,6 +49,7 @@ struct Layout {
   const int32_t* col;    // [NP*L] local column id (pads: the row itself)
   const uint8_t* tslot;  // [NP*L] slot of (col, row) in row col
   const uint8_t* card;   // [NP] valid slots in the (possibly truncated) stencil
+  const uint8_t* cardf;  // [NP] full stencil cardinality (ghost rows: the owner's)
   const uint8_t* diag;   // [NP] slot of the diagonal
   const double* c;       // [D][NP*L]  c_ij
   const double* egeo;    // [2(D+1)][n_edges]  n_ij, |c_ij|, n_ji, |c_ji| per upper edge
@@ -73,7 +74,7 @@ struct Work {
   double* Unext;     // [NV][NP]
   double* bounds;    // [3][NP] rho_min, rho_max, phi_min
   double* d;         // [NP*L]
-  double* l;         // [passes][NP*L]  l_ij of pass q
+  double* ml;        // [NP*L] min(l_ij, l_ji) of the current limiter pass
   double* P;         // [NV][NP*L] correction fluxes P_ij, rescaled in place per pass
   unsigned long long* tau_min_bits;  // CFL min over owned rows
   double* tau;       // tau of the current RK step / Euler step
@@ -109,12 +110,12 @@ void launch_row_visc(int dim, const Layout& m, const Gas& g, const double* U, Wo
                      bool want_tau, cudaStream_t st);
 void launch_low_order(int dim, const Layout& m, const Gas& g, const double* U, Work w,
                       StageParams sp, cudaStream_t st);
-// step4: l_0(i, s) = limiter(U^L_i, P^(0)_ij)
-void launch_limiter0(int dim, const Layout& m, const Gas& g, const double* U, Work w,
-                     StageParams sp, cudaStream_t st);
-// step5: non-final pass p (row update) fused with the limiter of pass p + 1
-void launch_pass(int dim, const Layout& m, const Gas& g, const double* U, Work w,
-                 StageParams sp, int pass, cudaStream_t st);
+// steps 4-5: P (q = 0) and min(l_ij, l_ji) of limiter pass q, one thread per edge
+void launch_edge_lim(int dim, const Layout& m, const Gas& g, const double* U, Work w,
+                     StageParams sp, int q, cudaStream_t st);
+// step5: non-final pass row update U_next += lam * sum min(l) P
+void launch_row_upd(int dim, const Layout& m, const Gas& g, const double* U, Work w,
+                    StageParams sp, cudaStream_t st);
 void launch_final(int dim, const Layout& m, const Gas& g, const double* U, const double* U0,
                   double* Uout, Work w, StageParams sp, cudaStream_t st);
 void launch_pow(const double* x, double y, double* out, int64_t n, cudaStream_t st);
