@@ -109,8 +109,9 @@ __global__ void k_scatter_state(Layout m, const double* __restrict__ U,
 template <int D>
 __device__ __forceinline__ void nodal_one(const double* Ui, const Gas& g, double& eor, double& phi) {
   const double rho = Ui[0];
-  const double eps = internal_energy<D>(Ui);
-  eor = dpow(rho * eps, g.gp1_inv) / rho;     // stepper.py:403
+  const Recip rr = recip(rho);  // shared by the two divisions by rho
+  const double eps = internal_energy<D>(Ui, rr);
+  eor = qdiv(dpow(rho * eps, g.gp1_inv), rr);  // stepper.py:403
   phi = eps * dpow(rho, g.neg_gamma);          // stepper.py:404
 }
 
