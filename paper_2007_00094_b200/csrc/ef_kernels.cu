@@ -194,11 +194,20 @@ __global__ void __launch_bounds__(TPB, EF_MINB_ROW(D)) k_row_visc(Layout m, Gas 
     double A = 0.0, B[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) B[k] = 0.0;
+    // 3D: the column of the next slot is fetched one iteration ahead (measured
+    // -18% on the 27-point stencil; slower in 2D, where the loop is unrolled)
+    constexpr bool kPrefetch = D == 3;
+    int jn = kPrefetch ? m.col[base] : 0;
     EF_UNROLL_ROW
     for (int s = 0; s < card; ++s) {  // indicator: sequential over slots
+      int j;
+      if (kPrefetch) {
+        j = jn;
+        if (s + 1 < card) jn = m.col[base + (s + 1) * 32];
+      }
       if (s == dg) continue;  // j == i contributes exact zeros
       const int p = base + s * 32;
-      const int j = m.col[p];
+      if (!kPrefetch) j = m.col[p];
       double Uj[NV];
       load_node<NV>(U, NP, j, Uj);
       double cc[D];
