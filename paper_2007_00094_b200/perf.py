@@ -21,14 +21,16 @@ __all__ = ["predict_traffic", "stage_doubles_per_nnz", "KERNEL_OF_PHASE", "PHASE
 
 INDEX_COST = 0.5
 PHASES = ["step0", "step1", "step2", "step3", "step4", "step5", "step6"]
-# phase -> the kernel of libef_b200.so that implements it
+# phase -> the kernel(s) of libef_b200.so that implement it; step5 (one per
+# extra limiter pass) is two kernels, the row update of the previous pass and
+# the edge limiter of the next one
 KERNEL_OF_PHASE = {
     "step0": "k_final (fused nodal update)",
     "step1": "k_edge_visc",
     "step2": "k_row_visc",
     "step3": "k_low_order",
-    "step4": "k_correction",
-    "step5": "k_limit_pass",
+    "step4": "k_edge_lim",
+    "step5": "k_row_upd + k_edge_lim",
     "step6": "k_final",
 }
 

@@ -21,5 +21,5 @@ for r in rows[2:]:
     tot = sum(v for v in stalls.values() if v == v)
     top = sorted(stalls.items(), key=lambda x: -x[1])[:4]
     unit = rows[1][hdr.index('dram__bytes_read.sum')]
-    print(f"{k:29s} {dur/1e3:8.1f}us regs={regs:.0f} occ={occ:4.1f}% ipc={ipc:.2f} fp64={fp:4.1f}% dram={dr+dw:7.1f}{unit} l2hit={l2hit:4.1f}%")
+    print(f"{k:29s} {dur/1e3:8.3f}ms regs={regs:.0f} occ={occ:4.1f}% ipc={ipc:.2f} fp64={fp:4.1f}% dram={dr+dw:7.1f}{unit} l2hit={l2hit:4.1f}%")
     print('      stalls:', ', '.join(f'{a}={b/tot*100:.0f}%' for a, b in top))
