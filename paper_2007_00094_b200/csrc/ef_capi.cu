@@ -276,6 +276,13 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
   // static edge geometry (riemann.py:131-136): n = c / |c|, |c| = sqrt(R1(c*c)),
   // for c_ij and c_ji, evaluated with the reference's operation order
   const int64_t NE = (int64_t)edges.size();
+  // endpoint tables: the edge kernels read j and the transposed position with
+  // the edge position (one coalesced load each) instead of through col/tslot
+  std::vector<int32_t> edge_j(std::max<int64_t>(NE, 1), 0), edge_pt(std::max<int64_t>(NE, 1), 0);
+  for (int64_t e = 0; e < NE; ++e) {
+    edge_j[e] = col[edges[e]];
+    edge_pt[e] = (int32_t)ef::sidx(col[edges[e]], tslot[edges[e]], L);
+  }
   std::vector<double> egeo((size_t)2 * (D + 1) * std::max<int64_t>(NE, 1), 0.0);
   for (int64_t e = 0; e < NE; ++e) {
     const int64_t p = edges[e];
@@ -361,7 +368,7 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
   double *d_c, *d_egeo, *d_mij, *d_mi, *d_invm, *d_lam, *d_bcn;
   int64_t* d_gid;
   int8_t* d_bck;
-  int32_t* d_edges;
+  int32_t *d_edges, *d_edge_j, *d_edge_pt;
   EF_TRY(upload(h, &d_col, col));
   EF_TRY(upload(h, &d_tslot, tslot));
   EF_TRY(upload(h, &d_card, card));
@@ -377,6 +384,8 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
   EF_TRY(upload(h, &d_bck, bc_kind));
   EF_TRY(upload(h, &d_bcn, bc_n));
   EF_TRY(upload(h, &d_edges, edges));
+  EF_TRY(upload(h, &d_edge_j, edge_j));
+  EF_TRY(upload(h, &d_edge_pt, edge_pt));
   m.col = d_col;
   m.tslot = d_tslot;
   m.card = d_card;
@@ -392,6 +401,8 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
   m.bc_kind = d_bck;
   m.bc_n = d_bcn;
   m.edges = d_edges;
+  m.edge_j = d_edge_j;
+  m.edge_pt = d_edge_pt;
   m.n_edges = (int64_t)edges.size();
   m.slab = ef::make_fastdiv((uint32_t)(32 * L));
   for (int k = 0; k < 5; ++k) m.farfield[k] = farfield[k];

@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(TPB, EF_MINB_EDGE(D)) k_edge_visc(Layout m, Ga
   if (e >= m.n_edges) return;
   const int p = m.edges[e];
   const int i = (int)fdiv((uint32_t)p, m.slab) * 32 + (p & 31);
-  const int j = m.col[p];
+  const int j = m.edge_j[e];
   const int NP = (int)m.NP, NE = (int)m.n_edges;
   double Ui[NV], Uj[NV], nij[D], nji[D];
   load_node<NV>(U, NP, i, Ui);
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(TPB, EF_MINB_EDGE(D)) k_edge_visc(Layout m, Ga
   // the lower-triangle entry of row j, written straight to its slot (the
   // reference's mirror, stepper.py:427-434, without a gather)
   w.d[p] = dv;
-  w.d[sidx32(j, m.tslot[p], m.L)] = dv;
+  w.d[m.edge_pt[e]] = dv;
   if (bad) atomicOr(w.err, ERR_PROJECT);
 }
 
@@ -173,6 +173,48 @@ __device__ __forceinline__ double warp_min(double v) {
 // (IndicatorAccumulator.reset/accumulate/result, indicator.py:35-73), the
 // mirror of the lower triangle with d_ii = -(numpy pairwise row sum)
 // (_k_mirror, stepper.py:427-434) and the CFL bound (_tau_local, :66-70).
+// Register-free gather prefetch: cp.async copies a neighbour's fields into this
+// thread's own shared-memory column one slot ahead (per-thread completion, no
+// block barrier), so a row loop overlaps slot s+1's loads with slot s's math.
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
+// Row loop over the real slots s != diag in ascending order with a two-stage
+// prefetch: slot s+1's fields are issued (issue(s, j, stage)) before slot s is
+// consumed (body(s, stage)); the column of slot s+2 is loaded one iteration
+// ahead so the issue never waits on it.  Measured on the 27-point stencil:
+// k_low_order -30%; in 2D (9 points, 69% L2 hits) it does not pay.
+template <class Issue, class Body>
+__device__ __forceinline__ void row_pipe(const int* __restrict__ col, int base, int card, int dg, Issue issue,
+                                         Body body) {
+  int sA = (dg == 0) ? 1 : 0;
+  int sB = sA + 1 + (sA + 1 == dg ? 1 : 0);
+  if (sA < card) issue(sA, col[base + sA * 32], 0);
+  cp_commit();
+  int jB = (sB < card) ? col[base + sB * 32] : 0;
+  for (int it = 0; sA < card; ++it) {
+    const int st = it & 1;
+    if (sB < card) issue(sB, jB, st ^ 1);
+    cp_commit();
+    const int sC = sB + 1 + (sB + 1 == dg ? 1 : 0);
+    const int jC = (sC < card) ? col[base + sC * 32] : 0;
+    cp_wait1();
+    body(sA, st);
+    sA = sB;
+    sB = sC;
+    jB = jC;
+  }
+}
+#ifndef EF_PIPE_2D
+#define EF_PIPE_2D 0
+#endif
+#define EF_PIPE(D) ((D) == 3 || EF_PIPE_2D)
+#define EF_PIPE_ROW(D) true  // k_row_visc: pays in 2D too (-3%)
+
 template <int D>
 __global__ void __launch_bounds__(TPB, EF_MINB_ROW(D)) k_row_visc(Layout m, Gas g, const double* __restrict__ U,
                                                   Work w, int want_tau) {
@@ -194,29 +236,12 @@ __global__ void __launch_bounds__(TPB, EF_MINB_ROW(D)) k_row_visc(Layout m, Gas 
     double A = 0.0, B[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) B[k] = 0.0;
-    // 3D: the column of the next slot is fetched one iteration ahead (measured
-    // -18% on the 27-point stencil; slower in 2D, where the loop is unrolled)
-    constexpr bool kPrefetch = D == 3;
-    int jn = kPrefetch ? m.col[base] : 0;
-    EF_UNROLL_ROW
-    for (int s = 0; s < card; ++s) {  // indicator: sequential over slots
-      int j;
-      if (kPrefetch) {
-        j = jn;
-        if (s + 1 < card) jn = m.col[base + (s + 1) * 32];
-      }
-      if (s == dg) continue;  // j == i contributes exact zeros
-      const int p = base + s * 32;
-      if (!kPrefetch) j = m.col[p];
-      double Uj[NV];
-      load_node<NV>(U, NP, j, Uj);
-      double cc[D];
-#pragma unroll
-      for (int a = 0; a < D; ++a) cc[a] = m.c[(size_t)a * NPL + p];
+    // one slot j != i (j == i contributes exact zeros), in slot order
+    auto slot = [&](const double* Uj, const double* cc, double eor_j) {
       double mc = 0.0;
 #pragma unroll
       for (int a = 0; a < D; ++a) mc = mc + Uj[1 + a] * cc[a];
-      A = A + (w.eor[j] - eor_i) * mc;
+      A = A + (eor_j - eor_i) * mc;
       double fj[NV][D];
       flux<D>(Uj, g, fj);
 #pragma unroll
@@ -225,6 +250,40 @@ __global__ void __launch_bounds__(TPB, EF_MINB_ROW(D)) k_row_visc(Layout m, Gas 
 #pragma unroll
         for (int a = 0; a < D; ++a) t = t + (fj[k][a] - fi[k][a]) * cc[a];
         B[k] = B[k] + t;
+      }
+    };
+    if constexpr (EF_PIPE_ROW(D)) {
+      constexpr int F = NV + 1 + D;  // U_j, eor_j, c
+      __shared__ double buf[2][F][TPB];
+      const int t = threadIdx.x;
+      auto issue = [&](int s, int j, int st) {
+        const int p = base + s * 32;
+#pragma unroll
+        for (int k = 0; k < NV; ++k) cp_async8(&buf[st][k][t], U + k * NP + j);
+        cp_async8(&buf[st][NV][t], w.eor + j);
+#pragma unroll
+        for (int a = 0; a < D; ++a) cp_async8(&buf[st][NV + 1 + a][t], m.c + (size_t)a * NPL + p);
+      };
+      auto body = [&](int, int st) {
+        double Uj[NV], cc[D];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) Uj[k] = buf[st][k][t];
+#pragma unroll
+        for (int a = 0; a < D; ++a) cc[a] = buf[st][NV + 1 + a][t];
+        slot(Uj, cc, buf[st][NV][t]);
+      };
+      row_pipe(m.col, base, card, dg, issue, body);
+    } else {
+      EF_UNROLL_ROW
+      for (int s = 0; s < card; ++s) {  // indicator: sequential over slots
+        if (s == dg) continue;
+        const int p = base + s * 32;
+        const int j = m.col[p];
+        double Uj[NV], cc[D];
+        load_node<NV>(U, NP, j, Uj);
+#pragma unroll
+        for (int a = 0; a < D; ++a) cc[a] = m.c[(size_t)a * NPL + p];
+        slot(Uj, cc, w.eor[j]);
       }
     }
     // d row sum over the L padded slots (lower slots were filled by k_edge_visc)
@@ -309,6 +368,7 @@ __device__ __forceinline__ double stage_tau(const Work& w, const StageParams& sp
   return tau;
 }
 
+
 template <int D>
 __global__ void __launch_bounds__(TPB, EF_MINB_LOW(D)) k_low_order(Layout m, Gas g, const double* __restrict__ U,
                                                    Work w, StageParams sp) {
@@ -337,20 +397,11 @@ __global__ void __launch_bounds__(TPB, EF_MINB_LOW(D)) k_low_order(Layout m, Gas
   double rmin = Ui[0], rmax = Ui[0], pmin = w.phi[i];
   const int card = m.card[i], dg = m.diag[i];
   const int base = sidx32(i, 0, L);
-  EF_UNROLL_LOW
-  for (int s = 0; s < card; ++s) {
-    if (s == dg) continue;
-    const int p = base + s * 32;
-    const int j = m.col[p];
-    double Uj[NV];
-    load_node<NV>(U, NP, j, Uj);
+  // one slot j != i of the row, in slot order (stepper.py:441-454)
+  auto slot = [&](const double* Uj, const double* cc, double dv, double alj, double phij) {
     double fj[NV][D];
     flux<D>(Uj, g, fj);
-    double cc[D];
-#pragma unroll
-    for (int a = 0; a < D; ++a) cc[a] = m.c[(size_t)a * NPL + p];
-    const double dv = w.d[p];
-    const double dH = dv * (0.5 * (ai + w.alpha[j]));
+    const double dH = dv * (0.5 * (ai + alj));
     double ubar = 0.0;
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
@@ -367,7 +418,44 @@ __global__ void __launch_bounds__(TPB, EF_MINB_LOW(D)) k_low_order(Layout m, Gas
     }
     rmin = npmin(rmin, ubar);
     rmax = npmax(rmax, ubar);
-    pmin = npmin(pmin, w.phi[j]);
+    pmin = npmin(pmin, phij);
+  };
+  if constexpr (EF_PIPE(D)) {
+    // fields per slot: U_j (NV), alpha_j, phi_j, c (D), d
+    constexpr int F = NV + 2 + D + 1;
+    __shared__ double buf[2][F][TPB];
+    const int t = threadIdx.x;
+    auto issue = [&](int s, int j, int st) {
+      const int p = base + s * 32;
+#pragma unroll
+      for (int k = 0; k < NV; ++k) cp_async8(&buf[st][k][t], U + k * NP + j);
+      cp_async8(&buf[st][NV][t], w.alpha + j);
+      cp_async8(&buf[st][NV + 1][t], w.phi + j);
+#pragma unroll
+      for (int a = 0; a < D; ++a) cp_async8(&buf[st][NV + 2 + a][t], m.c + (size_t)a * NPL + p);
+      cp_async8(&buf[st][NV + 2 + D][t], w.d + p);
+    };
+    auto body = [&](int, int st) {
+      double Uj[NV], cc[D];
+#pragma unroll
+      for (int k = 0; k < NV; ++k) Uj[k] = buf[st][k][t];
+#pragma unroll
+      for (int a = 0; a < D; ++a) cc[a] = buf[st][NV + 2 + a][t];
+      slot(Uj, cc, buf[st][NV + 2 + D][t], buf[st][NV][t], buf[st][NV + 1][t]);
+    };
+    row_pipe(m.col, base, card, dg, issue, body);
+  } else {
+    EF_UNROLL_LOW
+    for (int s = 0; s < card; ++s) {
+      if (s == dg) continue;
+      const int p = base + s * 32;
+      const int j = m.col[p];
+      double Uj[NV], cc[D];
+      load_node<NV>(U, NP, j, Uj);
+#pragma unroll
+      for (int a = 0; a < D; ++a) cc[a] = m.c[(size_t)a * NPL + p];
+      slot(Uj, cc, w.d[p], w.alpha[j], w.phi[j]);
+    }
   }
   const double fac = tau * m.inv_m[i];
 #pragma unroll
@@ -398,8 +486,8 @@ __global__ void __launch_bounds__(TPB, EF_MINB_ELIM(D)) k_edge_lim(Layout m, Gas
   if (e >= m.n_edges) return;
   const int p = m.edges[e];
   const int i = (int)fdiv((uint32_t)p, m.slab) * 32 + (p & 31);
-  const int j = m.col[p];
-  const int pt = sidx32(j, m.tslot[p], m.L);
+  const int j = m.edge_j[e];
+  const int pt = m.edge_pt[e];
   const int NP = (int)m.NP;
   const size_t NPL = (size_t)NP * m.L;
   double Pi[NV], Pj[NV];

@@ -61,6 +61,8 @@ struct Layout {
   const int8_t* bc_kind; // [NP] bit0 slip, bit1 inflow
   const double* bc_n;    // [D][NP] slip normal
   const int32_t* edges;  // [n_edges] SELL positions of the upper slots of all local rows, ascending
+  const int32_t* edge_j;   // [n_edges] column j of the edge (= col at edges[e])
+  const int32_t* edge_pt;  // [n_edges] SELL position of the transposed slot (j, i)
   int64_t n_edges;
   FastDiv slab;          // division by 32 * L (SELL slice size)
   double farfield[5];
