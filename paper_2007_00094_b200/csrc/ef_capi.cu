@@ -426,6 +426,7 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
   EF_TRY(h->alloc(&w.bounds, (size_t)3 * NP));
   EF_TRY(h->alloc(&w.d, NPL));
   EF_TRY(h->alloc(&w.ml, NPL));
+  EF_TRY(h->alloc(&w.ml2, NPL));
   EF_TRY(h->alloc(&w.P, (size_t)NV * NPL));
   EF_TRY(h->alloc(&w.tau_min_bits, 1));
   EF_TRY(h->alloc(&w.tau, 1));
@@ -433,6 +434,7 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
   EF_TRY(h->alloc(&w.bad_gid, 1));
   EF_CUDA(cudaMemset(w.d, 0, sizeof(double) * NPL));
   EF_CUDA(cudaMemset(w.ml, 0, sizeof(double) * NPL));
+  EF_CUDA(cudaMemset(w.ml2, 0, sizeof(double) * NPL));
   EF_CUDA(cudaMemset(w.P, 0, sizeof(double) * NV * NPL));
   EF_CUDA(cudaMemset(w.alpha, 0, sizeof(double) * NP));
   EF_CUDA(cudaMemset(w.R, 0, sizeof(double) * NV * NP));
@@ -942,7 +944,7 @@ int ef_debug_fetch(ef_solver* h, int32_t which, int32_t which_pass, double* out)
     case 3: return node_field(h->w.bounds, 3);
     case 4:  // min(l_ij, l_ji) of the last limiter pass
       (void)which_pass;
-      return slot_field(h->w.ml);
+      return slot_field(h->w.ml2);
     case 5: return node_field(h->w.eor, 1);
     case 6: return node_field(h->w.phi, 1);
     case 7: return node_field(h->Ubuf[h->cur], NV);

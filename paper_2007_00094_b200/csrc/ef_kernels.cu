@@ -519,18 +519,25 @@ __global__ void __launch_bounds__(TPB, EF_MINB_ELIM(D)) k_edge_lim(Layout m, Gas
       Pj[k] = w.P[(size_t)k * NPL + pt] * gj;
     }
   }
+  // The last pass q >= 1 leaves P_(q-1) and min(l) of pass q-1 in place: k_final
+  // forms the same product P_(q-1) (1 - min l) itself, which saves the largest
+  // write of the stage.  Every other pass stores its P_q.
+  const bool last = q == sp.passes - 1;
+  if (q == 0 || !last) {
 #pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    w.P[(size_t)k * NPL + p] = Pi[k];
-    w.P[(size_t)k * NPL + pt] = Pj[k];
+    for (int k = 0; k < NV; ++k) {
+      w.P[(size_t)k * NPL + p] = Pi[k];
+      w.P[(size_t)k * NPL + pt] = Pj[k];
+    }
   }
   double Un[NV];
   load_node<NV>(w.Unext, NP, i, Un);
   const double li = limiter<D>(Un, Pi, w.bounds[i], w.bounds[NP + i], w.bounds[2 * NP + i], sp.newton, g);
   load_node<NV>(w.Unext, NP, j, Un);
   const double lj = limiter<D>(Un, Pj, w.bounds[j], w.bounds[NP + j], w.bounds[2 * NP + j], sp.newton, g);
-  w.ml[p] = npmin(li, lj);   // row i: np.minimum(l_ij, l_ji)
-  w.ml[pt] = npmin(lj, li);  // row j: np.minimum(l_ji, l_ij)
+  double* __restrict__ ml = last ? w.ml2 : w.ml;
+  ml[p] = npmin(li, lj);   // row i: np.minimum(l_ij, l_ji)
+  ml[pt] = npmin(lj, li);  // row j: np.minimum(l_ji, l_ij)
 }
 
 // step5 (non-final pass): U_next_i += lam_i * sum_s min(l) P in slot order
@@ -580,13 +587,18 @@ __global__ void __launch_bounds__(TPB, EF_MINB_FINAL(D)) k_final(Layout m, Gas g
     double upd[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) upd[k] = 0.0;
+    const bool rescale = sp.passes >= 2;  // P of the last pass = P_(q-1) (1 - min l_(q-1))
     EF_UNROLL_FINAL
     for (int s = 0; s < card; ++s) {
       if (s == dg) continue;
       const int p = base + s * 32;
-      const double ml = w.ml[p];
+      const double ml = w.ml2[p];
+      const double gp = rescale ? 1.0 - w.ml[p] : 1.0;
 #pragma unroll
-      for (int k = 0; k < NV; ++k) upd[k] = upd[k] + ml * w.P[(size_t)k * NPL + p];
+      for (int k = 0; k < NV; ++k) {
+        const double Pk = rescale ? w.P[(size_t)k * NPL + p] * gp : w.P[(size_t)k * NPL + p];
+        upd[k] = upd[k] + ml * Pk;
+      }
     }
     const double lam = m.lam[i];
 #pragma unroll

@@ -76,7 +76,8 @@ struct Work {
   double* Unext;     // [NV][NP]
   double* bounds;    // [3][NP] rho_min, rho_max, phi_min
   double* d;         // [NP*L]
-  double* ml;        // [NP*L] min(l_ij, l_ji) of the current limiter pass
+  double* ml;        // [NP*L] min(l_ij, l_ji) of the current non-final limiter pass
+  double* ml2;       // [NP*L] min(l_ij, l_ji) of the last limiter pass
   double* P;         // [NV][NP*L] correction fluxes P_ij, rescaled in place per pass
   unsigned long long* tau_min_bits;  // CFL min over owned rows
   double* tau;       // tau of the current RK step / Euler step
