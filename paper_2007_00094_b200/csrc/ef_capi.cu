@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <array>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -167,8 +168,8 @@ struct ef_group {
   unsigned long long** bits_dev = nullptr;  // device array of the ranks' tau_min_bits
 };
 
-template <class T>
-static int upload(ef_solver* h, T** dst, const std::vector<T>& src) {
+template <class T, class A>
+static int upload(ef_solver* h, T** dst, const std::vector<T, A>& src) {
   EF_TRY(h->alloc(dst, src.size()));
   EF_CUDA(cudaMemcpy(*dst, src.data(), sizeof(T) * src.size(), cudaMemcpyHostToDevice));
   return EF_OK;
@@ -214,7 +215,9 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
     return fail(EF_ERR_ARG, "local rows/slots exceed 32-bit indexing (use more ranks)");
   h->gid_host = P.gid;
   h->orig_host.resize(n_local);
-  for (int64_t i = 0; i < n_local; ++i) h->orig_host[i] = P.cm_inv[P.gid[i]];
+  ef::parallel_for(n_local, [&](int64_t a, int64_t b, int) {
+    for (int64_t i = a; i < b; ++i) h->orig_host[i] = P.cm_inv[P.gid[i]];
+  });
   auto local_of = [&](int64_t g) -> int64_t {
     if (g >= P.s_lo && g < P.s_hi) return g - P.s_lo;
     auto it = std::lower_bound(P.gid.begin() + n_owned, P.gid.end(), g);
@@ -222,85 +225,115 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
     return -1;
   };
 
-  // SELL-32 host images
-  std::vector<int32_t> col(NPL);
-  std::vector<uint8_t> tslot(NPL, 0), card(NP, 1), cardf(NP, 1), diag(NP, 0);
-  std::vector<double> c((size_t)D * NPL, 0.0), mij(NPL, 0.0);
+  // SELL-32 host images, filled row by row on all host threads (every slot of
+  // every row, pads included, is written exactly once)
+  ef::hvec<int32_t> col(NPL);
+  ef::hvec<uint8_t> tslot(NPL);
+  ef::hvec<double> c((size_t)D * NPL), mij(NPL);
+  std::vector<uint8_t> card(NP, 1), cardf(NP, 1), diag(NP, 0);
   std::vector<double> m_i(NP, 1.0), inv_m(NP, 1.0), lam(NP, 1.0);
   std::vector<int64_t> gid(NP, 0);
-  for (int64_t i = 0; i < NP; ++i)
-    for (int s = 0; s < L; ++s) col[ef::sidx(i, s, L)] = (int32_t)std::min<int64_t>(i, n_local - 1);
-  int64_t nnz_owned = 0;
-  for (int64_t i = 0; i < n_local; ++i) {
-    const int64_t o = h->orig_host[i];
-    const int64_t cnt = P.rptr[i + 1] - P.rptr[i];
-    card[i] = (uint8_t)cnt;
-    if (i < n_owned) nnz_owned += cnt;
-    int dg = -1;
-    for (int64_t s = 0; s < cnt; ++s) {
-      const int64_t cg = P.rcm[P.rptr[i] + s];
-      const int64_t j = local_of(cg);
-      const int64_t q = P.rsrc[P.rptr[i] + s];
-      const int64_t p = ef::sidx(i, (int)s, L);
-      col[p] = (int32_t)j;
-      if (j == i) dg = (int)s;
-      mij[p] = mat->m[q];
-      for (int a = 0; a < D; ++a) c[(size_t)a * NPL + p] = mat->c[q * D + a];
-      // transpose slot: position of this row's CM id in row j (both rows local)
-      const int64_t* b = P.rcm.data() + P.rptr[j];
-      const int64_t* e = P.rcm.data() + P.rptr[j + 1];
-      const int64_t* it = std::lower_bound(b, e, P.gid[i]);
-      if (it == e || *it != P.gid[i]) return fail(EF_ERR_ARG, "stencil pattern is not structurally symmetric");
-      tslot[p] = (uint8_t)(it - b);
-    }
-    if (dg < 0) return fail(EF_ERR_ARG, "every stencil must contain its own row");
-    diag[i] = (uint8_t)dg;
-    cardf[i] = (uint8_t)(mat->indptr[o + 1] - mat->indptr[o]);
-    m_i[i] = mat->m_lumped[o];
-    inv_m[i] = mat->inv_m[o];
-    const int64_t den = std::max<int64_t>(cnt - 1, 1);
-    lam[i] = 1.0 / (double)den;  // stepper.py:214-215
-    gid[i] = P.gid[i];
-  }
-  h->nnz_owned = nnz_owned;
-  // upper-triangle edges with at least one owned endpoint (a ghost row's upper
-  // edge to an owned row is that row's lower entry)
-  std::vector<int32_t> edges;
-  for (int64_t sl = 0; sl < NP / 32; ++sl)
-    for (int s = 0; s < L; ++s)
-      for (int ln = 0; ln < 32; ++ln) {
-        const int64_t i = sl * 32 + ln;
-        if (i >= n_local || !(s > diag[i] && s < card[i])) continue;
-        if (i < n_owned || col[ef::sidx(i, s, L)] < n_owned) edges.push_back((int32_t)ef::sidx(i, s, L));
+  std::atomic<int64_t> nnz_acc{0};
+  std::atomic<int> bad{0};  // 1: not structurally symmetric, 2: missing diagonal
+  ef::parallel_for(NP, [&](int64_t a, int64_t b, int) {
+    int64_t nnz_part = 0;
+    for (int64_t i = a; i < b; ++i) {
+      const int64_t cnt = i < n_local ? P.rptr[i + 1] - P.rptr[i] : 0;
+      for (int64_t s = cnt; s < L; ++s) {  // pads (and padding rows): self column, zero values
+        const int64_t p = ef::sidx(i, (int)s, L);
+        col[p] = (int32_t)std::min<int64_t>(i, n_local - 1);
+        tslot[p] = 0;
+        mij[p] = 0.0;
+        for (int d = 0; d < D; ++d) c[(size_t)d * NPL + p] = 0.0;
       }
-  // static edge geometry (riemann.py:131-136): n = c / |c|, |c| = sqrt(R1(c*c)),
-  // for c_ij and c_ji, evaluated with the reference's operation order
+      if (i >= n_local) continue;
+      const int64_t o = h->orig_host[i];
+      card[i] = (uint8_t)cnt;
+      if (i < n_owned) nnz_part += cnt;
+      int dg = -1;
+      for (int64_t s = 0; s < cnt; ++s) {
+        const int64_t cg = P.rcm[P.rptr[i] + s];
+        const int64_t j = local_of(cg);
+        const int64_t q = P.rsrc[P.rptr[i] + s];
+        const int64_t p = ef::sidx(i, (int)s, L);
+        col[p] = (int32_t)j;
+        if (j == i) dg = (int)s;
+        mij[p] = mat->m[q];
+        for (int d = 0; d < D; ++d) c[(size_t)d * NPL + p] = mat->c[q * D + d];
+        // transpose slot: position of this row's CM id in row j (both rows local)
+        const int64_t* rb = P.rcm.data() + P.rptr[j];
+        const int64_t* re = P.rcm.data() + P.rptr[j + 1];
+        const int64_t* it = std::lower_bound(rb, re, P.gid[i]);
+        if (it == re || *it != P.gid[i]) {
+          bad.store(1);
+          tslot[p] = 0;
+        } else {
+          tslot[p] = (uint8_t)(it - rb);
+        }
+      }
+      if (dg < 0) {
+        bad.store(2);
+        dg = 0;
+      }
+      diag[i] = (uint8_t)dg;
+      cardf[i] = (uint8_t)(mat->indptr[o + 1] - mat->indptr[o]);
+      m_i[i] = mat->m_lumped[o];
+      inv_m[i] = mat->inv_m[o];
+      const int64_t den = std::max<int64_t>(cnt - 1, 1);
+      lam[i] = 1.0 / (double)den;  // stepper.py:214-215
+      gid[i] = P.gid[i];
+    }
+    nnz_acc += nnz_part;
+  }, 1024);
+  if (bad.load() == 1) return fail(EF_ERR_ARG, "stencil pattern is not structurally symmetric");
+  if (bad.load() == 2) return fail(EF_ERR_ARG, "every stencil must contain its own row");
+  h->nnz_owned = nnz_acc.load();
+  // upper-triangle edges with at least one owned endpoint (a ghost row's upper
+  // edge to an owned row is that row's lower entry), in ascending SELL position
+  std::vector<std::vector<int32_t>> epart(ef::par_threads());
+  const int nch = ef::parallel_for(NP / 32, [&](int64_t a, int64_t b, int t) {
+    auto& out = epart[t];
+    for (int64_t sl = a; sl < b; ++sl)
+      for (int s = 0; s < L; ++s)
+        for (int ln = 0; ln < 32; ++ln) {
+          const int64_t i = sl * 32 + ln;
+          if (i >= n_local || !(s > diag[i] && s < card[i])) continue;
+          if (i < n_owned || col[ef::sidx(i, s, L)] < n_owned) out.push_back((int32_t)ef::sidx(i, s, L));
+        }
+  }, 256);
+  std::vector<int32_t> edges;
+  for (int t = 0; t < nch; ++t) edges.insert(edges.end(), epart[t].begin(), epart[t].end());
+  epart.clear();
   const int64_t NE = (int64_t)edges.size();
   // endpoint tables: the edge kernels read j and the transposed position with
   // the edge position (one coalesced load each) instead of through col/tslot
   std::vector<int32_t> edge_j(std::max<int64_t>(NE, 1), 0), edge_pt(std::max<int64_t>(NE, 1), 0);
-  for (int64_t e = 0; e < NE; ++e) {
-    edge_j[e] = col[edges[e]];
-    edge_pt[e] = (int32_t)ef::sidx(col[edges[e]], tslot[edges[e]], L);
-  }
-  std::vector<double> egeo((size_t)2 * (D + 1) * std::max<int64_t>(NE, 1), 0.0);
-  for (int64_t e = 0; e < NE; ++e) {
-    const int64_t p = edges[e];
-    const int64_t pt = ef::sidx(col[p], tslot[p], L);
-    for (int dir = 0; dir < 2; ++dir) {
-      const int64_t q = dir ? pt : p;
-      volatile double ss = 0.0;  // ((0 + c0^2) + c1^2) + c2^2, no contraction
-      for (int a = 0; a < D; ++a) {
-        volatile double sq = c[(size_t)a * NPL + q] * c[(size_t)a * NPL + q];
-        ss = ss + sq;
+  // static edge geometry (riemann.py:131-136): n = c / |c|, |c| = sqrt(R1(c*c)),
+  // for c_ij and c_ji, evaluated with the reference's operation order
+  ef::hvec<double> egeo((size_t)2 * (D + 1) * std::max<int64_t>(NE, 1));
+  if (NE == 0)
+    for (auto& v : egeo) v = 0.0;
+  ef::parallel_for(NE, [&](int64_t a, int64_t b, int) {
+    for (int64_t e = a; e < b; ++e) {
+      const int64_t p = edges[e];
+      const int64_t pt = ef::sidx(col[p], tslot[p], L);
+      edge_j[e] = col[p];
+      edge_pt[e] = (int32_t)pt;
+      for (int dir = 0; dir < 2; ++dir) {
+        const int64_t q = dir ? pt : p;
+        volatile double ss = 0.0;  // ((0 + c0^2) + c1^2) + c2^2, no contraction
+        for (int d = 0; d < D; ++d) {
+          volatile double sq = c[(size_t)d * NPL + q] * c[(size_t)d * NPL + q];
+          ss = ss + sq;
+        }
+        const double nrm = std::sqrt((double)ss);
+        const int base = dir * (D + 1);
+        for (int d = 0; d < D; ++d)
+          egeo[(size_t)(base + d) * NE + e] = nrm > 0.0 ? c[(size_t)d * NPL + q] / nrm : (d == 0 ? 1.0 : 0.0);
+        egeo[(size_t)(base + D) * NE + e] = nrm;
       }
-      const double nrm = std::sqrt((double)ss);
-      const int base = dir * (D + 1);
-      for (int a = 0; a < D; ++a)
-        egeo[(size_t)(base + a) * NE + e] = nrm > 0.0 ? c[(size_t)a * NPL + q] / nrm : (a == 0 ? 1.0 : 0.0);
-      egeo[(size_t)(base + D) * NE + e] = nrm;
     }
-  }
+  });
   // boundary data (stepper.py:258-267): owned rows only
   std::vector<int8_t> bc_kind(NP, 0);
   std::vector<double> bc_n((size_t)D * NP, 0.0);

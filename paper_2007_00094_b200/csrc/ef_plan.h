@@ -17,9 +17,12 @@
 // CPU tests exercise these plans across gloo ranks.
 #pragma once
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <string>
 #include <vector>
+
+#include "ef_par.h"
 
 namespace ef {
 
@@ -30,7 +33,8 @@ struct Plan {
   std::vector<int64_t> ranges;        // nranks + 1
   std::vector<int64_t> cm_inv;        // CM id -> original id
   std::vector<int64_t> gid;           // local row -> CM id
-  std::vector<int64_t> rptr, rcm, rsrc;  // local stencils: CM column ids, source nnz index
+  std::vector<int64_t> rptr;          // local stencils: row pointers,
+  hvec<int64_t> rcm, rsrc;            // CM column ids, source nnz index
   // halo plans, one entry per peer rank (index = peer rank, empty when none)
   std::vector<std::vector<int64_t>> send_rows, recv_rows;  // local row ids
   std::vector<std::vector<int64_t>> send_slots, recv_slots;  // local row * 256 + slot
@@ -85,17 +89,25 @@ inline bool build_plan(int64_t n, const int64_t* indptr, const int64_t* indices,
   }
   P.L = (int)L;
   P.standard_card = (int)(std::max_element(hist.begin(), hist.end()) - hist.begin());
-  // ghost layer of every rank (exchange.py:419-422)
+  // ghost layer of every rank (exchange.py:419-422); none with one rank
   std::vector<std::vector<int64_t>> ghosts(nranks);
-  for (int q = 0; q < nranks; ++q) {
-    auto& gq = ghosts[q];
-    for (int64_t g = P.ranges[q]; g < P.ranges[q + 1]; ++g) {
-      const int64_t o = P.cm_inv[g];
-      for (int64_t k = indptr[o]; k < indptr[o + 1]; ++k) {
-        const int64_t c = cm_perm[indices[k]];
-        if (c < P.ranges[q] || c >= P.ranges[q + 1]) gq.push_back(c);
+  for (int q = 0; q < nranks && nranks > 1; ++q) {
+    const int64_t lo = P.ranges[q], hi = P.ranges[q + 1];
+    std::vector<std::vector<int64_t>> part(par_threads());
+    const int nch = parallel_for(hi - lo, [&](int64_t a, int64_t b, int t) {
+      auto& out = part[t];
+      for (int64_t g = lo + a; g < lo + b; ++g) {
+        const int64_t o = P.cm_inv[g];
+        for (int64_t k = indptr[o]; k < indptr[o + 1]; ++k) {
+          const int64_t c = cm_perm[indices[k]];
+          if (c < lo || c >= hi) out.push_back(c);
+        }
       }
-    }
+      std::sort(out.begin(), out.end());
+      out.erase(std::unique(out.begin(), out.end()), out.end());
+    });
+    auto& gq = ghosts[q];
+    for (int t = 0; t < nch; ++t) gq.insert(gq.end(), part[t].begin(), part[t].end());
     std::sort(gq.begin(), gq.end());
     gq.erase(std::unique(gq.begin(), gq.end()), gq.end());
   }
@@ -113,24 +125,39 @@ inline bool build_plan(int64_t n, const int64_t* indptr, const int64_t* indices,
   for (size_t k = 0; k < mine.size(); ++k) P.gid[P.n_owned + k] = mine[k];
   // local stencils sorted by CM id; ghost rows truncated to local columns
   P.rptr.assign(P.n_local + 1, 0);
-  P.rcm.clear();
-  P.rsrc.clear();
-  std::vector<std::pair<int64_t, int64_t>> tmp;
-  for (int64_t i = 0; i < P.n_local; ++i) {
-    const int64_t o = P.cm_inv[P.gid[i]];
-    tmp.clear();
-    for (int64_t k = indptr[o]; k < indptr[o + 1]; ++k) {
-      const int64_t c = cm_perm[indices[k]];
-      if (i >= P.n_owned && !is_local(rank, c)) continue;
-      tmp.emplace_back(c, k);
+  parallel_for(P.n_local, [&](int64_t a, int64_t b, int) {
+    for (int64_t i = a; i < b; ++i) {
+      const int64_t o = P.cm_inv[P.gid[i]];
+      int64_t cnt = indptr[o + 1] - indptr[o];
+      if (i >= P.n_owned) {
+        cnt = 0;
+        for (int64_t k = indptr[o]; k < indptr[o + 1]; ++k) cnt += is_local(rank, cm_perm[indices[k]]) ? 1 : 0;
+      }
+      P.rptr[i + 1] = cnt;
     }
-    std::sort(tmp.begin(), tmp.end());
-    for (auto& t : tmp) {
-      P.rcm.push_back(t.first);
-      P.rsrc.push_back(t.second);
+  });
+  for (int64_t i = 0; i < P.n_local; ++i) P.rptr[i + 1] += P.rptr[i];
+  P.rcm.resize(P.rptr[P.n_local]);
+  P.rsrc.resize(P.rptr[P.n_local]);
+  parallel_for(P.n_local, [&](int64_t a, int64_t b, int) {
+    std::vector<std::pair<int64_t, int64_t>> tmp;
+    for (int64_t i = a; i < b; ++i) {
+      const int64_t o = P.cm_inv[P.gid[i]];
+      tmp.clear();
+      for (int64_t k = indptr[o]; k < indptr[o + 1]; ++k) {
+        const int64_t c = cm_perm[indices[k]];
+        if (i >= P.n_owned && !is_local(rank, c)) continue;
+        tmp.emplace_back(c, k);
+      }
+      std::sort(tmp.begin(), tmp.end());
+      int64_t q = P.rptr[i];
+      for (auto& t : tmp) {
+        P.rcm[q] = t.first;
+        P.rsrc[q] = t.second;
+        ++q;
+      }
     }
-    P.rptr[i + 1] = (int64_t)P.rcm.size();
-  }
+  });
   // halo plans
   P.send_rows.assign(nranks, {});
   P.recv_rows.assign(nranks, {});

@@ -22,6 +22,8 @@ from __future__ import annotations
 from dataclasses import dataclass
 from typing import Callable, Optional
 
+import os
+
 import numpy as np
 import scipy.sparse as sp
 
@@ -507,16 +509,27 @@ def periodic_box_matrices(n: int) -> PrecomputedMatrices:
     for k in range(1, 27):
         m_i = m_i + m_sym[k]
     N = n ** 3
+    # Away from the periodic seams every row's columns are i + flat(o), already
+    # sorted by the offsets' flat order; only the seam rows need a per-row sort.
+    flat = (offs[:, 0] * n + offs[:, 1]) * n + offs[:, 2]
+    base_order = np.argsort(flat, kind="stable")
+    cols = np.arange(N, dtype=np.int64)[:, None] + flat[base_order][None, :]
+    m = np.broadcast_to(m_sym[base_order], (N, 27)).copy()
+    c = np.broadcast_to(c_off[base_order], (N, 27, 3)).copy()
     ix, iy, iz = np.unravel_index(np.arange(N, dtype=np.int64), (n, n, n))
-    cols = np.empty((N, 27), dtype=np.int64)
-    for k, o in enumerate(offs):
-        cols[:, k] = (((ix + o[0]) % n) * n + (iy + o[1]) % n) * n + (iz + o[2]) % n
-    order = np.argsort(cols, axis=1, kind="stable")
-    cols = np.take_along_axis(cols, order, axis=1)
+    seam = np.flatnonzero((ix == 0) | (ix == n - 1) | (iy == 0) | (iy == n - 1) | (iz == 0) | (iz == n - 1))
+    sx, sy, sz = ix[seam], iy[seam], iz[seam]
     del ix, iy, iz
-    m = m_sym[order].ravel()
-    c = c_off[order].reshape(-1, 3)
-    del order
+    sc = np.empty((len(seam), 27), dtype=np.int64)
+    for k, o in enumerate(offs):
+        sc[:, k] = (((sx + o[0]) % n) * n + (sy + o[1]) % n) * n + (sz + o[2]) % n
+    order = np.argsort(sc, axis=1, kind="stable")
+    cols[seam] = np.take_along_axis(sc, order, axis=1)
+    m[seam] = m_sym[order]
+    c[seam] = c_off[order]
+    del sc, order, sx, sy, sz, seam
+    m = m.ravel()
+    c = c.reshape(-1, 3)
     m_lumped = np.full(N, m_i)
     return PrecomputedMatrices(n=N, dim=3, indptr=np.arange(0, 27 * N + 1, 27, dtype=np.int64),
                                indices=cols.ravel(), m=m, c=c, beta=np.zeros(0), m_lumped=m_lumped,
@@ -534,15 +547,30 @@ def periodic_fourier_box(n: int = 320, seed: int = 2007, gas: GasConstants = AIR
     mesh = None
     rng = np.random.default_rng(seed)
     fields = []
-    for _ in range(5):
-        k = rng.integers(-2, 3, (modes, 3))
-        while np.any(np.all(k == 0, axis=1)):
-            bad = np.all(k == 0, axis=1)
-            k[bad] = rng.integers(-2, 3, (int(bad.sum()), 3))
-        a = rng.uniform(-1.0, 1.0, modes)
-        ph = rng.uniform(0.0, 2.0 * np.pi, modes)
-        gsum = np.sin(2.0 * np.pi * (rep @ k.T) + ph[None, :]) @ a
-        fields.append(gsum / np.abs(a).sum())
+    chunk = 1 << 20  # row chunks evaluated on all host threads (numpy releases the GIL)
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 1) as pool:
+        for _ in range(5):
+            k = rng.integers(-2, 3, (modes, 3))
+            while np.any(np.all(k == 0, axis=1)):
+                bad = np.all(k == 0, axis=1)
+                k[bad] = rng.integers(-2, 3, (int(bad.sum()), 3))
+            a = rng.uniform(-1.0, 1.0, modes)
+            ph = rng.uniform(0.0, 2.0 * np.pi, modes)
+            gsum = np.empty(len(rep))
+
+            def part(lo, k=k, a=a, ph=ph, gsum=gsum):
+                # elementwise in a fixed order, so the values do not depend on the chunking
+                r = rep[lo:lo + chunk]
+                acc = np.zeros(len(r))
+                for q in range(modes):
+                    kx = (r[:, 0] * k[q, 0] + r[:, 1] * k[q, 1]) + r[:, 2] * k[q, 2]
+                    acc += a[q] * np.sin(2.0 * np.pi * kx + ph[q])
+                gsum[lo:lo + chunk] = acc
+
+            list(pool.map(part, range(0, len(rep), chunk)))
+            fields.append(gsum / np.abs(a).sum())
     rho = 1.0 + 0.5 * fields[0]
     p = 1.0 + 0.5 * fields[1]
     vel = np.column_stack(fields[2:5]) / np.sqrt(3.0)
