@@ -54,6 +54,10 @@ typedef struct {
   double c_cfl;              /* (0, 1]                       */
   int32_t limiter_passes;    /* >= 0                         */
   int32_t newton_steps;      /* >= 0                         */
+  int32_t overlap;           /* Solver(overlap=...), stepper.py:97: with several
+                                ranks, compute the exported rows first and move
+                                their halo while the interior rows are computed
+                                (exchange.py:168-222); results are identical   */
 } ef_params;
 
 /* BoundaryConditions, stepper.py:40-52 (original node ids) */

@@ -29,7 +29,7 @@ class EfMatrices(ctypes.Structure):
 class EfParams(ctypes.Structure):
     _fields_ = [("gamma", _d), ("gm1", _d), ("gp1_inv", _d), ("gm1_over_2g", _d),
                 ("two_g_over_gm1", _d), ("c_cfl", _d), ("limiter_passes", _i32),
-                ("newton_steps", _i32)]
+                ("newton_steps", _i32), ("overlap", _i32)]
 
 
 class EfBoundary(ctypes.Structure):

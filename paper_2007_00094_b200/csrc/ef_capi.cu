@@ -16,6 +16,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -125,6 +126,13 @@ struct ef_solver {
   int64_t n_send_rows = 0, n_recv_rows = 0, n_send_pos = 0, n_recv_pos = 0;
   double *sendbuf = nullptr, *recvbuf = nullptr;
   int64_t sync_count = 0, sync_volume = 0;  // Solver.comm counters (exchange.py:131-157)
+  // communication overlap (stepper.py Alg. 4, exchange.py:168-222): rows other
+  // ranks import (a prefix and a suffix of the CM range) are computed first,
+  // their halo travels on `cst` while the interior rows are computed on `st`
+  bool overlap = true;
+  ef::RowSet rs_all, rs_B, rs_I;
+  cudaStream_t cst = nullptr;
+  cudaEvent_t evB = nullptr, evX = nullptr;
   // pinned readback block
   struct Readback {
     double tau;
@@ -159,6 +167,9 @@ struct ef_solver {
     for (auto& set : ring)
       for (auto& e : set) cudaEventDestroy(e);
     if (comm && nccl().ok) nccl().CommDestroy(comm);
+    if (evB) cudaEventDestroy(evB);
+    if (evX) cudaEventDestroy(evX);
+    if (cst) cudaStreamDestroy(cst);
     if (own_stream && st) cudaStreamDestroy(st);
   }
 };
@@ -387,6 +398,45 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
   }
   h->n_send_rows = (int64_t)srows.size();
   h->n_recv_rows = (int64_t)rrows.size();
+  // exported rows B = [0, a) u [b, n_owned) with the fewest rows covering every
+  // send row (RCM keeps them near both ends of the range); interior = [a, b)
+  h->rs_all = ef::all_rows(n_owned);
+  h->rs_B = ef::all_rows(n_owned);
+  h->rs_I = ef::all_rows(0);
+  if (R > 1) {
+    std::vector<int64_t> sr(srows.begin(), srows.end());
+    std::sort(sr.begin(), sr.end());
+    sr.erase(std::unique(sr.begin(), sr.end()), sr.end());
+    int64_t best_a = 0, best_b = n_owned, best = -1;
+    for (size_t k = 0; k <= sr.size(); ++k) {  // rows sr[0..k) low, sr[k..) high
+      const int64_t a = k > 0 ? sr[k - 1] + 1 : 0;
+      const int64_t b = k < sr.size() ? sr[k] : n_owned;
+      if (a > b) continue;
+      const int64_t cost = a + (n_owned - b);
+      if (best < 0 || cost < best) {
+        best = cost;
+        best_a = a;
+        best_b = b;
+      }
+    }
+    if (best < 0) {  // cannot happen (k = 0 covers everything); keep all rows exported
+      best_a = n_owned;
+      best_b = n_owned;
+    }
+    ef::RowSet B;
+    B.r0 = 0;
+    B.n0 = (int)best_a;
+    B.r2 = (int)best_b;
+    B.n = (int)(best_a + (n_owned - best_b));
+    B.lead = 1;
+    ef::RowSet I;
+    I.r0 = (int)best_a;
+    I.n0 = I.n = (int)(best_b - best_a);
+    I.r2 = (int)best_b;
+    I.lead = 0;
+    h->rs_B = B;
+    h->rs_I = I;
+  }
   h->n_send_pos = (int64_t)spos.size();
   h->n_recv_pos = (int64_t)rpos.size();
 
@@ -444,8 +494,9 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
     EF_TRY(upload(h, &h->recv_rows, rrows));
     EF_TRY(upload(h, &h->send_pos, spos));
     EF_TRY(upload(h, &h->recv_pos, rpos));
-    const int64_t sb = std::max(h->n_send_rows * NV, h->n_send_pos);
-    const int64_t rbn = std::max(h->n_recv_rows * NV, h->n_recv_pos);
+    // the widest message row: R, U^L and bounds after the low-order update
+    const int64_t sb = std::max(h->n_send_rows * (2 * NV + 3), h->n_send_pos);
+    const int64_t rbn = std::max(h->n_recv_rows * (2 * NV + 3), h->n_recv_pos);
     EF_TRY(h->alloc(&h->sendbuf, sb));
     EF_TRY(h->alloc(&h->recvbuf, rbn));
   }
@@ -523,66 +574,69 @@ static int mark(ef_solver* h, int k) {
   return EF_OK;
 }
 
-// Halo exchange of one field (exchange.py:145-157 semantics: owners' values
-// overwrite the ghost copies).  rows: ncomp doubles per row; slots: ncomp == 1.
-// `field(r)` returns rank r's device array (index into Driver::hs).
-template <class FieldOf>
-static int exchange(Driver& d, bool slots, int ncomp, FieldOf field) {
+// Halo exchange of several row fields in one message per peer
+// (exchange.py:145-157 semantics: owners' values overwrite the ghost copies).
+// A message row holds the fields' components back to back; `fld.of(r)` is rank
+// r's device array (index into Driver::hs).  Everything runs on stream `s`.
+struct Fld {
+  std::function<double*(size_t)> of;
+  int ncomp;
+};
+static int exchange(Driver& d, const std::vector<Fld>& flds, cudaStream_t s) {
   if (!d.multi()) return EF_OK;
+  int C = 0;
+  for (const Fld& f : flds) C += f.ncomp;
   for (size_t r = 0; r < d.hs.size(); ++r) {
     ef_solver* h = d.hs[r];
-    if (slots)
-      ef::launch_pack_pos(field(r), h->send_pos, h->n_send_pos, h->sendbuf, h->st);
-    else
-      ef::launch_pack_rows(field(r), ncomp, h->NP, h->send_rows, h->n_send_rows, h->sendbuf, h->st);
+    int off = 0;
+    for (const Fld& f : flds) {
+      ef::launch_pack_rows(f.of(r), f.ncomp, h->NP, h->send_rows, h->n_send_rows, h->sendbuf, C, off, s);
+      off += f.ncomp;
+    }
   }
   if (d.group) {
     for (ef_solver* h : d.hs)
       for (int q = 0; q < h->nranks; ++q) {
-        const int64_t cnt = slots ? h->xr_slots[q] : h->xr_rows[q] * ncomp;
+        const int64_t cnt = h->xr_rows[q] * C;
         if (cnt == 0) continue;
         ef_solver* src = d.hs[q];
-        const int64_t soff = slots ? src->os_slots[h->rank] : src->os_rows[h->rank] * ncomp;
-        const int64_t roff = slots ? h->or_slots[q] : h->or_rows[q] * ncomp;
-        EF_CUDA(cudaMemcpyAsync(h->recvbuf + roff, src->sendbuf + soff, sizeof(double) * cnt,
-                                cudaMemcpyDeviceToDevice, h->st));
+        EF_CUDA(cudaMemcpyAsync(h->recvbuf + h->or_rows[q] * C, src->sendbuf + src->os_rows[h->rank] * C,
+                                sizeof(double) * cnt, cudaMemcpyDeviceToDevice, s));
       }
   } else {
     ef_solver* h = d.h0();
     EF_NCCL(nccl().GroupStart());
     for (int q = 0; q < h->nranks; ++q) {
-      const int64_t sc = slots ? h->xs_slots[q] : h->xs_rows[q] * ncomp;
-      const int64_t rc = slots ? h->xr_slots[q] : h->xr_rows[q] * ncomp;
-      const int64_t so = slots ? h->os_slots[q] : h->os_rows[q] * ncomp;
-      const int64_t ro = slots ? h->or_slots[q] : h->or_rows[q] * ncomp;
-      if (sc) EF_NCCL(nccl().Send(h->sendbuf + so, (size_t)sc, ncclFloat64, q, h->comm, h->st));
-      if (rc) EF_NCCL(nccl().Recv(h->recvbuf + ro, (size_t)rc, ncclFloat64, q, h->comm, h->st));
+      const int64_t sc = h->xs_rows[q] * C, rc = h->xr_rows[q] * C;
+      if (sc) EF_NCCL(nccl().Send(h->sendbuf + h->os_rows[q] * C, (size_t)sc, ncclFloat64, q, h->comm, s));
+      if (rc) EF_NCCL(nccl().Recv(h->recvbuf + h->or_rows[q] * C, (size_t)rc, ncclFloat64, q, h->comm, s));
     }
     EF_NCCL(nccl().GroupEnd());
   }
   for (size_t r = 0; r < d.hs.size(); ++r) {
     ef_solver* h = d.hs[r];
-    if (slots)
-      ef::launch_unpack_pos(field(r), h->recv_pos, h->n_recv_pos, h->recvbuf, h->st);
-    else
-      ef::launch_unpack_rows(field(r), ncomp, h->NP, h->recv_rows, h->n_recv_rows, h->recvbuf, h->st);
+    int off = 0;
+    for (const Fld& f : flds) {
+      ef::launch_unpack_rows(f.of(r), f.ncomp, h->NP, h->recv_rows, h->n_recv_rows, h->recvbuf, C, off, s);
+      off += f.ncomp;
+    }
     h->sync_count++;
-    h->sync_volume += slots ? h->n_recv_pos : h->n_recv_rows * ncomp;
+    h->sync_volume += h->n_recv_rows * C;
   }
   return EF_OK;
 }
 
 // allreduce_min of the CFL bound (exchange.py:160-165): bit patterns of
 // positive doubles order like their values, so a uint64 min is exact.
-static int allreduce_tau(Driver& d) {
+static int allreduce_tau(Driver& d, cudaStream_t s) {
   if (!d.multi()) return EF_OK;
   if (d.group) {
-    ef::launch_group_min(d.bits_dev, (int)d.hs.size(), d.h0()->st);
+    ef::launch_group_min(d.bits_dev, (int)d.hs.size(), s);
     EF_CUDA(cudaGetLastError());
     return EF_OK;
   }
   ef_solver* h = d.h0();
-  EF_NCCL(nccl().AllReduce(h->w.tau_min_bits, h->w.tau_min_bits, 1, ncclUint64, ncclMin, h->comm, h->st));
+  EF_NCCL(nccl().AllReduce(h->w.tau_min_bits, h->w.tau_min_bits, 1, ncclUint64, ncclMin, h->comm, s));
   return EF_OK;
 }
 
@@ -597,43 +651,71 @@ static int run_stage(Driver& d, const std::vector<StageIO>& io, StageParams sp) 
   auto each = [&](auto fn) {
     for (size_t r = 0; r < d.hs.size(); ++r) fn(d.hs[r], io[r]);
   };
-  ef_solver* t = d.h0();  // timers are kept on the first handle
+  ef_solver* t = d.h0();  // timers, comm stream and events are kept on the first handle
+  const bool multi = d.multi();
+  const bool ov = multi && t->overlap;
+  cudaStream_t st = t->st;  // the ranks of a same-device group share it
+  const int NV = t->nvar;
+  // Run a row kernel launch(h, x, rows) over the owned rows, then the halo
+  // exchange of `flds`.  With overlap: exported rows first, their halo on the
+  // comm stream while the interior rows run, joined before the next phase.
+  auto produce = [&](auto launch, const std::vector<Fld>& flds) -> int {
+    if (!multi || flds.empty()) {
+      each([&](ef_solver* h, const StageIO& x) { launch(h, x, h->rs_all); });
+      return EF_OK;
+    }
+    if (!ov) {
+      each([&](ef_solver* h, const StageIO& x) { launch(h, x, h->rs_all); });
+      return exchange(d, flds, st);
+    }
+    each([&](ef_solver* h, const StageIO& x) { launch(h, x, h->rs_B); });
+    EF_CUDA(cudaEventRecord(t->evB, st));
+    EF_CUDA(cudaStreamWaitEvent(t->cst, t->evB, 0));
+    EF_TRY(exchange(d, flds, t->cst));
+    EF_CUDA(cudaEventRecord(t->evX, t->cst));
+    each([&](ef_solver* h, const StageIO& x) { launch(h, x, h->rs_I); });
+    EF_CUDA(cudaStreamWaitEvent(st, t->evX, 0));
+    return EF_OK;
+  };
+  auto fld = [&](double* Work::*member, int ncomp) {
+    return Fld{[&d, member](size_t r) { return d.hs[r]->w.*member; }, ncomp};
+  };
   EF_TRY(mark(t, 0));
   EF_TRY(mark(t, 1));  // step0 is fused into the previous stage's final kernel
-  each([&](ef_solver* h, const StageIO& x) { ef::launch_edge_visc(h->dim, h->lay, h->gas, x.U, h->w, want_tau, h->st); });
+  each([&](ef_solver* h, const StageIO& x) { ef::launch_edge_visc(h->dim, h->lay, h->gas, x.U, h->w, want_tau, st); });
   EF_TRY(mark(t, 2));
-  each([&](ef_solver* h, const StageIO& x) { ef::launch_row_visc(h->dim, h->lay, h->gas, x.U, h->w, want_tau, h->st); });
-  EF_TRY(exchange(d, false, 1, [&d](size_t r) { return d.hs[r]->w.alpha; }));
-  if (want_tau) EF_TRY(allreduce_tau(d));
+  EF_TRY(produce([&](ef_solver* h, const StageIO& x, ef::RowSet rs) {
+    ef::launch_row_visc(h->dim, h->lay, h->gas, x.U, h->w, want_tau, rs, st);
+  }, {fld(&Work::alpha, 1)}));
+  if (want_tau) EF_TRY(allreduce_tau(d, st));
   EF_TRY(mark(t, 3));
-  each([&](ef_solver* h, const StageIO& x) { ef::launch_low_order(h->dim, h->lay, h->gas, x.U, h->w, sp, h->st); });
-  // ghost rows: R for P, U^L and bounds for their own limiter side
-  EF_TRY(exchange(d, false, t->nvar, [&d](size_t r) { return d.hs[r]->w.R; }));
-  if (t->passes > 0) {
-    EF_TRY(exchange(d, false, t->nvar, [&d](size_t r) { return d.hs[r]->w.Unext; }));
-    EF_TRY(exchange(d, false, 3, [&d](size_t r) { return d.hs[r]->w.bounds; }));
-  }
+  // ghost rows need R for P, U^L and bounds for their own limiter side
+  std::vector<Fld> lo_flds;
+  if (t->passes > 0) lo_flds = {fld(&Work::R, NV), fld(&Work::Unext, NV), fld(&Work::bounds, 3)};
+  EF_TRY(produce([&](ef_solver* h, const StageIO& x, ef::RowSet rs) {
+    ef::launch_low_order(h->dim, h->lay, h->gas, x.U, h->w, sp, rs, st);
+  }, lo_flds));
   EF_TRY(mark(t, 4));
   if (t->passes > 0) {
-    each([&](ef_solver* h, const StageIO& x) { ef::launch_edge_lim(h->dim, h->lay, h->gas, x.U, h->w, sp, 0, h->st); });
+    each([&](ef_solver* h, const StageIO& x) { ef::launch_edge_lim(h->dim, h->lay, h->gas, x.U, h->w, sp, 0, st); });
     EF_TRY(mark(t, 5));
     for (int p = 0; p + 1 < t->passes; ++p) {
-      each([&](ef_solver* h, const StageIO& x) { ef::launch_row_upd(h->dim, h->lay, h->gas, x.U, h->w, sp, h->st); });
-      EF_TRY(exchange(d, false, t->nvar, [&d](size_t r) { return d.hs[r]->w.Unext; }));
-      each([&](ef_solver* h, const StageIO& x) { ef::launch_edge_lim(h->dim, h->lay, h->gas, x.U, h->w, sp, p + 1, h->st); });
+      EF_TRY(produce([&](ef_solver* h, const StageIO& x, ef::RowSet rs) {
+        ef::launch_row_upd(h->dim, h->lay, h->gas, x.U, h->w, sp, rs, st);
+      }, {fld(&Work::Unext, NV)}));
+      each([&](ef_solver* h, const StageIO& x) { ef::launch_edge_lim(h->dim, h->lay, h->gas, x.U, h->w, sp, p + 1, st); });
     }
     EF_TRY(mark(t, 6));
   } else {
     EF_TRY(mark(t, 5));
     EF_TRY(mark(t, 6));
   }
-  each([&](ef_solver* h, const StageIO& x) {
-    ef::launch_final(h->dim, h->lay, h->gas, x.U, x.U0, x.Uout, h->w, sp, h->st);
-  });
-  if (d.multi()) {
-    EF_TRY(exchange(d, false, t->nvar, [&io](size_t r) { return io[r].Uout; }));
+  EF_TRY(produce([&](ef_solver* h, const StageIO& x, ef::RowSet rs) {
+    ef::launch_final(h->dim, h->lay, h->gas, x.U, x.U0, x.Uout, h->w, sp, rs, st);
+  }, {Fld{[&io](size_t r) { return io[r].Uout; }, NV}}));
+  if (multi) {
     each([&](ef_solver* h, const StageIO& x) {  // step0 of the ghost rows
-      ef::launch_nodal(h->dim, h->lay, h->gas, x.Uout, h->w, h->n_owned, h->n_local, h->st);
+      ef::launch_nodal(h->dim, h->lay, h->gas, x.Uout, h->w, h->n_owned, h->n_local, st);
     });
   }
   EF_TRY(mark(t, 7));
@@ -823,8 +905,15 @@ int ef_create(const ef_matrices* mat, const ef_params* prm, const ef_boundary* b
     if (e != cudaSuccess) return bail(fail(EF_ERR_CUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(e)));
     h->own_stream = true;
   }
+  h->overlap = prm->overlap != 0;
   int rc = build(h, mat, bc, dist);
   if (rc != EF_OK) return bail(rc);
+  if (h->nranks > 1) {
+    e = cudaStreamCreateWithFlags(&h->cst, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->evB, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->evX, cudaEventDisableTiming);
+    if (e != cudaSuccess) return bail(fail(EF_ERR_CUDA, std::string("comm stream: ") + cudaGetErrorString(e)));
+  }
   if (h->nranks > 1 && dist->nccl_id) {
     if (!nccl().ok) return bail(fail(EF_ERR_NCCL, "libnccl.so.2 could not be loaded"));
     ncclUniqueId id;

@@ -217,12 +217,14 @@ __device__ __forceinline__ void row_pipe(const int* __restrict__ col, int base, 
 
 template <int D>
 __global__ void __launch_bounds__(TPB, EF_MINB_ROW(D)) k_row_visc(Layout m, Gas g, const double* __restrict__ U,
-                                                  Work w, int want_tau) {
+                                                  Work w, int want_tau, RowSet rs) {
   constexpr int NV = D + 2;
-  const int i = blockIdx.x * TPB + threadIdx.x;
+  const int t0 = blockIdx.x * TPB + threadIdx.x;
+  const bool act = t0 < rs.n;
+  const int i = act ? rs.row(t0) : 0;
   double cand = __longlong_as_double(0x7ff0000000000000LL);
   bool bad = false;
-  if (i < m.n_owned) {
+  if (act) {
     const int NP = (int)m.NP;
     const int L = m.L;
     const int NPL = NP * L;
@@ -371,17 +373,18 @@ __device__ __forceinline__ double stage_tau(const Work& w, const StageParams& sp
 
 template <int D>
 __global__ void __launch_bounds__(TPB, EF_MINB_LOW(D)) k_low_order(Layout m, Gas g, const double* __restrict__ U,
-                                                   Work w, StageParams sp) {
+                                                   Work w, StageParams sp, RowSet rs) {
   constexpr int NV = D + 2;
   const double tau = stage_tau(w, sp);
-  const int i = blockIdx.x * TPB + threadIdx.x;
-  if (i == 0 && sp.tau_mode != TAU_DEVICE) {
+  const int t0 = blockIdx.x * TPB + threadIdx.x;
+  if (t0 == 0 && rs.lead && sp.tau_mode != TAU_DEVICE) {
     *w.tau = tau;
     if (sp.tau_mode == TAU_CFL &&
         !(__longlong_as_double((long long)*w.tau_min_bits) < __longlong_as_double(0x7ff0000000000000LL)))
       atomicOr(w.err, ERR_TAU_UNBOUNDED);
   }
-  if (i >= m.n_owned) return;
+  if (t0 >= rs.n) return;
+  const int i = rs.row(t0);
   const int NP = (int)m.NP;
   const int L = m.L;
   const int NPL = NP * L;
@@ -544,10 +547,11 @@ __global__ void __launch_bounds__(TPB, EF_MINB_ELIM(D)) k_edge_lim(Layout m, Gas
 // (stepper.py:478-481); the rescale of P belongs to the next k_edge_lim.
 template <int D>
 __global__ void __launch_bounds__(TPB, EF_MINB_PASS(D)) k_row_upd(Layout m, Gas g, const double* __restrict__ U,
-                                                                Work w, StageParams sp) {
+                                                                Work w, StageParams sp, RowSet rs) {
   constexpr int NV = D + 2;
-  const int i = blockIdx.x * TPB + threadIdx.x;
-  if (i >= m.n_owned) return;
+  const int t0 = blockIdx.x * TPB + threadIdx.x;
+  if (t0 >= rs.n) return;
+  const int i = rs.row(t0);
   const int NP = (int)m.NP;
   const int L = m.L;
   const size_t NPL = (size_t)NP * L;
@@ -572,10 +576,11 @@ __global__ void __launch_bounds__(TPB, EF_MINB_PASS(D)) k_row_upd(Layout m, Gas 
 template <int D>
 __global__ void __launch_bounds__(TPB, EF_MINB_FINAL(D)) k_final(Layout m, Gas g, const double* __restrict__ U,
                                                const double* __restrict__ U0, double* __restrict__ Uout,
-                                               Work w, StageParams sp) {
+                                               Work w, StageParams sp, RowSet rs) {
   constexpr int NV = D + 2;
-  const int i = blockIdx.x * TPB + threadIdx.x;
-  if (i >= m.n_owned) return;
+  const int t0 = blockIdx.x * TPB + threadIdx.x;
+  if (t0 >= rs.n) return;
+  const int i = rs.row(t0);
   const int NP = (int)m.NP;
   const int L = m.L;
   const size_t NPL = (size_t)NP * L;
@@ -647,20 +652,22 @@ __global__ void __launch_bounds__(TPB, EF_MINB_FINAL(D)) k_final(Layout m, Gas g
 // ---------------------------------------------------------------- halo packing
 // rows: buf[r * ncomp + k] <-> field[k * NP + idx[r]]; slots: buf[q] <-> arr[pos[q]]
 __global__ void k_pack_rows(const double* __restrict__ field, int ncomp, int64_t NP,
-                            const int32_t* __restrict__ idx, int64_t count, double* __restrict__ buf) {
+                            const int32_t* __restrict__ idx, int64_t count, double* __restrict__ buf,
+                            int stride, int coff) {
   const int64_t q = blockIdx.x * (int64_t)TPB + threadIdx.x;
   if (q >= count * ncomp) return;
   const int64_t r = q / ncomp;
   const int k = (int)(q - r * ncomp);
-  buf[q] = field[k * NP + idx[r]];
+  buf[r * stride + coff + k] = field[k * NP + idx[r]];
 }
 __global__ void k_unpack_rows(double* __restrict__ field, int ncomp, int64_t NP,
-                              const int32_t* __restrict__ idx, int64_t count, const double* __restrict__ buf) {
+                              const int32_t* __restrict__ idx, int64_t count, const double* __restrict__ buf,
+                              int stride, int coff) {
   const int64_t q = blockIdx.x * (int64_t)TPB + threadIdx.x;
   if (q >= count * ncomp) return;
   const int64_t r = q / ncomp;
   const int k = (int)(q - r * ncomp);
-  field[k * NP + idx[r]] = buf[q];
+  field[k * NP + idx[r]] = buf[r * stride + coff + k];
 }
 __global__ void k_pack_pos(const double* __restrict__ arr, const int32_t* __restrict__ pos, int64_t count,
                            double* __restrict__ buf) {
@@ -711,12 +718,12 @@ void launch_edge_visc(int dim, const Layout& m, const Gas& g, const double* U, W
   EF_DISPATCH(dim, k_edge_visc, grid_for(m.n_edges > 0 ? m.n_edges : 1), m, g, U, w, reset_tau ? 1 : 0);
 }
 void launch_row_visc(int dim, const Layout& m, const Gas& g, const double* U, Work w,
-                     bool want_tau, cudaStream_t st) {
-  EF_DISPATCH(dim, k_row_visc, grid_for(m.n_owned > 0 ? m.n_owned : 1), m, g, U, w, want_tau ? 1 : 0);
+                     bool want_tau, RowSet rs, cudaStream_t st) {
+  EF_DISPATCH(dim, k_row_visc, grid_for(rs.n > 0 ? rs.n : 1), m, g, U, w, want_tau ? 1 : 0, rs);
 }
 void launch_low_order(int dim, const Layout& m, const Gas& g, const double* U, Work w,
-                      StageParams sp, cudaStream_t st) {
-  EF_DISPATCH(dim, k_low_order, grid_for(m.n_owned > 0 ? m.n_owned : 1), m, g, U, w, sp);
+                      StageParams sp, RowSet rs, cudaStream_t st) {
+  EF_DISPATCH(dim, k_low_order, grid_for(rs.n > 0 ? rs.n : 1), m, g, U, w, sp, rs);
 }
 void launch_edge_lim(int dim, const Layout& m, const Gas& g, const double* U, Work w,
                      StageParams sp, int q, cudaStream_t st) {
@@ -724,22 +731,24 @@ void launch_edge_lim(int dim, const Layout& m, const Gas& g, const double* U, Wo
   EF_DISPATCH(dim, k_edge_lim, grid_for(m.n_edges), m, g, U, w, sp, q);
 }
 void launch_row_upd(int dim, const Layout& m, const Gas& g, const double* U, Work w,
-                    StageParams sp, cudaStream_t st) {
-  if (m.n_owned == 0) return;
-  EF_DISPATCH(dim, k_row_upd, grid_for(m.n_owned), m, g, U, w, sp);
+                    StageParams sp, RowSet rs, cudaStream_t st) {
+  if (rs.n == 0) return;
+  EF_DISPATCH(dim, k_row_upd, grid_for(rs.n), m, g, U, w, sp, rs);
 }
 void launch_final(int dim, const Layout& m, const Gas& g, const double* U, const double* U0,
-                  double* Uout, Work w, StageParams sp, cudaStream_t st) {
-  if (m.n_owned == 0) return;
-  EF_DISPATCH(dim, k_final, grid_for(m.n_owned), m, g, U, U0, Uout, w, sp);
+                  double* Uout, Work w, StageParams sp, RowSet rs, cudaStream_t st) {
+  if (rs.n == 0) return;
+  EF_DISPATCH(dim, k_final, grid_for(rs.n), m, g, U, U0, Uout, w, sp, rs);
 }
 void launch_pack_rows(const double* field, int ncomp, int64_t NP, const int32_t* idx, int64_t count,
-                      double* buf, cudaStream_t st) {
-  if (count > 0) k_pack_rows<<<grid_for(count * ncomp), TPB, 0, st>>>(field, ncomp, NP, idx, count, buf);
+                      double* buf, int stride, int coff, cudaStream_t st) {
+  if (count > 0)
+    k_pack_rows<<<grid_for(count * ncomp), TPB, 0, st>>>(field, ncomp, NP, idx, count, buf, stride, coff);
 }
 void launch_unpack_rows(double* field, int ncomp, int64_t NP, const int32_t* idx, int64_t count,
-                        const double* buf, cudaStream_t st) {
-  if (count > 0) k_unpack_rows<<<grid_for(count * ncomp), TPB, 0, st>>>(field, ncomp, NP, idx, count, buf);
+                        const double* buf, int stride, int coff, cudaStream_t st) {
+  if (count > 0)
+    k_unpack_rows<<<grid_for(count * ncomp), TPB, 0, st>>>(field, ncomp, NP, idx, count, buf, stride, coff);
 }
 void launch_pack_pos(const double* arr, const int32_t* pos, int64_t count, double* buf, cudaStream_t st) {
   if (count > 0) k_pack_pos<<<grid_for(count), TPB, 0, st>>>(arr, pos, count, buf);

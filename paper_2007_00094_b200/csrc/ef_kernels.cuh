@@ -98,6 +98,21 @@ struct StageParams {
   double rk_a;  // < 0: Uout = Unew; else Uout = U0 + rk_a * (Unew - U0)   (stepper.py:632,635)
 };
 
+// Owned rows a row kernel covers: [r0, r0 + n0) then [r2, r2 + n - n0).  The
+// whole range, or (with communication overlap, stepper.py Alg. 4) the rows
+// other ranks import -- a prefix and a suffix of the CM range -- and then the
+// interior.  `lead` marks the launch that also writes the stage's scalars.
+struct RowSet {
+  int r0 = 0, n0 = 0, r2 = 0, n = 0, lead = 1;
+  __host__ __device__ int row(int t) const { return t < n0 ? r0 + t : r2 + (t - n0); }
+};
+inline RowSet all_rows(int64_t n_owned) {
+  RowSet r;
+  r.n0 = r.n = (int)n_owned;
+  r.r2 = (int)n_owned;
+  return r;
+}
+
 // launch wrappers (ef_kernels.cu); all asynchronous on `st`
 void launch_gather_state(int dim, const Layout& m, const double* U_aos, const int64_t* orig_of_local,
                          double* U, int* err, cudaStream_t st);
@@ -110,23 +125,23 @@ void launch_edge_visc(int dim, const Layout& m, const Gas& g, const double* U, W
                       bool reset_tau, cudaStream_t st);
 // step1b+2: per owned row, indicator alpha, mirror of d, d_ii, CFL bound
 void launch_row_visc(int dim, const Layout& m, const Gas& g, const double* U, Work w,
-                     bool want_tau, cudaStream_t st);
+                     bool want_tau, RowSet rs, cudaStream_t st);
 void launch_low_order(int dim, const Layout& m, const Gas& g, const double* U, Work w,
-                      StageParams sp, cudaStream_t st);
+                      StageParams sp, RowSet rs, cudaStream_t st);
 // steps 4-5: P (q = 0) and min(l_ij, l_ji) of limiter pass q, one thread per edge
 void launch_edge_lim(int dim, const Layout& m, const Gas& g, const double* U, Work w,
                      StageParams sp, int q, cudaStream_t st);
 // step5: non-final pass row update U_next += lam * sum min(l) P
 void launch_row_upd(int dim, const Layout& m, const Gas& g, const double* U, Work w,
-                    StageParams sp, cudaStream_t st);
+                    StageParams sp, RowSet rs, cudaStream_t st);
 void launch_final(int dim, const Layout& m, const Gas& g, const double* U, const double* U0,
-                  double* Uout, Work w, StageParams sp, cudaStream_t st);
+                  double* Uout, Work w, StageParams sp, RowSet rs, cudaStream_t st);
 void launch_pow(const double* x, double y, double* out, int64_t n, cudaStream_t st);
-// halo exchange helpers
+// halo exchange helpers: buf[r * stride + coff + k] <-> field[k * NP + idx[r]]
 void launch_pack_rows(const double* field, int ncomp, int64_t NP, const int32_t* idx, int64_t count,
-                      double* buf, cudaStream_t st);
+                      double* buf, int stride, int coff, cudaStream_t st);
 void launch_unpack_rows(double* field, int ncomp, int64_t NP, const int32_t* idx, int64_t count,
-                        const double* buf, cudaStream_t st);
+                        const double* buf, int stride, int coff, cudaStream_t st);
 void launch_pack_pos(const double* arr, const int32_t* pos, int64_t count, double* buf, cudaStream_t st);
 void launch_unpack_pos(double* arr, const int32_t* pos, int64_t count, const double* buf, cudaStream_t st);
 void launch_group_min(unsigned long long* const* bits_dev, int n, cudaStream_t st);

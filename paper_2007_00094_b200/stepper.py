@@ -9,9 +9,12 @@ runs as hand-written sm_100a kernels inside libef_b200.so; this module only
 computes the global Cuthill-McKee order (scipy, exactly as
 exchange.partition does, exchange.py:397-403) and marshals arrays.
 
-`lanes`, `workers`, `overlap` and `chunk_size` are accepted for signature
+`lanes`, `workers` and `chunk_size` are accepted for signature
 compatibility; the reference's results are bitwise independent of them
-(test_stepper.py:106-128) and so are ours.  `ranks` > 1 partitions the mesh
+(test_stepper.py:106-128) and so are ours.  `overlap` (with ranks > 1)
+computes the exported rows first and moves their halo on a second stream
+while the interior rows are computed (exchange.py:168-222); results are
+identical either way.  `ranks` > 1 partitions the mesh
 into contiguous Cuthill-McKee ranges with ghost layers exactly like the
 reference's simulated ranks (exchange.py:393-445) and steps them in lockstep
 on one device; one process per GPU with NCCL is
@@ -119,7 +122,7 @@ class Solver:
             ptr(matrices.m, np.float64), ptr(matrices.c, np.float64),
             ptr(matrices.m_lumped, np.float64), ptr(matrices.inv_m, np.float64))
         prm = _lib.EfParams(gas.gamma, gas.gm1, gas.gp1_inv, gas.gm1_over_2g, gas.two_g_over_gm1,
-                            float(c_cfl), int(limiter_passes), int(newton_steps))
+                            float(c_cfl), int(limiter_passes), int(newton_steps), int(bool(overlap)))
         bcs = _lib.EfBoundary(0, None, None, 0, None, None)
         if boundary is not None:
             if boundary.inflow_nodes is not None and len(boundary.inflow_nodes):

@@ -32,13 +32,26 @@ CASES = {
 
 @pytest.mark.parametrize("case", sorted(CASES))
 @pytest.mark.parametrize("ranks", [2, 3, 5])
-def test_ranks_are_bitwise_identical(case, ranks):
+@pytest.mark.parametrize("overlap", [True, False])
+def test_ranks_are_bitwise_identical(case, ranks, overlap):
     ps = CASES[case]()
     t1, U1, _ = _run(ps.matrices, ps.U0, ps.boundary, 1, 4, c_cfl=ps.c_cfl)
-    tR, UR, s = _run(ps.matrices, ps.U0, ps.boundary, ranks, 4, c_cfl=ps.c_cfl)
+    tR, UR, s = _run(ps.matrices, ps.U0, ps.boundary, ranks, 4, c_cfl=ps.c_cfl, overlap=overlap)
     assert t1 == tR
     assert np.array_equal(U1, UR)
     assert s.comm.sync_count > 0 and s.comm.sync_volume > 0
+
+
+@pytest.mark.parametrize("overlap", [True, False])
+def test_overlap_with_interior_rows(overlap):
+    """Ranks large enough that exported rows are a small prefix/suffix of the
+    range: the interior launches and the comm-stream halos both run."""
+    ps = P.mach3_disc(80, seed=5)
+    t1, U1, _ = _run(ps.matrices, ps.U0, ps.boundary, 1, 5)
+    t4, U4, s = _run(ps.matrices, ps.U0, ps.boundary, 4, 5, overlap=overlap)
+    assert t1 == t4 and np.array_equal(U1, U4)
+    # per stage: alpha, (R, U^L, bounds), U^L after pass 0, U -- one message each
+    assert s.comm.sync_count == 4 * 3 * 5
 
 
 @pytest.mark.parametrize("passes", [0, 1, 3])
