@@ -230,9 +230,11 @@ def run_ours(args, rank, world, local_rank):
     stage_bytes = 8.0 * stage_doubles_per_nnz(dim, card, passes) * nnz
     stage_s = (ms * 1e-3) / (3 * args.steps)
     traffic = None  # dram read + write bytes per launch from the committed ncu --set full capture
+    prof = {}
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-            traffic = json.load(fh).get(args.config, {}).get(KERNEL_OF_PHASE[dom], {}).get("traffic_bytes")
+            prof = json.load(fh).get(args.config, {}).get(KERNEL_OF_PHASE[dom], {})
+        traffic = prof.get("traffic_bytes")
     except Exception:
         traffic = None
     roofline = {
@@ -240,6 +242,8 @@ def run_ours(args, rank, world, local_rank):
         "traffic": traffic, "kernel": KERNEL_OF_PHASE[dom], "phase": dom,
         "kernel_ms": per_launch[dom] * 1e3, "algorithmic_bytes_per_launch": phase_bytes[dom],
         "peak_kind": peak_kind,
+        # co-limiter from the same ncu capture: the edge kernels are fp64-issue bound
+        "fp64_pipe_active": prof.get("fp64_pipe_active"), "warps_active": prof.get("warps_active"),
         "phase_ms": {k: round(v * 1e3, 4) for k, v in per_launch.items()},
         "stage": {"algorithmic_bytes": stage_bytes, "achieved": stage_bytes / stage_s / 1e9,
                   "frac": stage_bytes / stage_s / 1e9 / peak,

@@ -29,7 +29,10 @@ for r in rows[2:]:
         key = f"{name}#{k}"
         k += 1
     rd, wr = val(r, "dram__bytes_read.sum"), val(r, "dram__bytes_write.sum")
+    pct = lambda name: float(r[hdr.index(name)].replace(",", "")) / 100.0  # noqa: E731
     res[key] = {"dram_read_bytes": rd, "dram_write_bytes": wr, "traffic_bytes": rd + wr,
+                "fp64_pipe_active": pct("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                "warps_active": pct("sm__warps_active.avg.pct_of_peak_sustained_active"),
                 "duration_ns": float(r[hdr.index("gpu__time_duration.sum")].replace(",", ""))
                 * {"us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6}.get(units[hdr.index("gpu__time_duration.sum")], 1.0)}
 path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "ncu_traffic.json")
