@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(TPB, EF_MINB_ROW(D)) k_row_visc(Layout m, Gas 
     }
     const double denom = fabs(A) + wb;
     const double safe = denom > kDenomFloor ? denom : 1.0;
-    const double al = npclip(numer / safe, 0.0, 1.0);
+    const double al = npclip(div0(numer, safe), 0.0, 1.0);
     w.alpha[i] = denom > kDenomFloor ? al : 0.0;
   }
   if (bad) atomicOr(w.err, ERR_PROJECT);
@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(TPB, EF_MINB_LOW(D)) k_low_order(Layout m, Gas
       sumL[k] = sumL[k] + ((dv * dU) - fdc);
       sumR[k] = sumR[k] + ((dH * dU) - fdc);
       if (k == 0) {
-        const double corr = dv != 0.0 ? fdc / (2.0 * dv) : 0.0;
+        const double corr = dv != 0.0 ? div0(fdc, 2.0 * dv) : 0.0;
         ubar = (0.5 * (Ui[0] + Uj[0])) - corr;
       }
     }

@@ -599,6 +599,8 @@ def make_config(name: str, scale: str = "full", gas: GasConstants = AIR) -> Prob
         return sod_box(*((31, 7, 7) if small else (511, 127, 127)), gas=gas)
     if name == "c5":
         return periodic_fourier_box(12 if small else 320, gas=gas)
+    if name == "c3m":  # mid-size Sod box (1.05M nodes) for quick measurements
+        return sod_box(*((31, 7, 7) if small else (255, 63, 63)), gas=gas)
     if name == "c5m":  # mid-size 3D instance for quick measurements
         return periodic_fourier_box(12 if small else 160, gas=gas)
     raise ValueError(f"unknown config {name!r}")
