@@ -43,6 +43,8 @@ CONFIG_NAMES = {
     "c1": "C1 2D isentropic vortex 129x129, CFL 0.5",
     "c2": "C2 2D Mach-3 flow past a disc, ~1.24M Q1 nodes, shuffled ids + RCM",
     "c3": "C3 3D Sod box 512x128x128 (jittered)",
+    "c4": "C4 3D Mach-3 flow past a cylinder, extruded O-grid, ~67M nodes (8 GPUs)",
+    "c4m": "C4-shaped 3D Mach-3 cylinder, extruded O-grid 100x50 (~2.1M nodes)",
     "c5": "C5 3D periodic Fourier box 320^3 (32.8M nodes)",
     "c3m": "C3-shaped 3D Sod box 256x64x64 (jittered, 1.05M nodes)",
     "c5m": "C5-shaped 3D periodic Fourier box 160^3 (4.1M nodes)",

@@ -148,7 +148,7 @@ def _inv_det(J: np.ndarray):
     return np.linalg.inv(J), det
 
 
-def assemble_q1(mesh: Mesh, chunk: int = 1 << 18) -> PrecomputedMatrices:
+def assemble_q1(mesh: Mesh, chunk: int = 1 << 15) -> PrecomputedMatrices:
     """Assemble m_ij, c_ij and the lumped mass on the Q1 stencil graph."""
     d = mesh.dim
     cells = mesh.cells
@@ -160,8 +160,7 @@ def assemble_q1(mesh: Mesh, chunk: int = 1 << 18) -> PrecomputedMatrices:
     w = 0.5**d
     shapes = [_shape(d, xi) for xi in qpts]
 
-    rows_all, cols_all, mv_all, cv_all = [], [], [], []
-    for lo in range(0, len(cells), chunk):
+    def local(lo):  # local matrices of one chunk of cells (numpy releases the GIL)
         cc = cells[lo : lo + chunk]
         X = mesh.points[cc]  # (M, nv, d)
         m_loc = np.zeros((len(cc), nv, nv))
@@ -176,10 +175,20 @@ def assemble_q1(mesh: Mesh, chunk: int = 1 << 18) -> PrecomputedMatrices:
             m_loc += scale[:, None, None] * (N[:, None] * N[None, :])[None]
             c_loc += scale[:, None, None, None] * N[None, :, None, None] * grad[:, None, :, :]
         rc = red[cc]
-        rows_all.append(np.repeat(rc, nv, axis=1).ravel())
-        cols_all.append(np.tile(rc, (1, nv)).ravel())
-        mv_all.append(m_loc.ravel())
-        cv_all.append(c_loc.reshape(-1, d))
+        return (np.repeat(rc, nv, axis=1).ravel(), np.tile(rc, (1, nv)).ravel(), m_loc.ravel(),
+                c_loc.reshape(-1, d))
+
+    from concurrent.futures import ThreadPoolExecutor
+
+    # the same chunks as a sequential loop, evaluated on all host threads: per-cell
+    # values do not depend on the chunking, so the result is identical
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 1) as pool:
+        parts = list(pool.map(local, range(0, len(cells), chunk)))
+    rows_all = [q[0] for q in parts]
+    cols_all = [q[1] for q in parts]
+    mv_all = [q[2] for q in parts]
+    cv_all = [q[3] for q in parts]
+    del parts
     rows = np.concatenate(rows_all)
     cols = np.concatenate(cols_all)
     mv = np.concatenate(mv_all)
@@ -475,6 +484,43 @@ def sod_box(nx: int = 511, ny: int = 127, nz: int = 127, jitter: float = 0.2, se
     return ProblemSetup("c3-sod-box", mat, U0, bc, c_cfl=0.9, steps=steps, mesh=mesh)
 
 
+def extrude(mesh2d: Mesh, nz: int, z_range=(0.0, 1.0)) -> Mesh:
+    """Hex mesh from a 2D quad mesh extruded over nz uniform layers in z; the
+    quad (a, b, c, d) of layer k gives the hex (a, b, c, d) at z_k then at
+    z_{k+1}, the reference corner order of a counterclockwise quad."""
+    if mesh2d.dim != 2:
+        raise ValueError("extrude needs a 2D mesh")
+    n2 = len(mesh2d.points)
+    zs = np.linspace(z_range[0], z_range[1], nz + 1)
+    pts = np.empty(((nz + 1) * n2, 3))
+    pts[:, :2] = np.tile(mesh2d.points, (nz + 1, 1))
+    pts[:, 2] = np.repeat(zs, n2)
+    q = mesh2d.cells
+    k = np.arange(nz, dtype=np.int64)[:, None, None] * n2
+    cells = np.concatenate([q[None] + k, q[None] + k + n2], axis=2).reshape(-1, 8)
+    return Mesh(points=pts, cells=cells.astype(np.int64), dim=3)
+
+
+def mach3_cylinder(ny: int = 255, nz: int = 255, seed: int = 2007, gas: GasConstants = AIR,
+                   steps: int = 50, shuffle: bool = True) -> ProblemSetup:
+    """BASELINE C4: Mach 3 past a cylinder r=0.1 along z at (0.6, 0.5) in
+    [0,4]x[0,1]x[0,1]: the C2 O-grid (`disc_channel_mesh(ny)`) extruded over nz
+    layers.  ny = nz = 255 gives ~67M nodes (8 GPUs); smaller ny/nz give
+    single-GPU and oracle-sized instances.  Inflow x=0 (rho=1.4, u=(3,0,0),
+    p=1), do-nothing x=4, slip on the cylinder and the four side walls."""
+    mesh = extrude(disc_channel_mesh(ny), nz)
+    if shuffle:
+        perm = np.random.default_rng(seed).permutation(len(mesh.points))  # old -> new
+        pts = np.empty_like(mesh.points)
+        pts[perm] = mesh.points
+        mesh = Mesh(points=pts, cells=perm[mesh.cells], dim=3)
+    mat = assemble_q1(mesh)
+    ff = _conserved(np.array([1.4]), np.array([[3.0, 0.0, 0.0]]), np.array([1.0]), gas)[0]
+    bc = _slip_inflow_bc(mesh, lambda X: X[..., 0] < 1e-9, lambda X: X[..., 0] > 4.0 - 1e-9, ff)
+    U0 = np.tile(ff, (mat.n, 1))
+    return ProblemSetup("c4-mach3-cylinder", mat, U0, bc, c_cfl=0.9, steps=steps, mesh=mesh)
+
+
 def periodic_box_matrices(n: int) -> PrecomputedMatrices:
     """Q1 matrices of the uniform periodic n^3 hex mesh of the unit cube, built
     from its translation invariance (every node has the same 27-point stencil
@@ -599,6 +645,10 @@ def make_config(name: str, scale: str = "full", gas: GasConstants = AIR) -> Prob
         return sod_box(*((31, 7, 7) if small else (511, 127, 127)), gas=gas)
     if name == "c5":
         return periodic_fourier_box(12 if small else 320, gas=gas)
+    if name == "c4":  # ~67M nodes: the 8-GPU configuration
+        return mach3_cylinder(*((20, 6) if small else (255, 255)), gas=gas)
+    if name == "c4m":  # single-GPU C4-shaped instance (~2.1M nodes)
+        return mach3_cylinder(*((20, 6) if small else (100, 50)), gas=gas)
     if name == "c3m":  # mid-size Sod box (1.05M nodes) for quick measurements
         return sod_box(*((31, 7, 7) if small else (255, 63, 63)), gas=gas)
     if name == "c5m":  # mid-size 3D instance for quick measurements

@@ -173,6 +173,13 @@ def small_cases():
     U = P.random_state(np.random.default_rng(4096), mat.n, dim=3)
     save_case("periodic3d_random_euler", mat, U, None, base(), 1, "euler")
     save_case("periodic3d_random_rk3", mat, U, None, base(), 2, "rk3")
+    c4_case()
+
+
+def c4_case():
+    """C4-shaped (extruded O-grid around a cylinder), oracle size."""
+    ps = P.mach3_cylinder(10, 3, seed=13)
+    save_case("c4_cylinder", ps.matrices, ps.U0, ps.boundary, base(), 2, "rk3", record_internals=False)
 
 
 def c1_full():
@@ -222,9 +229,12 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--c1-full", action="store_true")
     ap.add_argument("--only-c1-full", action="store_true")
+    ap.add_argument("--only-c4", action="store_true")
     args = ap.parse_args()
     r_physics.set_power_function(O.shared_pow)
-    if not args.only_c1_full:
+    if args.only_c4:
+        c4_case()
+    elif not args.only_c1_full:
         small_cases()
         default_pow_divergence()
     if args.c1_full or args.only_c1_full:

@@ -27,6 +27,7 @@ CASES = {
     "c2": lambda: P.mach3_disc(20, seed=7),
     "c3": lambda: P.sod_box(15, 4, 4, seed=3),
     "c5": lambda: P.periodic_fourier_box(8, seed=2),
+    "c4": lambda: P.mach3_cylinder(10, 3, seed=6),
 }
 
 

@@ -80,6 +80,11 @@ def test_gpu_c3_sod_box():
     _compare(ps.matrices, ps.U0, ps.boundary, 8)
 
 
+def test_gpu_c4_cylinder():
+    ps = P.mach3_cylinder(20, 6, seed=8)
+    _compare(ps.matrices, ps.U0, ps.boundary, 3)
+
+
 def test_gpu_c5_periodic_box():
     ps = P.periodic_fourier_box(12, seed=4)
     _compare(ps.matrices, ps.U0, None, 5)

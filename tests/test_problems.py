@@ -34,6 +34,7 @@ def _check_matrices(mat):
     lambda: P.mach3_disc(20, seed=1).matrices,
     lambda: P.sod_box(7, 3, 3, seed=2).matrices,
     lambda: P.periodic_fourier_box(5).matrices,
+    lambda: P.mach3_cylinder(10, 3, seed=3).matrices,
 ])
 def test_assembly_invariants(maker):
     _check_matrices(maker())
@@ -77,3 +78,16 @@ def test_vortex_initial_state_is_admissible_and_far_field_matches():
     assert (U[:, 0] > 0).all() and (eps > 0).all()
     corner = np.argmax(np.abs(ps.mesh.points).sum(axis=1))
     assert np.allclose(U[corner], ps.boundary.farfield, rtol=1e-6)
+
+
+def test_c4_extruded_cylinder_geometry():
+    """C4: [0,4]x[0,1]^2 minus the cylinder r=0.1 (polygonal O-grid boundary),
+    stencils of 27 points with 33 at the O-grid junctions."""
+    ps = P.mach3_cylinder(20, 4, seed=3)
+    mat = ps.matrices
+    vol = mat.m_lumped.sum()
+    assert abs(vol - (4.0 - np.pi * 0.01)) < 2e-3
+    card = np.diff(mat.indptr)
+    assert np.bincount(card).argmax() == 27 and card.max() <= 33
+    assert len(ps.boundary.inflow_nodes) > 0 and len(ps.boundary.slip_nodes) > 0
+    assert np.allclose(np.linalg.norm(ps.boundary.slip_normals, axis=1), 1.0)
