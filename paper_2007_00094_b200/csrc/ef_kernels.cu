@@ -34,16 +34,33 @@ constexpr int TPB = EF_TPB;
 #ifndef EF_MINB
 #define EF_MINB 8
 #endif
-#define EF_MINB_EDGE(D) 8
-#define EF_MINB_ROW(D) ((D) == 3 ? 5 : EF_MINB)
-#define EF_MINB_LOW(D) ((D) == 3 ? 5 : EF_MINB)
+#ifndef EF_MINB_EDGE2
+#define EF_MINB_EDGE2 8
+#endif
+#ifndef EF_MINB_ROW2
+#define EF_MINB_ROW2 EF_MINB
+#endif
+#ifndef EF_MINB_LOW2
+#define EF_MINB_LOW2 EF_MINB
+#endif
+#define EF_MINB_EDGE(D) ((D) == 3 ? 8 : EF_MINB_EDGE2)
+#define EF_MINB_ROW(D) ((D) == 3 ? 5 : EF_MINB_ROW2)
+#define EF_MINB_LOW(D) ((D) == 3 ? 5 : EF_MINB_LOW2)
 #ifndef EF_MINB_ELIM2
 #define EF_MINB_ELIM2 EF_MINB
 #endif
 #ifndef EF_MINB_ELIM3
 #define EF_MINB_ELIM3 6
 #endif
-#define EF_MINB_ELIM(D) ((D) == 3 ? EF_MINB_ELIM3 : EF_MINB_ELIM2)
+// the first pass (forms P) wants more registers than the rescaling passes
+#ifndef EF_MINB_ELIM2_FIRST
+#define EF_MINB_ELIM2_FIRST 7
+#endif
+#ifndef EF_MINB_ELIM3_FIRST
+#define EF_MINB_ELIM3_FIRST EF_MINB_ELIM3
+#endif
+#define EF_MINB_ELIM(D, FIRST) \
+  ((D) == 3 ? ((FIRST) ? EF_MINB_ELIM3_FIRST : EF_MINB_ELIM3) : ((FIRST) ? EF_MINB_ELIM2_FIRST : EF_MINB_ELIM2))
 #ifndef EF_MINB_UPD
 #define EF_MINB_UPD 10
 #endif
@@ -481,9 +498,10 @@ __global__ void __launch_bounds__(TPB, EF_MINB_LOW(D)) k_low_order(Layout m, Gas
 // kernels then only stream their own slots.  Every operation is the
 // reference's, in its order; each side uses its own m_ij / m_ji, alpha sum and
 // factor, so nothing assumes symmetry that the inputs might not have.
-template <int D>
-__global__ void __launch_bounds__(TPB, EF_MINB_ELIM(D)) k_edge_lim(Layout m, Gas g, const double* __restrict__ U,
-                                                                 Work w, StageParams sp, int q) {
+template <int D, bool FIRST>
+__global__ void __launch_bounds__(TPB, EF_MINB_ELIM(D, FIRST)) k_edge_lim(Layout m, Gas g,
+                                                                        const double* __restrict__ U,
+                                                                        Work w, StageParams sp, int q) {
   constexpr int NV = D + 2;
   const int e = blockIdx.x * TPB + threadIdx.x;
   if (e >= m.n_edges) return;
@@ -494,7 +512,7 @@ __global__ void __launch_bounds__(TPB, EF_MINB_ELIM(D)) k_edge_lim(Layout m, Gas
   const int NP = (int)m.NP;
   const size_t NPL = (size_t)NP * m.L;
   double Pi[NV], Pj[NV];
-  if (q == 0) {
+  if (FIRST) {  // q == 0
     const double tau = *w.tau;
     const double imi = m.inv_m[i], imj = m.inv_m[j];
     const double fi = (tau * imi) * (double)(m.cardf[i] - 1);  // stepper.py:467 (full card)
@@ -526,7 +544,7 @@ __global__ void __launch_bounds__(TPB, EF_MINB_ELIM(D)) k_edge_lim(Layout m, Gas
   // forms the same product P_(q-1) (1 - min l) itself, which saves the largest
   // write of the stage.  Every other pass stores its P_q.
   const bool last = q == sp.passes - 1;
-  if (q == 0 || !last) {
+  if (FIRST || !last) {
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
       w.P[(size_t)k * NPL + p] = Pi[k];
@@ -728,7 +746,14 @@ void launch_low_order(int dim, const Layout& m, const Gas& g, const double* U, W
 void launch_edge_lim(int dim, const Layout& m, const Gas& g, const double* U, Work w,
                      StageParams sp, int q, cudaStream_t st) {
   if (m.n_edges == 0) return;
-  EF_DISPATCH(dim, k_edge_lim, grid_for(m.n_edges), m, g, U, w, sp, q);
+  const unsigned grid = grid_for(m.n_edges);
+  if (dim == 2) {
+    if (q == 0) k_edge_lim<2, true><<<grid, TPB, 0, st>>>(m, g, U, w, sp, q);
+    else k_edge_lim<2, false><<<grid, TPB, 0, st>>>(m, g, U, w, sp, q);
+  } else {
+    if (q == 0) k_edge_lim<3, true><<<grid, TPB, 0, st>>>(m, g, U, w, sp, q);
+    else k_edge_lim<3, false><<<grid, TPB, 0, st>>>(m, g, U, w, sp, q);
+  }
 }
 void launch_row_upd(int dim, const Layout& m, const Gas& g, const double* U, Work w,
                     StageParams sp, RowSet rs, cudaStream_t st) {
