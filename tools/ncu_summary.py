@@ -11,6 +11,8 @@ def g(r, name):
 for r in rows[2:]:
     k = r[hdr.index('Kernel Name')][:28]
     dur = g(r, 'gpu__time_duration.sum')
+    dunit = rows[1][hdr.index('gpu__time_duration.sum')]
+    dur *= {'ms': 1e3, 'msecond': 1e3, 'ns': 1e-3, 'nsecond': 1e-3}.get(dunit, 1.0)  # -> us
     fp = g(r, 'sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active')
     dr = g(r, 'dram__bytes_read.sum'); dw = g(r, 'dram__bytes_write.sum')
     occ = g(r, 'sm__warps_active.avg.pct_of_peak_sustained_active')
