@@ -43,9 +43,18 @@ constexpr int TPB = EF_TPB;
 #ifndef EF_MINB_LOW2
 #define EF_MINB_LOW2 EF_MINB
 #endif
-#define EF_MINB_EDGE(D) ((D) == 3 ? 8 : EF_MINB_EDGE2)
-#define EF_MINB_ROW(D) ((D) == 3 ? 5 : EF_MINB_ROW2)
-#define EF_MINB_LOW(D) ((D) == 3 ? 5 : EF_MINB_LOW2)
+#ifndef EF_MINB_EDGE3
+#define EF_MINB_EDGE3 8
+#endif
+#define EF_MINB_EDGE(D) ((D) == 3 ? EF_MINB_EDGE3 : EF_MINB_EDGE2)
+#ifndef EF_MINB_ROW3
+#define EF_MINB_ROW3 5
+#endif
+#ifndef EF_MINB_LOW3
+#define EF_MINB_LOW3 4
+#endif
+#define EF_MINB_ROW(D) ((D) == 3 ? EF_MINB_ROW3 : EF_MINB_ROW2)
+#define EF_MINB_LOW(D) ((D) == 3 ? EF_MINB_LOW3 : EF_MINB_LOW2)
 #ifndef EF_MINB_ELIM2
 #define EF_MINB_ELIM2 EF_MINB
 #endif
