@@ -41,7 +41,7 @@ constexpr int TPB = EF_TPB;
 #define EF_MINB_ROW2 EF_MINB
 #endif
 #ifndef EF_MINB_LOW2
-#define EF_MINB_LOW2 EF_MINB
+#define EF_MINB_LOW2 5
 #endif
 #ifndef EF_MINB_EDGE3
 #define EF_MINB_EDGE3 8
@@ -212,8 +212,7 @@ __device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1
 // Row loop over the real slots s != diag in ascending order with a two-stage
 // prefetch: slot s+1's fields are issued (issue(s, j, stage)) before slot s is
 // consumed (body(s, stage)); the column of slot s+2 is loaded one iteration
-// ahead so the issue never waits on it.  Measured on the 27-point stencil:
-// k_low_order -30%; in 2D (9 points, 69% L2 hits) it does not pay.
+// ahead so the issue never waits on it.
 template <class Issue, class Body>
 __device__ __forceinline__ void row_pipe(const int* __restrict__ col, int base, int card, int dg, Issue issue,
                                          Body body) {
@@ -235,11 +234,13 @@ __device__ __forceinline__ void row_pipe(const int* __restrict__ col, int base, 
     jB = jC;
   }
 }
-#ifndef EF_PIPE_2D
-#define EF_PIPE_2D 0
+// k_low_order: the prefetch pays once the kernel may keep more registers
+// (2D 5 blocks/SM: -21%; 3D 4 blocks/SM: -23%); k_row_visc: -3% in 2D.
+#ifndef EF_PIPE_LOW
+#define EF_PIPE_LOW 1
 #endif
-#define EF_PIPE(D) ((D) == 3 || EF_PIPE_2D)
-#define EF_PIPE_ROW(D) true  // k_row_visc: pays in 2D too (-3%)
+#define EF_PIPE(D) (EF_PIPE_LOW != 0)
+#define EF_PIPE_ROW(D) true
 
 template <int D>
 __global__ void __launch_bounds__(TPB, EF_MINB_ROW(D)) k_row_visc(Layout m, Gas g, const double* __restrict__ U,
