@@ -27,7 +27,18 @@ namespace ef {
 #ifndef EF_TPB
 #define EF_TPB 128
 #endif
-constexpr int TPB = EF_TPB;
+constexpr int TPB = EF_TPB;  // state I/O, halo and pow kernels
+// Stage kernels: 64-thread blocks in 2D (a shorter last wave: +1%), 128 in 3D
+// (64 measured -1%).  The register caps below count resident 128-thread
+// blocks per SM; EF_LB rescales them to the kernel's block size.
+#ifndef EF_TPB2
+#define EF_TPB2 64
+#endif
+#ifndef EF_TPB3
+#define EF_TPB3 128
+#endif
+#define EF_TPB_D(D) ((D) == 3 ? EF_TPB3 : EF_TPB2)
+#define EF_LB(n, D) ((n) * 128 / EF_TPB_D(D))
 // Resident blocks per SM requested from ptxas (i.e. the register cap) per
 // kernel and dimension, measured on B200 (C2 2D, 160^3 periodic 3D): these
 // kernels are latency-bound, so occupancy usually beats spill-free code.
@@ -159,10 +170,10 @@ __global__ void k_nodal(Layout m, Gas g, const double* __restrict__ U, Work w, i
 // positions in ascending order, so a warp reads 32 consecutive positions of
 // one slot row (coalesced) and the row / slot are recovered from the position.
 template <int D>
-__global__ void __launch_bounds__(TPB, EF_MINB_EDGE(D)) k_edge_visc(Layout m, Gas g, const double* __restrict__ U,
+__global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_EDGE(D), D)) k_edge_visc(Layout m, Gas g, const double* __restrict__ U,
                                                    Work w, int reset_tau) {
   constexpr int NV = D + 2;
-  const int e = blockIdx.x * TPB + threadIdx.x;
+  const int e = blockIdx.x * EF_TPB_D(D) + threadIdx.x;
   if (reset_tau && e == 0) *w.tau_min_bits = 0x7ff0000000000000ULL;
   if (e >= m.n_edges) return;
   const int p = m.edges[e];
@@ -243,10 +254,10 @@ __device__ __forceinline__ void row_pipe(const int* __restrict__ col, int base, 
 #define EF_PIPE_ROW(D) true
 
 template <int D>
-__global__ void __launch_bounds__(TPB, EF_MINB_ROW(D)) k_row_visc(Layout m, Gas g, const double* __restrict__ U,
+__global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ROW(D), D)) k_row_visc(Layout m, Gas g, const double* __restrict__ U,
                                                   Work w, int want_tau, RowSet rs) {
   constexpr int NV = D + 2;
-  const int t0 = blockIdx.x * TPB + threadIdx.x;
+  const int t0 = blockIdx.x * EF_TPB_D(D) + threadIdx.x;
   const bool act = t0 < rs.n;
   const int i = act ? rs.row(t0) : 0;
   double cand = __longlong_as_double(0x7ff0000000000000LL);
@@ -283,7 +294,7 @@ __global__ void __launch_bounds__(TPB, EF_MINB_ROW(D)) k_row_visc(Layout m, Gas 
     };
     if constexpr (EF_PIPE_ROW(D)) {
       constexpr int F = NV + 1 + D;  // U_j, eor_j, c
-      __shared__ double buf[2][F][TPB];
+      __shared__ double buf[2][F][EF_TPB_D(D)];
       const int t = threadIdx.x;
       auto issue = [&](int s, int j, int st) {
         const int p = base + s * 32;
@@ -369,14 +380,14 @@ __global__ void __launch_bounds__(TPB, EF_MINB_ROW(D)) k_row_visc(Layout m, Gas 
   }
   if (bad) atomicOr(w.err, ERR_PROJECT);
   if (!want_tau) return;
-  __shared__ double red[TPB / 32];
+  __shared__ double red[EF_TPB_D(D) / 32];
   cand = warp_min(cand);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cand;
   __syncthreads();
   if (threadIdx.x == 0) {
     double b = red[0];
 #pragma unroll
-    for (int q = 1; q < TPB / 32; ++q) b = fmin(b, red[q]);
+    for (int q = 1; q < EF_TPB_D(D) / 32; ++q) b = fmin(b, red[q]);
     // tau > 0: the IEEE bit pattern orders like the value
     atomicMin(w.tau_min_bits, (unsigned long long)__double_as_longlong(b));
   }
@@ -399,11 +410,11 @@ __device__ __forceinline__ double stage_tau(const Work& w, const StageParams& sp
 
 
 template <int D>
-__global__ void __launch_bounds__(TPB, EF_MINB_LOW(D)) k_low_order(Layout m, Gas g, const double* __restrict__ U,
+__global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_LOW(D), D)) k_low_order(Layout m, Gas g, const double* __restrict__ U,
                                                    Work w, StageParams sp, RowSet rs) {
   constexpr int NV = D + 2;
   const double tau = stage_tau(w, sp);
-  const int t0 = blockIdx.x * TPB + threadIdx.x;
+  const int t0 = blockIdx.x * EF_TPB_D(D) + threadIdx.x;
   if (t0 == 0 && rs.lead && sp.tau_mode != TAU_DEVICE) {
     *w.tau = tau;
     if (sp.tau_mode == TAU_CFL &&
@@ -453,7 +464,7 @@ __global__ void __launch_bounds__(TPB, EF_MINB_LOW(D)) k_low_order(Layout m, Gas
   if constexpr (EF_PIPE(D)) {
     // fields per slot: U_j (NV), alpha_j, phi_j, c (D), d
     constexpr int F = NV + 2 + D + 1;
-    __shared__ double buf[2][F][TPB];
+    __shared__ double buf[2][F][EF_TPB_D(D)];
     const int t = threadIdx.x;
     auto issue = [&](int s, int j, int st) {
       const int p = base + s * 32;
@@ -509,11 +520,11 @@ __global__ void __launch_bounds__(TPB, EF_MINB_LOW(D)) k_low_order(Layout m, Gas
 // reference's, in its order; each side uses its own m_ij / m_ji, alpha sum and
 // factor, so nothing assumes symmetry that the inputs might not have.
 template <int D, bool FIRST>
-__global__ void __launch_bounds__(TPB, EF_MINB_ELIM(D, FIRST)) k_edge_lim(Layout m, Gas g,
+__global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ELIM(D, FIRST), D)) k_edge_lim(Layout m, Gas g,
                                                                         const double* __restrict__ U,
                                                                         Work w, StageParams sp, int q) {
   constexpr int NV = D + 2;
-  const int e = blockIdx.x * TPB + threadIdx.x;
+  const int e = blockIdx.x * EF_TPB_D(D) + threadIdx.x;
   if (e >= m.n_edges) return;
   const int p = m.edges[e];
   const int i = (int)fdiv((uint32_t)p, m.slab) * 32 + (p & 31);
@@ -574,10 +585,10 @@ __global__ void __launch_bounds__(TPB, EF_MINB_ELIM(D, FIRST)) k_edge_lim(Layout
 // step5 (non-final pass): U_next_i += lam_i * sum_s min(l) P in slot order
 // (stepper.py:478-481); the rescale of P belongs to the next k_edge_lim.
 template <int D>
-__global__ void __launch_bounds__(TPB, EF_MINB_PASS(D)) k_row_upd(Layout m, Gas g, const double* __restrict__ U,
+__global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_PASS(D), D)) k_row_upd(Layout m, Gas g, const double* __restrict__ U,
                                                                 Work w, StageParams sp, RowSet rs) {
   constexpr int NV = D + 2;
-  const int t0 = blockIdx.x * TPB + threadIdx.x;
+  const int t0 = blockIdx.x * EF_TPB_D(D) + threadIdx.x;
   if (t0 >= rs.n) return;
   const int i = rs.row(t0);
   const int NP = (int)m.NP;
@@ -602,11 +613,11 @@ __global__ void __launch_bounds__(TPB, EF_MINB_PASS(D)) k_row_upd(Layout m, Gas 
 }
 
 template <int D>
-__global__ void __launch_bounds__(TPB, EF_MINB_FINAL(D)) k_final(Layout m, Gas g, const double* __restrict__ U,
+__global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_FINAL(D), D)) k_final(Layout m, Gas g, const double* __restrict__ U,
                                                const double* __restrict__ U0, double* __restrict__ Uout,
                                                Work w, StageParams sp, RowSet rs) {
   constexpr int NV = D + 2;
-  const int t0 = blockIdx.x * TPB + threadIdx.x;
+  const int t0 = blockIdx.x * EF_TPB_D(D) + threadIdx.x;
   if (t0 >= rs.n) return;
   const int i = rs.row(t0);
   const int NP = (int)m.NP;
@@ -725,6 +736,16 @@ __global__ void k_pow(const double* __restrict__ x, double y, double* __restrict
     if ((dim) == 2) KERNEL<2><<<(GRID), TPB, 0, st>>>(__VA_ARGS__);          \
     else KERNEL<3><<<(GRID), TPB, 0, st>>>(__VA_ARGS__);                     \
   } while (0)
+// stage kernels: grid for n items with the dimension's block size
+static inline unsigned grid_d(int dim, int64_t n) {
+  const int b = dim == 3 ? EF_TPB3 : EF_TPB2;
+  return (unsigned)((n + b - 1) / b);
+}
+#define EF_DISPATCH_STAGE(dim, KERNEL, N, ...)                                                      \
+  do {                                                                                              \
+    if ((dim) == 2) KERNEL<2><<<grid_d(2, (N)), EF_TPB2, 0, st>>>(__VA_ARGS__);                     \
+    else KERNEL<3><<<grid_d(3, (N)), EF_TPB3, 0, st>>>(__VA_ARGS__);                                \
+  } while (0)
 
 void launch_gather_state(int dim, const Layout& m, const double* U_aos, const int64_t* orig,
                          double* U, int* err, cudaStream_t st) {
@@ -743,37 +764,38 @@ void launch_nodal(int dim, const Layout& m, const Gas& g, const double* U, Work 
 }
 void launch_edge_visc(int dim, const Layout& m, const Gas& g, const double* U, Work w,
                       bool reset_tau, cudaStream_t st) {
-  EF_DISPATCH(dim, k_edge_visc, grid_for(m.n_edges > 0 ? m.n_edges : 1), m, g, U, w, reset_tau ? 1 : 0);
+  EF_DISPATCH_STAGE(dim, k_edge_visc, m.n_edges > 0 ? m.n_edges : 1, m, g, U, w, reset_tau ? 1 : 0);
 }
 void launch_row_visc(int dim, const Layout& m, const Gas& g, const double* U, Work w,
                      bool want_tau, RowSet rs, cudaStream_t st) {
-  EF_DISPATCH(dim, k_row_visc, grid_for(rs.n > 0 ? rs.n : 1), m, g, U, w, want_tau ? 1 : 0, rs);
+  EF_DISPATCH_STAGE(dim, k_row_visc, rs.n > 0 ? rs.n : 1, m, g, U, w, want_tau ? 1 : 0, rs);
 }
 void launch_low_order(int dim, const Layout& m, const Gas& g, const double* U, Work w,
                       StageParams sp, RowSet rs, cudaStream_t st) {
-  EF_DISPATCH(dim, k_low_order, grid_for(rs.n > 0 ? rs.n : 1), m, g, U, w, sp, rs);
+  EF_DISPATCH_STAGE(dim, k_low_order, rs.n > 0 ? rs.n : 1, m, g, U, w, sp, rs);
 }
 void launch_edge_lim(int dim, const Layout& m, const Gas& g, const double* U, Work w,
                      StageParams sp, int q, cudaStream_t st) {
   if (m.n_edges == 0) return;
-  const unsigned grid = grid_for(m.n_edges);
   if (dim == 2) {
-    if (q == 0) k_edge_lim<2, true><<<grid, TPB, 0, st>>>(m, g, U, w, sp, q);
-    else k_edge_lim<2, false><<<grid, TPB, 0, st>>>(m, g, U, w, sp, q);
+    const unsigned grid = grid_d(2, m.n_edges);
+    if (q == 0) k_edge_lim<2, true><<<grid, EF_TPB2, 0, st>>>(m, g, U, w, sp, q);
+    else k_edge_lim<2, false><<<grid, EF_TPB2, 0, st>>>(m, g, U, w, sp, q);
   } else {
-    if (q == 0) k_edge_lim<3, true><<<grid, TPB, 0, st>>>(m, g, U, w, sp, q);
-    else k_edge_lim<3, false><<<grid, TPB, 0, st>>>(m, g, U, w, sp, q);
+    const unsigned grid = grid_d(3, m.n_edges);
+    if (q == 0) k_edge_lim<3, true><<<grid, EF_TPB3, 0, st>>>(m, g, U, w, sp, q);
+    else k_edge_lim<3, false><<<grid, EF_TPB3, 0, st>>>(m, g, U, w, sp, q);
   }
 }
 void launch_row_upd(int dim, const Layout& m, const Gas& g, const double* U, Work w,
                     StageParams sp, RowSet rs, cudaStream_t st) {
   if (rs.n == 0) return;
-  EF_DISPATCH(dim, k_row_upd, grid_for(rs.n), m, g, U, w, sp, rs);
+  EF_DISPATCH_STAGE(dim, k_row_upd, rs.n, m, g, U, w, sp, rs);
 }
 void launch_final(int dim, const Layout& m, const Gas& g, const double* U, const double* U0,
                   double* Uout, Work w, StageParams sp, RowSet rs, cudaStream_t st) {
   if (rs.n == 0) return;
-  EF_DISPATCH(dim, k_final, grid_for(rs.n), m, g, U, U0, Uout, w, sp, rs);
+  EF_DISPATCH_STAGE(dim, k_final, rs.n, m, g, U, U0, Uout, w, sp, rs);
 }
 void launch_pack_rows(const double* field, int ncomp, int64_t NP, const int32_t* idx, int64_t count,
                       double* buf, int stride, int coff, cudaStream_t st) {
