@@ -504,6 +504,8 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
   Work& w = h->w;
   EF_TRY(h->alloc(&w.eor, NP));
   EF_TRY(h->alloc(&w.phi, NP));
+  EF_TRY(h->alloc(&w.vp, (size_t)(D + 1) * NP));
+  EF_CUDA(cudaMemset(w.vp, 0, sizeof(double) * (D + 1) * NP));
   EF_TRY(h->alloc(&w.alpha, NP));
   EF_TRY(h->alloc(&w.R, (size_t)NV * NP));
   EF_TRY(h->alloc(&w.Unext, (size_t)NV * NP));

@@ -143,13 +143,18 @@ __global__ void k_scatter_state(Layout m, const double* __restrict__ U,
 }
 
 // ---------------------------------------------------------------- step0
+// step0 (stepper.py:399-405) of node i: eta/rho, phi, and the flux inputs
+// v = m / rho, p = gm1 * eps that the row kernels reuse for every stencil slot
 template <int D>
-__device__ __forceinline__ void nodal_one(const double* Ui, const Gas& g, double& eor, double& phi) {
+__device__ __forceinline__ void nodal_one(const double* Ui, const Gas& g, Work& w, int NP, int i) {
   const double rho = Ui[0];
-  const Recip rr = recip(rho);  // shared by the two divisions by rho
+  const Recip rr = recip(rho);  // shared by the divisions by rho
   const double eps = internal_energy<D>(Ui, rr);
-  eor = qdiv(dpow(rho * eps, g.gp1_inv), rr);  // stepper.py:403
-  phi = eps * dpow(rho, g.neg_gamma);          // stepper.py:404
+  w.eor[i] = qdiv(dpow(rho * eps, g.gp1_inv), rr);  // stepper.py:403
+  w.phi[i] = eps * dpow(rho, g.neg_gamma);          // stepper.py:404
+#pragma unroll
+  for (int a = 0; a < D; ++a) w.vp[a * NP + i] = qdiv(Ui[1 + a], rr);  // physics.py:157
+  w.vp[D * NP + i] = g.gm1 * eps;                                        // physics.py:94
 }
 
 template <int D>
@@ -158,10 +163,7 @@ __global__ void k_nodal(Layout m, Gas g, const double* __restrict__ U, Work w, i
   if (i >= hi) return;
   double Ui[D + 2];
   load_node<D + 2>(U, m.NP, i, Ui);
-  double e, p;
-  nodal_one<D>(Ui, g, e, p);
-  w.eor[i] = e;
-  w.phi[i] = p;
+  nodal_one<D>(Ui, g, w, (int)m.NP, (int)i);
 }
 
 // ---------------------------------------------------------------- step1a
@@ -252,6 +254,25 @@ __device__ __forceinline__ void row_pipe(const int* __restrict__ col, int base, 
 #endif
 #define EF_PIPE(D) (EF_PIPE_LOW != 0)
 #define EF_PIPE_ROW(D) true
+// the row kernels form neighbour fluxes from v, p cached by step0 (measured:
+// 2D k_row_visc -5%, k_low_order -10%, 3D k_low_order -19%; 3D k_row_visc
+// +4%, so it keeps computing them)
+#ifndef EF_VP
+#define EF_VP 1
+#endif
+#define EF_VP_ROW(D) (EF_VP && (D) == 2)
+#define EF_VP_LOW(D) (EF_VP != 0)
+template <int D, bool USE>
+__device__ __forceinline__ void node_flux(const double* Ui, const Work& w, int NP, int i, const Gas& g,
+                                          double (*f)[D]) {
+  if (USE) {
+    double vp[D + 1];
+    load_node<D + 1>(w.vp, NP, i, vp);
+    flux_vp<D>(Ui, vp, vp[D], f);
+  } else {
+    flux<D>(Ui, g, f);
+  }
+}
 
 template <int D>
 __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ROW(D), D)) k_row_visc(Layout m, Gas g, const double* __restrict__ U,
@@ -271,19 +292,20 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ROW(D), D)) k_row_v
     double Ui[NV];
     load_node<NV>(U, NP, i, Ui);
     double fi[NV][D];
-    flux<D>(Ui, g, fi);
+    node_flux<D, EF_VP_ROW(D)>(Ui, w, NP, i, g, fi);
     const double eor_i = w.eor[i];
     double A = 0.0, B[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) B[k] = 0.0;
     // one slot j != i (j == i contributes exact zeros), in slot order
-    auto slot = [&](const double* Uj, const double* cc, double eor_j) {
+    auto slot = [&](const double* Uj, const double* cc, double eor_j, const double* vpj) {
       double mc = 0.0;
 #pragma unroll
       for (int a = 0; a < D; ++a) mc = mc + Uj[1 + a] * cc[a];
       A = A + (eor_j - eor_i) * mc;
       double fj[NV][D];
-      flux<D>(Uj, g, fj);
+      if (EF_VP_ROW(D)) flux_vp<D>(Uj, vpj, vpj[D], fj);
+      else flux<D>(Uj, g, fj);
 #pragma unroll
       for (int k = 0; k < NV; ++k) {
         double t = 0.0;
@@ -293,7 +315,8 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ROW(D), D)) k_row_v
       }
     };
     if constexpr (EF_PIPE_ROW(D)) {
-      constexpr int F = NV + 1 + D;  // U_j, eor_j, c
+      constexpr int NQ = EF_VP_ROW(D) ? D + 1 : 0;  // v_j, p_j
+      constexpr int F = NV + 1 + D + NQ;     // U_j, eor_j, c, (v_j, p_j)
       __shared__ double buf[2][F][EF_TPB_D(D)];
       const int t = threadIdx.x;
       auto issue = [&](int s, int j, int st) {
@@ -303,14 +326,18 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ROW(D), D)) k_row_v
         cp_async8(&buf[st][NV][t], w.eor + j);
 #pragma unroll
         for (int a = 0; a < D; ++a) cp_async8(&buf[st][NV + 1 + a][t], m.c + (size_t)a * NPL + p);
+#pragma unroll
+        for (int a = 0; a < NQ; ++a) cp_async8(&buf[st][NV + 1 + D + a][t], w.vp + a * NP + j);
       };
       auto body = [&](int, int st) {
-        double Uj[NV], cc[D];
+        double Uj[NV], cc[D], vpj[D + 1];
 #pragma unroll
         for (int k = 0; k < NV; ++k) Uj[k] = buf[st][k][t];
 #pragma unroll
         for (int a = 0; a < D; ++a) cc[a] = buf[st][NV + 1 + a][t];
-        slot(Uj, cc, buf[st][NV][t]);
+#pragma unroll
+        for (int a = 0; a < NQ; ++a) vpj[a] = buf[st][NV + 1 + D + a][t];
+        slot(Uj, cc, buf[st][NV][t], vpj);
       };
       row_pipe(m.col, base, card, dg, issue, body);
     } else {
@@ -319,11 +346,12 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ROW(D), D)) k_row_v
         if (s == dg) continue;
         const int p = base + s * 32;
         const int j = m.col[p];
-        double Uj[NV], cc[D];
+        double Uj[NV], cc[D], vpj[D + 1];
         load_node<NV>(U, NP, j, Uj);
 #pragma unroll
         for (int a = 0; a < D; ++a) cc[a] = m.c[(size_t)a * NPL + p];
-        slot(Uj, cc, w.eor[j]);
+        if (EF_VP_ROW(D)) load_node<D + 1>(w.vp, NP, j, vpj);
+        slot(Uj, cc, w.eor[j], vpj);
       }
     }
     // d row sum over the L padded slots (lower slots were filled by k_edge_visc)
@@ -429,7 +457,7 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_LOW(D), D)) k_low_o
   double Ui[NV];
   load_node<NV>(U, NP, i, Ui);
   double fi[NV][D];
-  flux<D>(Ui, g, fi);
+  node_flux<D, EF_VP_LOW(D)>(Ui, w, NP, i, g, fi);
   const double ai = w.alpha[i];
   double sumL[NV], sumR[NV];
 #pragma unroll
@@ -439,9 +467,10 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_LOW(D), D)) k_low_o
   const int card = m.card[i], dg = m.diag[i];
   const int base = sidx32(i, 0, L);
   // one slot j != i of the row, in slot order (stepper.py:441-454)
-  auto slot = [&](const double* Uj, const double* cc, double dv, double alj, double phij) {
+  auto slot = [&](const double* Uj, const double* cc, double dv, double alj, double phij, const double* vpj) {
     double fj[NV][D];
-    flux<D>(Uj, g, fj);
+    if (EF_VP_LOW(D)) flux_vp<D>(Uj, vpj, vpj[D], fj);
+    else flux<D>(Uj, g, fj);
     const double dH = dv * (0.5 * (ai + alj));
     double ubar = 0.0;
 #pragma unroll
@@ -463,7 +492,8 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_LOW(D), D)) k_low_o
   };
   if constexpr (EF_PIPE(D)) {
     // fields per slot: U_j (NV), alpha_j, phi_j, c (D), d
-    constexpr int F = NV + 2 + D + 1;
+    constexpr int NQ = EF_VP_LOW(D) ? D + 1 : 0;  // v_j, p_j
+    constexpr int F = NV + 2 + D + 1 + NQ;
     __shared__ double buf[2][F][EF_TPB_D(D)];
     const int t = threadIdx.x;
     auto issue = [&](int s, int j, int st) {
@@ -475,6 +505,8 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_LOW(D), D)) k_low_o
 #pragma unroll
       for (int a = 0; a < D; ++a) cp_async8(&buf[st][NV + 2 + a][t], m.c + (size_t)a * NPL + p);
       cp_async8(&buf[st][NV + 2 + D][t], w.d + p);
+#pragma unroll
+      for (int a = 0; a < NQ; ++a) cp_async8(&buf[st][NV + 3 + D + a][t], w.vp + a * NP + j);
     };
     auto body = [&](int, int st) {
       double Uj[NV], cc[D];
@@ -482,7 +514,10 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_LOW(D), D)) k_low_o
       for (int k = 0; k < NV; ++k) Uj[k] = buf[st][k][t];
 #pragma unroll
       for (int a = 0; a < D; ++a) cc[a] = buf[st][NV + 2 + a][t];
-      slot(Uj, cc, buf[st][NV + 2 + D][t], buf[st][NV][t], buf[st][NV + 1][t]);
+      double vpj[D + 1];
+#pragma unroll
+      for (int a = 0; a < NQ; ++a) vpj[a] = buf[st][NV + 3 + D + a][t];
+      slot(Uj, cc, buf[st][NV + 2 + D][t], buf[st][NV][t], buf[st][NV + 1][t], vpj);
     };
     row_pipe(m.col, base, card, dg, issue, body);
   } else {
@@ -495,7 +530,9 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_LOW(D), D)) k_low_o
       load_node<NV>(U, NP, j, Uj);
 #pragma unroll
       for (int a = 0; a < D; ++a) cc[a] = m.c[(size_t)a * NPL + p];
-      slot(Uj, cc, w.d[p], w.alpha[j], w.phi[j]);
+      double vpj[D + 1];
+      if (EF_VP_LOW(D)) load_node<D + 1>(w.vp, NP, j, vpj);
+      slot(Uj, cc, w.d[p], w.alpha[j], w.phi[j], vpj);
     }
   }
   const double fac = tau * m.inv_m[i];
@@ -682,10 +719,7 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_FINAL(D), D)) k_fin
   }
 #pragma unroll
   for (int k = 0; k < NV; ++k) Uout[k * NP + i] = Uo[k];
-  double e, ph;
-  nodal_one<D>(Uo, g, e, ph);  // next stage's step0
-  w.eor[i] = e;
-  w.phi[i] = ph;
+  nodal_one<D>(Uo, g, w, NP, i);  // next stage's step0
 }
 
 // ---------------------------------------------------------------- halo packing

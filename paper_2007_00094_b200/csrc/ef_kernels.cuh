@@ -71,6 +71,7 @@ struct Layout {
 struct Work {
   double* eor;       // [NP]
   double* phi;       // [NP]
+  double* vp;        // [(D+1)*NP] v = m / rho (D comps), p = gm1 * eps: the flux inputs
   double* alpha;     // [NP]
   double* R;         // [NV][NP]
   double* Unext;     // [NV][NP]
