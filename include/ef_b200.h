@@ -130,6 +130,17 @@ int ef_local_gids(ef_solver* h, int64_t* out);
 /* The shared deterministic pow (csrc/ef_pow.h): host build, to be installed
  * into the reference through physics.set_power_function, and the same code
  * evaluated on the device (test hook). */
+/* Function-level checks through the device code of the stage (diagnostics,
+ * like ef_debug_fetch): riemann.d_ij_low (riemann.py:119-142) for n pairs
+ * (Ui, Uj: (n, dim+2) AoS; cij, cji: (n, dim); out: d_ij; bad: projection
+ * error flags) and limiter.limiter_compute (limiter.py:149-193) for n lanes
+ * (U, P: (n, dim+2); bounds: (n, 3) rho_min, rho_max, phi_min; newton_steps
+ * from prm).  Gas constants from prm; run on the current device. */
+int ef_eval_dij(const ef_params* prm, int32_t dim, int64_t n, const double* Ui, const double* Uj,
+                const double* cij, const double* cji, double* out, int32_t* bad);
+int ef_eval_limiter(const ef_params* prm, int32_t dim, int64_t n, const double* U, const double* P,
+                    const double* bounds, double* out);
+
 void ef_pow_host(const double* x, double y, double* out, int64_t n);
 int ef_pow_device(const double* x, double y, double* out, int64_t n);
 

@@ -189,14 +189,14 @@ static inline double rho_eps(const double* V, int dim) { /* limiter.py:81-85 */
 
 static inline double psi_at(const double* U, const double* P, double t, double phi_min, int dim,
                             const Gas* g) { /* psi_entropy(U + t P), limiter.py:88-91 */
-  double V[5];
+  double V[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
   for (int k = 0; k < dim + 2; ++k) V[k] = U[k] + t * P[k];
   return rho_eps(V, dim) - (phi_min * opow(V[0], g->gamma + 1.0));
 }
 
 static inline double dpsi_at(const double* U, const double* P, double t, double phi_min, int dim,
                              const Gas* g) { /* dpsi_dt, limiter.py:94-110 */
-  double V[5];
+  double V[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
   for (int k = 0; k < dim + 2; ++k) V[k] = U[k] + t * P[k];
   double mm = 0.0;
   for (int a = 0; a < dim; ++a) mm += V[1 + a] * P[1 + a];
@@ -693,4 +693,29 @@ void or_pow(const double* x, double y, double* out, int64_t n) {
 }
 void or_pow2(const double* x, const double* y, double* out, int64_t n) {
   for (int64_t q = 0; q < n; ++q) out[q] = ef_pow(x[q], y[q]);
+}
+
+/* Function-level checks (riemann.d_ij_low, limiter.limiter_compute) on batches of
+ * independent inputs; the tests compare them with the reference's functions and
+ * with the device path (ef_eval_dij / ef_eval_limiter). */
+void or_eval_dij(int dim, double gamma, double gm1, double gp1_inv, double gm1_over_2g,
+                 double two_g_over_gm1, int64_t n, const double* Ui, const double* Uj,
+                 const double* cij, const double* cji, double* out, int32_t* err) {
+  Gas g = {gamma, gm1, gp1_inv, gm1_over_2g, two_g_over_gm1};
+  const int nv = dim + 2;
+  for (int64_t q = 0; q < n; ++q) {
+    int e = 0;
+    out[q] = d_ij_low(Ui + q * nv, Uj + q * nv, cij + q * dim, cji + q * dim, dim, &g, &e);
+    err[q] = e;
+  }
+}
+
+void or_eval_limiter(int dim, double gamma, double gm1, double gp1_inv, double gm1_over_2g,
+                     double two_g_over_gm1, int64_t n, const double* U, const double* P,
+                     const double* bounds, int newton, double* out) {
+  Gas g = {gamma, gm1, gp1_inv, gm1_over_2g, two_g_over_gm1};
+  const int nv = dim + 2;
+  for (int64_t q = 0; q < n; ++q)
+    out[q] = limiter_lane(U + q * nv, P + q * nv, bounds[3 * q], bounds[3 * q + 1], bounds[3 * q + 2],
+                          newton, dim, &g);
 }

@@ -66,6 +66,8 @@ def lib():
         L.or_set_threads.argtypes = [_p, _i]
         L.or_pow.argtypes = [_p, _d, _p, _i64]
         L.or_pow2.argtypes = [_p, _p, _p, _i64]
+        L.or_eval_dij.argtypes = [_i, _d, _d, _d, _d, _d, _i64, _p, _p, _p, _p, _p, _p]
+        L.or_eval_limiter.argtypes = [_i, _d, _d, _d, _d, _d, _i64, _p, _p, _p, _i, _p]
         _lib = L
     return _lib
 
@@ -251,3 +253,31 @@ class OracleSolver:
         if lib().or_fetch(self._h, self._WHICH[which], out.ctypes.data) != 0:
             raise KeyError(which)
         return out
+
+
+def _gas_args(gas):
+    if gas is None:
+        g = 7.0 / 5.0
+        return (g, g - 1.0, 1.0 / (g + 1.0), (g - 1.0) / (2.0 * g), 2.0 * g / (g - 1.0))
+    return (gas.gamma, gas.gm1, gas.gp1_inv, gas.gm1_over_2g, gas.two_g_over_gm1)
+
+
+def eval_dij(Ui, Uj, cij, cji, gas=None):
+    """riemann.d_ij_low (riemann.py:119-142) on a batch of pairs: (d, projection error flags)."""
+    Ui, Uj, cij, cji = (np.ascontiguousarray(a, dtype=np.float64) for a in (Ui, Uj, cij, cji))
+    n, dim = cij.shape
+    out = np.empty(n)
+    err = np.zeros(n, dtype=np.int32)
+    lib().or_eval_dij(dim, *_gas_args(gas), n, Ui.ctypes.data, Uj.ctypes.data, cij.ctypes.data,
+                      cji.ctypes.data, out.ctypes.data, err.ctypes.data)
+    return out, err
+
+
+def eval_limiter(U, P, bounds, newton=2, gas=None):
+    """limiter.limiter_compute (limiter.py:149-193) lane by lane."""
+    U, P, bounds = (np.ascontiguousarray(a, dtype=np.float64) for a in (U, P, bounds))
+    n, nv = U.shape
+    out = np.empty(n)
+    lib().or_eval_limiter(nv - 2, *_gas_args(gas), n, U.ctypes.data, P.ctypes.data, bounds.ctypes.data,
+                          int(newton), out.ctypes.data)
+    return out

@@ -857,6 +857,23 @@ struct ef_plan {
   ef::Plan p;
 };
 
+// scratch device buffers of the function-check entry points, freed on every path
+struct DevBufs {
+  std::vector<void*> p;
+  ~DevBufs() {
+    for (void* q : p) cudaFree(q);
+  }
+  template <class T>
+  int get(T** out, size_t count, const T* host = nullptr) {
+    void* q = nullptr;
+    EF_CUDA(cudaMalloc(&q, sizeof(T) * (count > 0 ? count : 1)));
+    p.push_back(q);
+    if (host) EF_CUDA(cudaMemcpy(q, host, sizeof(T) * count, cudaMemcpyHostToDevice));
+    *out = (T*)q;
+    return EF_OK;
+  }
+};
+
 extern "C" {
 
 const char* ef_last_error(void) { return g_err.c_str(); }
@@ -1092,6 +1109,48 @@ int ef_pow_device(const double* x, double y, double* out, int64_t n) {
   EF_CUDA(cudaMemcpy(out, dy, sizeof(double) * n, cudaMemcpyDeviceToHost));
   cudaFree(dx);
   cudaFree(dy);
+  return EF_OK;
+}
+
+int ef_eval_dij(const ef_params* prm, int32_t dim, int64_t n, const double* Ui, const double* Uj,
+                const double* cij, const double* cji, double* out, int32_t* bad) {
+  if (!prm || (dim != 2 && dim != 3) || n < 0) return fail(EF_ERR_ARG, "bad arguments");
+  if (n == 0) return EF_OK;
+  if (!Ui || !Uj || !cij || !cji || !out || !bad) return fail(EF_ERR_ARG, "null argument");
+  const Gas g = make_gas(prm);
+  const size_t nv = (size_t)dim + 2;
+  DevBufs b;
+  double *dUi, *dUj, *dci, *dcj, *dout;
+  int* dbad;
+  EF_TRY(b.get(&dUi, n * nv, Ui));
+  EF_TRY(b.get(&dUj, n * nv, Uj));
+  EF_TRY(b.get(&dci, n * (size_t)dim, cij));
+  EF_TRY(b.get(&dcj, n * (size_t)dim, cji));
+  EF_TRY(b.get(&dout, (size_t)n));
+  EF_TRY(b.get(&dbad, (size_t)n));
+  ef::launch_eval_dij(dim, g, n, dUi, dUj, dci, dcj, dout, dbad, 0);
+  EF_CUDA(cudaGetLastError());
+  EF_CUDA(cudaMemcpy(out, dout, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  EF_CUDA(cudaMemcpy(bad, dbad, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+  return EF_OK;
+}
+
+int ef_eval_limiter(const ef_params* prm, int32_t dim, int64_t n, const double* U, const double* P,
+                    const double* bounds, double* out) {
+  if (!prm || (dim != 2 && dim != 3) || n < 0) return fail(EF_ERR_ARG, "bad arguments");
+  if (n == 0) return EF_OK;
+  if (!U || !P || !bounds || !out) return fail(EF_ERR_ARG, "null argument");
+  const Gas g = make_gas(prm);
+  const size_t nv = (size_t)dim + 2;
+  DevBufs b;
+  double *dU, *dP, *dB, *dout;
+  EF_TRY(b.get(&dU, n * nv, U));
+  EF_TRY(b.get(&dP, n * nv, P));
+  EF_TRY(b.get(&dB, n * (size_t)3, bounds));
+  EF_TRY(b.get(&dout, (size_t)n));
+  ef::launch_eval_limiter(dim, g, n, dU, dP, dB, prm->newton_steps, dout, 0);
+  EF_CUDA(cudaGetLastError());
+  EF_CUDA(cudaMemcpy(out, dout, sizeof(double) * n, cudaMemcpyDeviceToHost));
   return EF_OK;
 }
 

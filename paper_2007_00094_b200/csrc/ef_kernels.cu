@@ -855,4 +855,64 @@ void launch_pow(const double* x, double y, double* out, int64_t n, cudaStream_t 
   k_pow<<<grid_for(n), TPB, 0, st>>>(x, y, out, n);
 }
 
+// ---------------------------------------------------------------- function checks
+// d_ij and the limiter on batches of independent inputs (AoS), through exactly
+// the device code the stage kernels run (the edge geometry formed as the
+// setup forms it: |c| = sqrt(R1(c*c)), n = c / |c|, e_1 for c = 0).
+template <int D>
+__global__ void k_eval_dij(Gas g, int64_t n, const double* __restrict__ Ui, const double* __restrict__ Uj,
+                           const double* __restrict__ cij, const double* __restrict__ cji,
+                           double* __restrict__ out, int* __restrict__ bad) {
+  constexpr int NV = D + 2;
+  const int64_t q = blockIdx.x * (int64_t)TPB + threadIdx.x;
+  if (q >= n) return;
+  double a[NV], b[NV], nij[D], nji[D];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    a[k] = Ui[q * NV + k];
+    b[k] = Uj[q * NV + k];
+  }
+  double sij = 0.0, sji = 0.0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    sij = sij + cij[q * D + k] * cij[q * D + k];
+    sji = sji + cji[q * D + k] * cji[q * D + k];
+  }
+  const double norm_ij = sqrt(sij), norm_ji = sqrt(sji);
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    nij[k] = norm_ij > 0.0 ? cij[q * D + k] / norm_ij : (k == 0 ? 1.0 : 0.0);
+    nji[k] = norm_ji > 0.0 ? cji[q * D + k] / norm_ji : (k == 0 ? 1.0 : 0.0);
+  }
+  bool bd = false;
+  out[q] = d_ij_geo<D>(a, b, nij, norm_ij, nji, norm_ji, g, bd);
+  bad[q] = bd ? 1 : 0;
+}
+
+template <int D>
+__global__ void k_eval_limiter(Gas g, int64_t n, const double* __restrict__ U, const double* __restrict__ P,
+                               const double* __restrict__ bounds, int newton, double* __restrict__ out) {
+  constexpr int NV = D + 2;
+  const int64_t q = blockIdx.x * (int64_t)TPB + threadIdx.x;
+  if (q >= n) return;
+  double u[NV], pp[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    u[k] = U[q * NV + k];
+    pp[k] = P[q * NV + k];
+  }
+  out[q] = limiter<D>(u, pp, bounds[3 * q], bounds[3 * q + 1], bounds[3 * q + 2], newton, g);
+}
+
+void launch_eval_dij(int dim, const Gas& g, int64_t n, const double* Ui, const double* Uj, const double* cij,
+                     const double* cji, double* out, int* bad, cudaStream_t st) {
+  if (n <= 0) return;
+  EF_DISPATCH(dim, k_eval_dij, grid_for(n), g, n, Ui, Uj, cij, cji, out, bad);
+}
+void launch_eval_limiter(int dim, const Gas& g, int64_t n, const double* U, const double* P,
+                         const double* bounds, int newton, double* out, cudaStream_t st) {
+  if (n <= 0) return;
+  EF_DISPATCH(dim, k_eval_limiter, grid_for(n), g, n, U, P, bounds, newton, out);
+}
+
 }  // namespace ef

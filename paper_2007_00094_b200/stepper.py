@@ -35,7 +35,8 @@ from . import _lib
 from .physics import AIR, AdmissibilityError, GasConstants, is_admissible
 from .problems import BoundaryConditions
 
-__all__ = ["Solver", "BoundaryConditions", "compute_tau", "cm_permutation", "STEP_NAMES"]
+__all__ = ["Solver", "BoundaryConditions", "compute_tau", "cm_permutation", "STEP_NAMES", "eval_dij",
+           "eval_limiter"]
 
 STEP_NAMES = ["step0", "step1", "step2", "step3", "step4", "step5", "step6"]
 
@@ -322,3 +323,35 @@ def shared_pow(x, y):
             _lib.load().ef_pow_host(flat_x[k:k + 1].ctypes.data, float(flat_y[k]), tmp.ctypes.data, 1)
             o[k] = tmp[0]
     return out if out.ndim else out[()]
+
+
+def _params(gas, newton_steps=2):
+    gas = gas if gas is not None else AIR
+    return _lib.EfParams(gas.gamma, gas.gm1, gas.gp1_inv, gas.gm1_over_2g, gas.two_g_over_gm1,
+                         0.9, 2, int(newton_steps), 1)
+
+
+def eval_dij(Ui, Uj, cij, cji, gas=None):
+    """riemann.d_ij_low (riemann.py:119-142) on a batch of independent pairs,
+    evaluated on the GPU by the stage's own device code.  Returns (d, bad) with
+    bad = projection error flags (rho <= 0 or p <= 0)."""
+    Ui, Uj, cij, cji = (np.ascontiguousarray(a, dtype=np.float64) for a in (Ui, Uj, cij, cji))
+    n, dim = cij.shape
+    out = np.empty(n)
+    bad = np.zeros(n, dtype=np.int32)
+    prm = _params(gas)
+    _raise(_lib.load().ef_eval_dij(ctypes.byref(prm), dim, n, Ui.ctypes.data, Uj.ctypes.data,
+                                   cij.ctypes.data, cji.ctypes.data, out.ctypes.data, bad.ctypes.data))
+    return out, bad
+
+
+def eval_limiter(U, P, bounds, newton_steps=2, gas=None):
+    """limiter.limiter_compute (limiter.py:149-193) lane by lane on the GPU;
+    bounds = (n, 3) rho_min, rho_max, phi_min."""
+    U, P, bounds = (np.ascontiguousarray(a, dtype=np.float64) for a in (U, P, bounds))
+    n, nv = U.shape
+    out = np.empty(n)
+    prm = _params(gas, newton_steps)
+    _raise(_lib.load().ef_eval_limiter(ctypes.byref(prm), nv - 2, n, U.ctypes.data, P.ctypes.data,
+                                       bounds.ctypes.data, out.ctypes.data))
+    return out

@@ -43,6 +43,8 @@ from eulerflow import assembly as r_assembly  # noqa: E402
 from eulerflow import mesh as r_mesh  # noqa: E402
 from eulerflow import physics as r_physics  # noqa: E402
 from eulerflow import problems as r_problems  # noqa: E402
+from eulerflow import limiter as r_limiter  # noqa: E402
+from eulerflow import riemann as r_riemann  # noqa: E402
 from eulerflow.assembly import PrecomputedMatrices as RefMatrices  # noqa: E402
 from eulerflow.stepper import BoundaryConditions as RefBC  # noqa: E402
 from eulerflow.stepper import Solver as RefSolver  # noqa: E402
@@ -174,12 +176,65 @@ def small_cases():
     save_case("periodic3d_random_euler", mat, U, None, base(), 1, "euler")
     save_case("periodic3d_random_rk3", mat, U, None, base(), 2, "rk3")
     c4_case()
+    function_cases()
 
 
 def c4_case():
     """C4-shaped (extruded O-grid around a cylinder), oracle size."""
     ps = P.mach3_cylinder(10, 3, seed=13)
     save_case("c4_cylinder", ps.matrices, ps.U0, ps.boundary, base(), 2, "rk3", record_internals=False)
+
+
+def function_cases():
+    """riemann.d_ij_low and limiter.limiter_compute of the unmodified reference on
+    seeded batches (function-level parity, like test_riemann.py / test_limiter.py):
+    densities 1e-3..10, pressures 1e-4..1e4 (log-uniform), |u| ~ N(0, 2), equal
+    states, equal pressures, zero and exactly antisymmetric c vectors; limiter
+    lanes with corrections from 1e-2 to 10 times the state, bounds around it."""
+    gas = r_physics.AIR
+    for dim in (2, 3):
+        rng = np.random.default_rng(7000 + dim)
+        n = 3000
+
+        def states(k):
+            rho = np.exp(rng.uniform(np.log(1e-3), np.log(10.0), k))
+            u = rng.normal(0.0, 2.0, (k, dim))
+            p = np.exp(rng.uniform(np.log(1e-4), np.log(1e4), k))
+            U = np.empty((k, dim + 2))
+            U[:, 0] = rho
+            U[:, 1:-1] = rho[:, None] * u
+            U[:, -1] = p / gas.gm1 + 0.5 * rho * (u * u).sum(axis=1)
+            return U
+
+        Ui, Uj = states(n), states(n)
+        Uj[: n // 10] = Ui[: n // 10]                               # identical pairs
+        k = slice(n // 10, n // 5)                                     # equal pressures
+        pi = gas.gm1 * (Ui[k, -1] - 0.5 * (Ui[k, 1:-1] ** 2).sum(axis=1) / Ui[k, 0])
+        Uj[k, -1] = pi / gas.gm1 + 0.5 * (Uj[k, 1:-1] ** 2).sum(axis=1) / Uj[k, 0]
+        cij = rng.normal(0.0, 1.0, (n, dim))
+        cji = rng.normal(0.0, 1.0, (n, dim))
+        cji[n // 5: n // 2] = -cij[n // 5: n // 2]                     # antisymmetric
+        cij[-n // 20:] = 0.0                                           # zero c_ij
+        cji[-n // 40:] = 0.0
+        d = r_riemann.d_ij_low(Ui, Uj, cij, cji, gas)
+        U = states(n)
+        scale = np.exp(rng.uniform(np.log(1e-2), np.log(10.0), n))
+        Pc = rng.normal(0.0, 1.0, (n, dim + 2)) * U * scale[:, None]
+        rho = U[:, 0]
+        rmin = rho * (1.0 - rng.uniform(0.0, 0.3, n))
+        rmax = rho * (1.0 + rng.uniform(0.0, 0.3, n))
+        eps = U[:, -1] - 0.5 * (U[:, 1:-1] ** 2).sum(axis=1) / rho
+        phi = eps * rho ** (-gas.gamma)
+        pmin = phi * (1.0 - rng.uniform(0.0, 0.1, n))
+        pmin[: n // 10] = phi[: n // 10]                               # bound at the state itself
+        bounds = np.column_stack([rmin, rmax, pmin])
+        l2 = r_limiter.limiter_compute(U, Pc, rmin, rmax, pmin, 2, gas)
+        l4 = r_limiter.limiter_compute(U, Pc, rmin, rmax, pmin, 4, gas)
+        path = os.path.join(HERE, f"functions_{dim}d.npz")
+        np.savez_compressed(path, Ui=Ui, Uj=Uj, cij=cij, cji=cji, d=d, U=U, P=Pc, bounds=bounds,
+                            l_newton2=l2, l_newton4=l4)
+        print(f"functions_{dim}d: d in [{d.min():.3g}, {d.max():.3g}], "
+              f"l<1 on {int((l2 < 1).sum())}/{n} lanes -> {os.path.getsize(path) / 1024:.0f} KiB")
 
 
 def c1_full():
@@ -230,10 +285,13 @@ if __name__ == "__main__":
     ap.add_argument("--c1-full", action="store_true")
     ap.add_argument("--only-c1-full", action="store_true")
     ap.add_argument("--only-c4", action="store_true")
+    ap.add_argument("--only-functions", action="store_true")
     args = ap.parse_args()
     r_physics.set_power_function(O.shared_pow)
     if args.only_c4:
         c4_case()
+    elif args.only_functions:
+        function_cases()
     elif not args.only_c1_full:
         small_cases()
         default_pow_divergence()

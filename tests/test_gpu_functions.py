@@ -1,0 +1,103 @@
+"""Function-level parity and properties of the device arithmetic, through the
+C-ABI checks ef_eval_dij / ef_eval_limiter (the stage kernels' own device code).
+
+* bitwise equal to the unmodified reference's riemann.d_ij_low and
+  limiter.limiter_compute on the seeded batches of tests/golden/functions_*.npz
+  (extreme density/pressure ratios, identical states, equal pressures, zero and
+  antisymmetric c vectors; Newton steps 2 and 4), and to the oracle on fresh
+  random batches;
+* the reference's unit-test properties (test_riemann.py:23-30, :87-98;
+  test_limiter.py:86-102, :153-158): the identical-state pair gives
+  (|u.n| + c)|c|, d is symmetric, l lies in [0, 1] and U + l P keeps the
+  density inside the bounds."""
+
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+from goldens import GOLDEN_DIR
+from paper_2007_00094_b200.physics import AIR
+from paper_2007_00094_b200.stepper import eval_dij, eval_limiter
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_device_functions_match_reference(dim):
+    z = np.load(os.path.join(GOLDEN_DIR, f"functions_{dim}d.npz"))
+    d, bad = eval_dij(z["Ui"], z["Uj"], z["cij"], z["cji"])
+    assert not bad.any()
+    assert np.array_equal(d, z["d"])
+    for newton in (2, 4):
+        l = eval_limiter(z["U"], z["P"], z["bounds"], newton)
+        assert np.array_equal(l, z[f"l_newton{newton}"])
+
+
+def _states(rng, n, dim):
+    rho = np.exp(rng.uniform(np.log(1e-6), np.log(1e3), n))
+    u = rng.normal(0.0, 5.0, (n, dim))
+    p = np.exp(rng.uniform(np.log(1e-8), np.log(1e8), n))
+    U = np.empty((n, dim + 2))
+    U[:, 0] = rho
+    U[:, 1:-1] = rho[:, None] * u
+    U[:, -1] = p / AIR.gm1 + 0.5 * rho * (u * u).sum(axis=1)
+    return U
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_device_dij_equals_oracle_on_random_batches(dim):
+    rng = np.random.default_rng(11 + dim)
+    n = 200000
+    Ui, Uj = _states(rng, n, dim), _states(rng, n, dim)
+    cij, cji = rng.normal(0.0, 1.0, (n, dim)), rng.normal(0.0, 1.0, (n, dim))
+    d, bad = eval_dij(Ui, Uj, cij, cji)
+    do, bo = O.eval_dij(Ui, Uj, cij, cji)
+    assert np.array_equal(d, do) and np.array_equal(bad, bo)
+    # symmetry (test_riemann.py:87-98)
+    d2, _ = eval_dij(Uj, Ui, cji, cij)
+    assert np.array_equal(d, d2)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_identical_states_give_wave_speed(dim):
+    """test_riemann.py:23-30: for U_i = U_j the bound is |u.n| + c, times |c|."""
+    rng = np.random.default_rng(5)
+    n = 10000
+    # moderate Mach numbers: p recovered from E without cancellation
+    rho = np.exp(rng.uniform(np.log(1e-2), np.log(1e2), n))
+    u = rng.normal(0.0, 1.0, (n, dim))
+    p = np.exp(rng.uniform(np.log(1e-1), np.log(1e1), n)) * rho
+    U = np.empty((n, dim + 2))
+    U[:, 0] = rho
+    U[:, 1:-1] = rho[:, None] * u
+    U[:, -1] = p / AIR.gm1 + 0.5 * rho * (u * u).sum(axis=1)
+    c = rng.normal(0.0, 1.0, (n, dim))
+    d, _ = eval_dij(U, U, c, -c)
+    cs = np.sqrt(AIR.gamma * p / rho)
+    nrm = np.linalg.norm(c, axis=1)
+    expect = (np.abs((u * c).sum(axis=1) / nrm) + cs) * nrm
+    assert np.allclose(d, expect, rtol=1e-11, atol=0.0)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_limiter_properties_and_parity(dim):
+    """l in [0, 1], density of U + l P inside [rho_min, rho_max] (test_limiter.py:
+    153-158), Psi(U + l P) >= -tol (:86-102); equal to the oracle bitwise."""
+    rng = np.random.default_rng(23 + dim)
+    n = 100000
+    U = _states(rng, n, dim)
+    P = rng.normal(0.0, 1.0, (n, dim + 2)) * U * np.exp(rng.uniform(-4, 2, n))[:, None]
+    rho = U[:, 0]
+    rmin = rho * (1.0 - rng.uniform(0.0, 0.5, n))
+    rmax = rho * (1.0 + rng.uniform(0.0, 0.5, n))
+    eps = U[:, -1] - 0.5 * (U[:, 1:-1] ** 2).sum(axis=1) / rho
+    pmin = eps * rho ** (-AIR.gamma) * (1.0 - rng.uniform(0.0, 0.2, n))
+    bounds = np.column_stack([rmin, rmax, pmin])
+    for newton in (1, 2, 4):
+        l = eval_limiter(U, P, bounds, newton)
+        assert np.array_equal(l, O.eval_limiter(U, P, bounds, newton))
+        assert np.all((l >= 0.0) & (l <= 1.0))
+        r = rho + l * P[:, 0]
+        assert np.all(r >= rmin * (1 - 1e-12)) and np.all(r <= rmax * (1 + 1e-12))

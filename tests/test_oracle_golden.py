@@ -65,3 +65,17 @@ def test_oracle_errors_match_reference_semantics():
     bad[3, 0] = -1.0
     with pytest.raises(ValueError):
         o.set_state(bad)        # AdmissibilityError is a ValueError (physics.py:55)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_oracle_functions_match_reference(dim):
+    """Function level: the oracle's d_ij_low and limiter_compute equal the
+    reference's (riemann.py:119-142, limiter.py:149-193) bit for bit on the
+    seeded batches of tests/golden/functions_{dim}d.npz (make_golden.py)."""
+    z = np.load(os.path.join(GOLDEN_DIR, f"functions_{dim}d.npz"))
+    d, err = O.eval_dij(z["Ui"], z["Uj"], z["cij"], z["cji"])
+    assert not err.any()
+    assert np.array_equal(d, z["d"])
+    for newton in (2, 4):
+        l = O.eval_limiter(z["U"], z["P"], z["bounds"], newton)
+        assert np.array_equal(l, z[f"l_newton{newton}"])
