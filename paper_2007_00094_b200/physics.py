@@ -11,7 +11,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-__all__ = ["GasConstants", "AIR", "AdmissibilityError", "internal_energy", "is_admissible",
+__all__ = ["GasConstants", "AIR", "AdmissibilityError", "internal_energy", "is_admissible", "pressure",
            "n_variables"]
 
 
@@ -49,3 +49,8 @@ def internal_energy(U: np.ndarray) -> np.ndarray:
 
 def is_admissible(U: np.ndarray) -> np.ndarray:
     return (U[..., 0] > 0.0) & (internal_energy(U) > 0.0)
+
+
+def pressure(U: np.ndarray, gas: GasConstants = AIR) -> np.ndarray:
+    """p = (gamma - 1) eps (physics.py:92-94)."""
+    return gas.gm1 * internal_energy(U)

@@ -175,3 +175,19 @@ def test_device_pow_equals_host_pow():
         assert _lib.load().ef_pow_device(x.ctypes.data, y, dev.ctypes.data, x.size) == 0
         assert np.array_equal(host, dev, equal_nan=True)
         assert np.array_equal(host, O.shared_pow(x, y), equal_nan=True)
+
+
+def test_perf_report_and_snapshot(tmp_path):  # perf.py:92-153, output.py:53-106
+    from paper_2007_00094_b200 import output, perf
+
+    ps = P.isentropic_vortex(24)
+    s = Solver(ps.matrices, c_cfl=ps.c_cfl, boundary=ps.boundary)
+    s.set_state(ps.U0)
+    s.enable_timers(True)
+    for _ in range(3):
+        s.ssp_rk3_step()
+    txt = perf.report(s, csv_path=str(tmp_path / "perf.csv"))
+    assert "s/stage" in txt and "syncs=" in txt
+    assert (tmp_path / "perf.csv").read_text().startswith("phase,kernel")
+    output.write_vtk(str(tmp_path / "v.vtk"), ps.mesh, s.get_state(), ps.matrices)
+    assert (tmp_path / "v.vtk").stat().st_size > 0
