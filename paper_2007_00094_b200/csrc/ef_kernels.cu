@@ -14,12 +14,15 @@
 //   k_row_upd      = step5 non-final limited update (:480-481), one thread per row
 //   k_final        = step6 final pass + _k_boundary + _finish_step check
 //                    + SSP-RK3 combination + next stage's step0 (:493-504, :612-636, :399-405)
-// k_edge_visc is one thread per edge; the others one thread per owned row.
-// (A row-group variant -- G lanes per row, ordered sums from shared memory --
-// measured 40% slower on C2 and was dropped.)
-// k_edge_visc writes d_ij also into the lower slot of row j (d is symmetric)
-// and k_edge_lim writes P and min(l_ij, l_ji) to both rows of an edge, so the
-// row kernels stream their own slots instead of gathering transposes.
+// The edge kernels run one thread per upper edge, the row kernels one thread
+// per owned row.  k_edge_visc writes d_ij also into the lower slot of row j
+// (d is symmetric) and k_edge_lim writes P and min(l_ij, l_ji) to both rows of
+// an edge, so the row kernels stream their own slots instead of gathering
+// transposes.  The gather loops of k_row_visc / k_low_order prefetch the next
+// slot's neighbour fields with cp.async (row_pipe); step0 (fused into k_final
+// and k_nodal) caches v = m / rho and p for the neighbour fluxes.  Variants
+// measured slower (row groups, slot-parallel and row-owned limiters, half-edge
+// limiter, PDL, ...) are listed in DESIGN.md §6.
 #include "ef_kernels.cuh"
 
 namespace ef {
