@@ -110,6 +110,9 @@ const char* ef_last_error(void);
 /* Solver.timers (stepper.py:37, 515-607): seconds per phase step0..step6,
  * accumulated while timing is enabled (adds a sync per phase). */
 int ef_enable_timers(ef_solver* h, int32_t on);
+/* CUDA-graph replay of whole steps (single rank; on by default unless the
+ * environment sets EF_GRAPHS=0).  Results are identical either way. */
+int ef_enable_graphs(ef_solver* h, int32_t on);
 int ef_phase_times(ef_solver* h, double* seconds7);
 /* Solver.n_euler_steps, comm.sync_count, comm.sync_volume (doubles) */
 int ef_counters(ef_solver* h, int64_t* out3);

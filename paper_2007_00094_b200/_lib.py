@@ -58,6 +58,7 @@ SIGNATURES = {
     "ef_bad_node": (_i64, [_p]),
     "ef_last_error": (ctypes.c_char_p, []),
     "ef_enable_timers": (_i32, [_p, _i32]),
+    "ef_enable_graphs": (_i32, [_p, _i32]),
     "ef_phase_times": (_i32, [_p, _p]),
     "ef_counters": (_i32, [_p, _p]),
     "ef_info": (_i32, [_p, _p]),

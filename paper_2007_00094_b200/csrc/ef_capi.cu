@@ -15,6 +15,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <string>
@@ -149,6 +150,25 @@ struct ef_solver {
   // into phase_s when the ring fills or the timers are read
   std::vector<std::array<cudaEvent_t, 8>> ring;
   int ring_used = 0;
+  // CUDA graphs of whole steps (single rank, timers off): one launch replays the
+  // ~25 kernels and memsets of an RK step.  Keyed by everything the captured
+  // launches depend on; a few entries cover the rotating U buffers.
+  struct GraphKey {
+    int rk3, cur, has_tau;
+    double tau, tau_max;
+    bool operator==(const GraphKey& o) const {
+      return rk3 == o.rk3 && cur == o.cur && has_tau == o.has_tau &&
+             std::memcmp(&tau, &o.tau, sizeof tau) == 0 && std::memcmp(&tau_max, &o.tau_max, sizeof tau_max) == 0;
+    }
+  };
+  struct GraphEntry {
+    GraphKey key;
+    cudaGraphExec_t exec;
+    uint64_t used;
+  };
+  std::vector<GraphEntry> graphs;
+  uint64_t graph_clock = 0;
+  bool use_graphs = true;
 
   template <class T>
   int alloc(T** p, size_t count) {
@@ -166,6 +186,7 @@ struct ef_solver {
     if (rb) cudaFreeHost(rb);
     for (auto& set : ring)
       for (auto& e : set) cudaEventDestroy(e);
+    for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
     if (comm && nccl().ok) nccl().CommDestroy(comm);
     if (evB) cudaEventDestroy(evB);
     if (evX) cudaEventDestroy(evX);
@@ -774,6 +795,51 @@ static int rk3_async(Driver& d, int32_t has_tau, double tau, double tau_max, int
   return EF_OK;
 }
 
+// One step (forward Euler or SSP-RK3) queued on the stream.  A single rank with
+// the timers off replays a CUDA graph of the step's launches, captured on first
+// use per (kind, U buffer, tau arguments); anything else launches directly.  A
+// capture that fails turns graphs off for the handle and runs the step directly.
+static int step_async(Driver& d, bool rk3, int32_t has_tau, double tau, double tau_max, int* out_buf) {
+  ef_solver* h = d.h0();
+  auto body = [&]() {
+    return rk3 ? rk3_async(d, has_tau, tau, tau_max, out_buf) : euler_async(d, has_tau, tau, tau_max, out_buf);
+  };
+  if (!h->use_graphs || h->timing || d.group || h->nranks > 1) return body();
+  const ef_solver::GraphKey key{rk3 ? 1 : 0, h->cur, has_tau ? 1 : 0, has_tau ? tau : 0.0, tau_max};
+  for (auto& g : h->graphs)
+    if (g.key == key) {
+      g.used = ++h->graph_clock;
+      EF_CUDA(cudaGraphLaunch(g.exec, h->st));
+      *out_buf = (h->cur + 1) % 3;  // euler: in + 1; rk3: u0 + 1
+      h->n_euler += rk3 ? 3 : 1;
+      return EF_OK;
+    }
+  const int64_t n0 = h->n_euler;
+  cudaError_t e = cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal);
+  int rc = e == cudaSuccess ? body() : EF_ERR_CUDA;
+  cudaGraph_t graph = nullptr;
+  if (e == cudaSuccess) e = cudaStreamEndCapture(h->st, &graph);
+  cudaGraphExec_t exec = nullptr;
+  if (rc == EF_OK && e == cudaSuccess && graph) e = cudaGraphInstantiate(&exec, graph, 0);
+  if (graph) cudaGraphDestroy(graph);
+  if (rc != EF_OK || e != cudaSuccess || !exec) {
+    if (exec) cudaGraphExecDestroy(exec);
+    cudaGetLastError();
+    h->use_graphs = false;
+    h->n_euler = n0;
+    return body();
+  }
+  if (h->graphs.size() >= 8) {
+    auto old = std::min_element(h->graphs.begin(), h->graphs.end(),
+                                [](const auto& a, const auto& b) { return a.used < b.used; });
+    cudaGraphExecDestroy(old->exec);
+    h->graphs.erase(old);
+  }
+  h->graphs.push_back({key, exec, ++h->graph_clock});
+  EF_CUDA(cudaGraphLaunch(exec, h->st));  // n_euler was advanced by the captured body
+  return EF_OK;
+}
+
 static int readback(ef_solver* h) {
   EF_CUDA(cudaMemcpyAsync(&h->rb->tau, h->w.tau, sizeof(double), cudaMemcpyDeviceToHost, h->st));
   EF_CUDA(cudaMemcpyAsync(&h->rb->err, h->w.err, sizeof(int), cudaMemcpyDeviceToHost, h->st));
@@ -925,6 +991,10 @@ int ef_create(const ef_matrices* mat, const ef_params* prm, const ef_boundary* b
     h->own_stream = true;
   }
   h->overlap = prm->overlap != 0;
+  {
+    const char* ge = std::getenv("EF_GRAPHS");
+    h->use_graphs = !(ge && ge[0] == '0');
+  }
   int rc = build(h, mat, bc, dist);
   if (rc != EF_OK) return bail(rc);
   if (h->nranks > 1) {
@@ -983,7 +1053,7 @@ int ef_euler_step(ef_solver* h, int32_t has_tau, double tau, double tau_max, dou
   Driver d;
   EF_TRY(single_driver(h, d));
   int out;
-  EF_TRY(euler_async(d, has_tau, tau, tau_max, &out));
+  EF_TRY(step_async(d, false, has_tau, tau, tau_max, &out));
   return finish(d, out, tau_used);
 }
 
@@ -991,7 +1061,7 @@ int ef_ssp_rk3_step(ef_solver* h, int32_t has_tau, double tau, double tau_max, d
   Driver d;
   EF_TRY(single_driver(h, d));
   int out;
-  EF_TRY(rk3_async(d, has_tau, tau, tau_max, &out));
+  EF_TRY(step_async(d, true, has_tau, tau, tau_max, &out));
   return finish(d, out, tau_used);
 }
 
@@ -1000,7 +1070,7 @@ int ef_ssp_rk3_step_async(ef_solver* h, int32_t has_tau, double tau, double tau_
   EF_TRY(single_driver(h, d));
   if (h->pending_out >= 0) h->cur = h->pending_out;  // chain on the unchecked result
   int out;
-  EF_TRY(rk3_async(d, has_tau, tau, tau_max, &out));
+  EF_TRY(step_async(d, true, has_tau, tau, tau_max, &out));
   h->pending_out = out;
   return EF_OK;
 }
@@ -1023,6 +1093,12 @@ int64_t ef_bad_node(const ef_solver* h) { return h ? h->bad_node : -1; }
 int ef_enable_timers(ef_solver* h, int32_t on) {
   if (!h) return fail(EF_ERR_ARG, "null handle");
   h->timing = on != 0;
+  return EF_OK;
+}
+
+int ef_enable_graphs(ef_solver* h, int32_t on) {
+  if (!h) return fail(EF_ERR_ARG, "null handle");
+  h->use_graphs = on != 0;
   return EF_OK;
 }
 
@@ -1226,7 +1302,7 @@ int ef_group_euler_step(ef_group* g, int32_t has_tau, double tau, double tau_max
   if (!g) return fail(EF_ERR_ARG, "null handle");
   Driver d = group_driver(g);
   int out;
-  EF_TRY(euler_async(d, has_tau, tau, tau_max, &out));
+  EF_TRY(step_async(d, false, has_tau, tau, tau_max, &out));
   return finish(d, out, tau_used);
 }
 
@@ -1234,7 +1310,7 @@ int ef_group_ssp_rk3_step(ef_group* g, int32_t has_tau, double tau, double tau_m
   if (!g) return fail(EF_ERR_ARG, "null handle");
   Driver d = group_driver(g);
   int out;
-  EF_TRY(rk3_async(d, has_tau, tau, tau_max, &out));
+  EF_TRY(step_async(d, true, has_tau, tau, tau_max, &out));
   return finish(d, out, tau_used);
 }
 

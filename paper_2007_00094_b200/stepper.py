@@ -281,6 +281,11 @@ class Solver:
         _raise(_lib.load().ef_enable_timers(self._h, 1 if on else 0))
         self._timers_on = on
 
+    def enable_graphs(self, on: bool = True):
+        """CUDA-graph replay of whole steps (default on; identical results)."""
+        for h in self._handles:
+            _raise(_lib.load().ef_enable_graphs(h, 1 if on else 0))
+
     @property
     def timers(self) -> Dict[str, float]:
         s = np.zeros(7)

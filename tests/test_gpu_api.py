@@ -191,3 +191,30 @@ def test_perf_report_and_snapshot(tmp_path):  # perf.py:92-153, output.py:53-106
     assert (tmp_path / "perf.csv").read_text().startswith("phase,kernel")
     output.write_vtk(str(tmp_path / "v.vtk"), ps.mesh, s.get_state(), ps.matrices)
     assert (tmp_path / "v.vtk").stat().st_size > 0
+
+
+def test_graph_replay_is_bitwise_identical():
+    """Steps replayed from captured CUDA graphs equal directly launched steps:
+    RK3 and Euler, CFL and given tau, tau_max, the async chain, a state reset
+    between replays, and the step counter."""
+    ps = P.make_config("c1", scale="small")
+    runs = []
+    for graphs in (True, False):
+        s = Solver(ps.matrices, c_cfl=ps.c_cfl, boundary=ps.boundary)
+        s.enable_graphs(graphs)
+        s.set_state(ps.U0)
+        taus = [s.ssp_rk3_step() for _ in range(4)]
+        taus.append(s.euler_step(tau=1e-3))
+        taus.append(s.euler_step(tau=1e-3))
+        taus.append(s.euler_step(tau=5e-4))
+        taus.append(s.ssp_rk3_step(tau_max=1e-3))
+        mid = s.get_state()
+        s.set_state(mid)
+        for _ in range(5):
+            s.ssp_rk3_step_async()
+        taus.append(s.sync())
+        runs.append((np.array(taus), s.get_state(), s.n_euler_steps))
+    (ta, Ua, na), (tb, Ub, nb) = runs
+    assert np.array_equal(ta, tb)
+    assert np.array_equal(Ua, Ub)
+    assert na == nb == 4 * 3 + 3 + 3 + 5 * 3
