@@ -634,6 +634,63 @@ def random_state(rng, n: int, dim: int = 2) -> np.ndarray:
     return U
 
 
+def _reduced_points(mesh: Mesh) -> np.ndarray:
+    """One representative point per solver node (the last periodic copy wins)."""
+    pts = np.zeros((mesh.n_nodes, mesh.dim))
+    pts[mesh.reduced_index] = mesh.points
+    return pts
+
+
+def periodic_smooth(n: int = 32, refine: int = 0, velocity=(1.0, 0.5), gas: GasConstants = AIR,
+                    steps: int = 0) -> ProblemSetup:
+    """Density wave advected through the periodic unit square at constant
+    velocity and pressure, with its exact solution (reference problems.py:84-121)."""
+    n = n * (2 ** refine)
+    mesh = rectangle_mesh(n, n, periodic=(True, True))
+    v = np.asarray(velocity, dtype=np.float64)
+
+    def exact(points, t):
+        rho = 1.0 + 0.3 * np.sin(2.0 * np.pi * (points[:, 0] - v[0] * t)) * np.sin(
+            2.0 * np.pi * (points[:, 1] - v[1] * t))
+        U = np.zeros((len(points), 4))
+        U[:, 0] = rho
+        U[:, 1] = rho * v[0]
+        U[:, 2] = rho * v[1]
+        U[:, 3] = 1.0 / gas.gm1 + 0.5 * rho * (v @ v)
+        return U
+
+    U0 = exact(_reduced_points(mesh), 0.0)
+    return ProblemSetup("periodic-smooth", assemble_q1(mesh), U0, None, c_cfl=0.9, steps=steps, mesh=mesh,
+                        exact=exact)
+
+
+def sod1d(n: int = 100, refine: int = 0, gas: GasConstants = AIR, steps: int = 0) -> ProblemSetup:
+    """Shock tube on a y-periodic strip of n x 1 quads (reference problems.py:124-137)."""
+    n = n * (2 ** refine)
+    mesh = rectangle_mesh(n, 1, (0.0, 1.0), (0.0, 1.0 / n), periodic=(False, True))
+    left = _reduced_points(mesh)[:, 0] < 0.5
+    U0 = np.zeros((mesh.n_nodes, 4))
+    U0[:, 0] = np.where(left, 1.0, 0.125)
+    U0[:, 3] = np.where(left, 1.0, 0.1) / gas.gm1
+    return ProblemSetup("sod1d", assemble_q1(mesh), U0, None, c_cfl=0.9, steps=steps, mesh=mesh)
+
+
+# problem names the command line accepts (cli.py): the BASELINE.json configs and
+# the reference's two analytic 2D set-ups
+PROBLEMS = ("c1", "c2", "c3", "c4", "c5", "c3m", "c4m", "c5m", "periodic-smooth", "sod1d")
+
+
+def make_problem(name: str, refine: int = 0, scale: str = "full", gas: GasConstants = AIR) -> ProblemSetup:
+    """Problem factory of the command line (reference problems.py:140-146)."""
+    if name == "periodic-smooth":
+        return periodic_smooth(refine=refine, gas=gas)
+    if name == "sod1d":
+        return sod1d(refine=refine, gas=gas)
+    if name in PROBLEMS:
+        return make_config(name, scale=scale, gas=gas)
+    raise ValueError(f"unknown problem {name!r}")
+
+
 def make_config(name: str, scale: str = "full", gas: GasConstants = AIR) -> ProblemSetup:
     """BASELINE.json configs by name; scale='small' gives oracle-sized instances."""
     small = scale == "small"
