@@ -35,6 +35,7 @@ __all__ = [
     "Mesh",
     "ProblemSetup",
     "assemble_q1",
+    "assemble_q1_rows",
     "rectangle_mesh",
     "box_mesh",
     "disc_channel_mesh",
@@ -148,20 +149,20 @@ def _inv_det(J: np.ndarray):
     return np.linalg.inv(J), det
 
 
-def assemble_q1(mesh: Mesh, chunk: int = 1 << 15) -> PrecomputedMatrices:
-    """Assemble m_ij, c_ij and the lumped mass on the Q1 stencil graph."""
+def _q1_local_fn(mesh: Mesh, chunk: int):
+    """Per-chunk local Q1 matrices (2-point tensor Gauss): f(cell_ids) ->
+    (rows, cols, m, c) in cell order, local (a, b) row-major within a cell."""
     d = mesh.dim
     cells = mesh.cells
     red = np.asarray(mesh.reduced_index, dtype=np.int64)
-    n = mesh.n_nodes
     nv = cells.shape[1]
     g = np.array([0.5 - 0.5 / np.sqrt(3.0), 0.5 + 0.5 / np.sqrt(3.0)])
     qpts = np.stack(np.meshgrid(*([g] * d), indexing="ij"), axis=-1).reshape(-1, d)
     w = 0.5**d
     shapes = [_shape(d, xi) for xi in qpts]
 
-    def local(lo):  # local matrices of one chunk of cells (numpy releases the GIL)
-        cc = cells[lo : lo + chunk]
+    def local(ids):  # numpy releases the GIL
+        cc = cells[ids]
         X = mesh.points[cc]  # (M, nv, d)
         m_loc = np.zeros((len(cc), nv, nv))
         c_loc = np.zeros((len(cc), nv, nv, d))
@@ -178,12 +179,80 @@ def assemble_q1(mesh: Mesh, chunk: int = 1 << 15) -> PrecomputedMatrices:
         return (np.repeat(rc, nv, axis=1).ravel(), np.tile(rc, (1, nv)).ravel(), m_loc.ravel(),
                 c_loc.reshape(-1, d))
 
+    return local
+
+
+def _local_parts(mesh: Mesh, cell_ids: np.ndarray, chunk: int):
+    """Local matrices of the given cells (ascending), chunked over all host
+    threads; per-cell values do not depend on the chunking."""
     from concurrent.futures import ThreadPoolExecutor
 
-    # the same chunks as a sequential loop, evaluated on all host threads: per-cell
-    # values do not depend on the chunking, so the result is identical
+    local = _q1_local_fn(mesh, chunk)
     with ThreadPoolExecutor(max_workers=os.cpu_count() or 1) as pool:
-        parts = list(pool.map(local, range(0, len(cells), chunk)))
+        return list(pool.map(lambda lo: local(cell_ids[lo:lo + chunk]), range(0, len(cell_ids), chunk)))
+
+
+def assemble_q1_rows(mesh: Mesh, slabs: int, chunk: int = 1 << 15) -> PrecomputedMatrices:
+    """`assemble_q1` one range of rows at a time (memory ~1/slabs of it): the
+    rows of a range take the same cell contributions in the same order, so every
+    value is bit-identical.  For meshes whose cells never repeat a node (m is
+    then exactly symmetric, so the symmetrisation is the identity); used for the
+    8.4M-node C3 box."""
+    d = mesh.dim
+    n = mesh.n_nodes
+    red = np.asarray(mesh.reduced_index, dtype=np.int64)
+    rc_all = red[mesh.cells]
+    if np.any(np.sort(rc_all, axis=1)[:, 1:] == np.sort(rc_all, axis=1)[:, :-1]):
+        raise ValueError("assemble_q1_rows needs cells with distinct nodes")
+    bounds = np.linspace(0, n, slabs + 1).astype(np.int64)
+    counts = np.zeros(n, dtype=np.int64)
+    idx_parts, m_parts, c_parts = [], [], []
+    for r0, r1 in zip(bounds[:-1], bounds[1:]):
+        if r1 <= r0:
+            continue
+        cell_ids = np.flatnonzero(((rc_all >= r0) & (rc_all < r1)).any(axis=1))
+        parts = _local_parts(mesh, cell_ids, chunk)
+        rows = np.concatenate([q[0] for q in parts])
+        keep = (rows >= r0) & (rows < r1)
+        rows = rows[keep]
+        cols = np.concatenate([q[1] for q in parts])[keep]
+        mv = np.concatenate([q[2] for q in parts])[keep]
+        cv = np.concatenate([q[3] for q in parts])[keep]
+        del parts, keep
+        key = rows * n + cols
+        order = np.argsort(key, kind="stable")
+        key = key[order]
+        first = np.ones(len(key), dtype=bool)
+        first[1:] = key[1:] != key[:-1]
+        seg = np.flatnonzero(first)
+        m_parts.append(np.add.reduceat(mv[order], seg))
+        c_parts.append(np.add.reduceat(cv[order], seg, axis=0))
+        ukey = key[seg]
+        idx_parts.append((ukey % n).astype(np.int64))
+        counts[r0:r1] = np.bincount(ukey // n - r0, minlength=r1 - r0)
+        del rows, cols, mv, cv, key, order, first, seg, ukey
+    indptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(counts, out=indptr[1:])
+    indices = np.concatenate(idx_parts)
+    m_data = np.concatenate(m_parts)
+    del idx_parts, m_parts
+    c_data = np.concatenate(c_parts)
+    del c_parts
+    m_sym = 0.5 * (m_data + m_data)  # = m exactly: the local mass matrices are symmetric
+    m_lumped = np.add.reduceat(m_sym, indptr[:-1])
+    if np.any(m_lumped <= 0.0):
+        raise ValueError("non-positive lumped mass entry")
+    return PrecomputedMatrices(
+        n=n, dim=d, indptr=indptr, indices=indices, m=m_sym, c=c_data,
+        beta=np.zeros(0), m_lumped=m_lumped, inv_m=1.0 / m_lumped,
+    )
+
+
+def assemble_q1(mesh: Mesh, chunk: int = 1 << 15) -> PrecomputedMatrices:
+    """Assemble m_ij, c_ij and the lumped mass on the Q1 stencil graph."""
+    n = mesh.n_nodes
+    d = mesh.dim
+    parts = _local_parts(mesh, np.arange(len(mesh.cells)), chunk)
     rows_all = [q[0] for q in parts]
     cols_all = [q[1] for q in parts]
     mv_all = [q[2] for q in parts]
@@ -475,7 +544,8 @@ def sod_box(nx: int = 511, ny: int = 127, nz: int = 127, jitter: float = 0.2, se
     """BASELINE C3: [0,1]x[0,.25]^2 hex box, (nx+1)(ny+1)(nz+1) nodes, interior
     jitter ±0.2h, Sod states split at x=0.5, slip walls."""
     mesh = box_mesh(nx, ny, nz, (0.0, 1.0), (0.0, 0.25), (0.0, 0.25), jitter=jitter, seed=seed)
-    mat = assemble_q1(mesh)
+    cells = len(mesh.cells)  # full C3: row ranges of ~0.5M cells keep host memory ~10x lower
+    mat = assemble_q1(mesh) if cells <= (1 << 21) else assemble_q1_rows(mesh, slabs=-(-cells // (1 << 19)))
     left = mesh.points[:, 0] < 0.5
     rho = np.where(left, 1.0, 0.125)
     p = np.where(left, 1.0, 0.1)

@@ -91,3 +91,15 @@ def test_c4_extruded_cylinder_geometry():
     assert np.bincount(card).argmax() == 27 and card.max() <= 33
     assert len(ps.boundary.inflow_nodes) > 0 and len(ps.boundary.slip_nodes) > 0
     assert np.allclose(np.linalg.norm(ps.boundary.slip_normals, axis=1), 1.0)
+
+
+@pytest.mark.parametrize("slabs", [1, 3, 7])
+def test_row_range_assembly_is_bitwise_identical(slabs):
+    """assemble_q1_rows (used for the full C3 box) equals assemble_q1 bit for bit."""
+    meshes = [P.box_mesh(9, 5, 4, jitter=0.2, seed=3), P.extrude(P.disc_channel_mesh(10), 3), P.disc_channel_mesh(20),
+              P.rectangle_mesh(7, 5)]
+    for mesh in meshes:
+        a = P.assemble_q1(mesh)
+        b = P.assemble_q1_rows(mesh, slabs=slabs)
+        for f in ("indptr", "indices", "m", "c", "m_lumped", "inv_m"):
+            assert np.array_equal(getattr(a, f), getattr(b, f)), f
