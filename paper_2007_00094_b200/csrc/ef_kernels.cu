@@ -117,6 +117,19 @@ __device__ __forceinline__ void load_node(const double* __restrict__ U, int64_t 
   for (int k = 0; k < NV; ++k) out[k] = U[k * NP + i];
 }
 
+// L2 prefetch of the streamed per-edge index arrays about one wave of resident
+// threads ahead (k_edge_lim: EF_PF_LIM edges; k_edge_visc: EF_PF_DIST, 0 = off):
+// those loads miss L2 (read once per launch), and their DRAM latency otherwise
+// heads every edge's dependent load chain.  Measured: limiter passes -2% (2D)
+// / -3% (3D); k_edge_visc +3% in 3D (issue-bound), so off there.
+#ifndef EF_PF_DIST
+#define EF_PF_DIST 0
+#endif
+#ifndef EF_PF_LIM
+#define EF_PF_LIM 131072
+#endif
+__device__ __forceinline__ void pf_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
 // ---------------------------------------------------------------- state I/O
 template <int D>
 __global__ void k_gather_state(Layout m, const double* __restrict__ Uaos,
@@ -181,10 +194,19 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_EDGE(D), D)) k_edge
   const int e = blockIdx.x * EF_TPB_D(D) + threadIdx.x;
   if (reset_tau && e == 0) *w.tau_min_bits = 0x7ff0000000000000ULL;
   if (e >= m.n_edges) return;
+  const int NP = (int)m.NP, NE = (int)m.n_edges;
+  if (EF_PF_DIST > 0 && e + EF_PF_DIST < NE) {
+    const int f = e + EF_PF_DIST;
+    pf_l2(m.edges + f);
+    pf_l2(m.edge_j + f);
+    pf_l2(m.edge_pt + f);
+#pragma unroll
+    for (int a = 0; a < 2 * (D + 1); ++a) pf_l2(m.egeo + (size_t)a * NE + f);
+  }
   const int p = m.edges[e];
   const int i = (int)fdiv((uint32_t)p, m.slab) * 32 + (p & 31);
   const int j = m.edge_j[e];
-  const int NP = (int)m.NP, NE = (int)m.n_edges;
+  const int pt = m.edge_pt[e];
   double Ui[NV], Uj[NV], nij[D], nji[D];
   load_node<NV>(U, NP, i, Ui);
   load_node<NV>(U, NP, j, Uj);
@@ -200,7 +222,7 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_EDGE(D), D)) k_edge
   // the lower-triangle entry of row j, written straight to its slot (the
   // reference's mirror, stepper.py:427-434, without a gather)
   w.d[p] = dv;
-  w.d[m.edge_pt[e]] = dv;
+  w.d[pt] = dv;
   if (bad) atomicOr(w.err, ERR_PROJECT);
 }
 
@@ -560,16 +582,11 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_LOW(D), D)) k_low_o
 // reference's, in its order; each side uses its own m_ij / m_ji, alpha sum and
 // factor, so nothing assumes symmetry that the inputs might not have.
 template <int D, bool FIRST>
-__global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ELIM(D, FIRST), D)) k_edge_lim(Layout m, Gas g,
-                                                                        const double* __restrict__ U,
-                                                                        Work w, StageParams sp, int q) {
+__device__ __forceinline__ void edge_lim_one(const Layout& m, const Gas& g, const double* __restrict__ U,
+                                             const Work& w, const StageParams& sp, int q, int p, int j,
+                                             int pt) {
   constexpr int NV = D + 2;
-  const int e = blockIdx.x * EF_TPB_D(D) + threadIdx.x;
-  if (e >= m.n_edges) return;
-  const int p = m.edges[e];
   const int i = (int)fdiv((uint32_t)p, m.slab) * 32 + (p & 31);
-  const int j = m.edge_j[e];
-  const int pt = m.edge_pt[e];
   const int NP = (int)m.NP;
   const size_t NPL = (size_t)NP * m.L;
   double Pi[NV], Pj[NV];
@@ -620,6 +637,22 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ELIM(D, FIRST), D))
   double* __restrict__ ml = last ? w.ml2 : w.ml;
   ml[p] = npmin(li, lj);   // row i: np.minimum(l_ij, l_ji)
   ml[pt] = npmin(lj, li);  // row j: np.minimum(l_ji, l_ij)
+}
+
+template <int D, bool FIRST>
+__global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ELIM(D, FIRST), D)) k_edge_lim(Layout m, Gas g,
+                                                                        const double* __restrict__ U,
+                                                                        Work w, StageParams sp, int q) {
+  const int e = blockIdx.x * EF_TPB_D(D) + threadIdx.x;
+  const int NE = (int)m.n_edges;
+  if (e >= NE) return;
+  if (EF_PF_LIM > 0 && e + EF_PF_LIM < NE) {
+    const int f = e + EF_PF_LIM;
+    pf_l2(m.edges + f);
+    pf_l2(m.edge_j + f);
+    pf_l2(m.edge_pt + f);
+  }
+  edge_lim_one<D, FIRST>(m, g, U, w, sp, q, m.edges[e], m.edge_j[e], m.edge_pt[e]);
 }
 
 // step5 (non-final pass): U_next_i += lam_i * sum_s min(l) P in slot order
