@@ -535,6 +535,8 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
   EF_TRY(h->alloc(&w.ml, NPL));
   EF_TRY(h->alloc(&w.ml2, NPL));
   EF_TRY(h->alloc(&w.P, (size_t)NV * NPL));
+  EF_TRY(h->alloc(&w.lz, NP));
+  EF_CUDA(cudaMemset(w.lz, 0, sizeof(double) * NP));
   EF_TRY(h->alloc(&w.tau_min_bits, 1));
   EF_TRY(h->alloc(&w.tau, 1));
   EF_TRY(h->alloc(&w.err, 1));
@@ -725,7 +727,7 @@ static int run_stage(Driver& d, const std::vector<StageIO>& io, StageParams sp) 
     for (int p = 0; p + 1 < t->passes; ++p) {
       EF_TRY(produce([&](ef_solver* h, const StageIO& x, ef::RowSet rs) {
         ef::launch_row_upd(h->dim, h->lay, h->gas, x.U, h->w, sp, rs, st);
-      }, {fld(&Work::Unext, NV)}));
+      }, {fld(&Work::Unext, NV), fld(&Work::lz, 1)}));
       each([&](ef_solver* h, const StageIO& x) { ef::launch_edge_lim(h->dim, h->lay, h->gas, x.U, h->w, sp, p + 1, st); });
     }
     EF_TRY(mark(t, 6));
@@ -866,6 +868,7 @@ static int finish(Driver& d, int out_buf, double* tau_used) {
   }
   if (err & ef::ERR_TAU_UNBOUNDED) return fail(EF_ERR_TAU_UNBOUNDED, "constant field, the time step bound is unbounded");
   if (err & ef::ERR_PROJECT) return fail(EF_ERR_INADMISSIBLE, "projected state requires rho > 0 and p > 0");
+  if (err & ef::ERR_NONFINITE_P) return fail(EF_ERR_INADMISSIBLE, "non-finite correction flux P_ij (overflow)");
   if (err & ef::ERR_BAD_STATE) {
     int64_t orig = -1;  // original id of the smallest inadmissible CM id (any local copy)
     for (ef_solver* h : d.hs)
@@ -1166,6 +1169,7 @@ int ef_debug_fetch(ef_solver* h, int32_t which, int32_t which_pass, double* out)
     case 6: return node_field(h->w.phi, 1);
     case 7: return node_field(h->Ubuf[h->cur], NV);
     case 8: return node_field(h->w.Unext, NV);
+    case 9: return slot_field(h->w.ml);  // min(l_ij, l_ji) of the last non-final pass
   }
   return fail(EF_ERR_ARG, "unknown field");
 }

@@ -125,6 +125,10 @@ __device__ __forceinline__ void load_node(const double* __restrict__ U, int64_t 
 #ifndef EF_PF_DIST
 #define EF_PF_DIST 0
 #endif
+// P = 0 shortcut of the limiter passes after the first (EF_ZSKIP, default on)
+#ifndef EF_ZSKIP
+#define EF_ZSKIP 1
+#endif
 #ifndef EF_PF_LIM
 #define EF_PF_LIM 131072
 #endif
@@ -612,11 +616,37 @@ __device__ __forceinline__ void edge_lim_one(const Layout& m, const Gas& g, cons
     }
   } else {
     const double gi = 1.0 - w.ml[p], gj = 1.0 - w.ml[pt];
+    if (EF_ZSKIP && gi == 0.0 && gj == 0.0) {
+      // min(l) of the previous pass was 1: P rescales to (+-)0 on both sides
+      // (P is finite, k_edge_lim<FIRST> checks), and limiter(U^L, +-0, bounds)
+      // depends on the row alone -- k_row_upd stored it as lz (the sign of a
+      // zero P cannot reach the result: V = U^L exactly, and the Newton branch
+      // is never taken with P = 0).  The P loads, the two limiter evaluations
+      // and (last pass) the P store are skipped; k_final skips the same slots.
+      if (q != sp.passes - 1) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+          w.P[(size_t)k * NPL + p] = 0.0;
+          w.P[(size_t)k * NPL + pt] = 0.0;
+        }
+      }
+      const double li = w.lz[i], lj = w.lz[j];
+      double* __restrict__ mo = q == sp.passes - 1 ? w.ml2 : w.ml;
+      mo[p] = npmin(li, lj);
+      mo[pt] = npmin(lj, li);
+      return;
+    }
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
       Pi[k] = w.P[(size_t)k * NPL + p] * gi;
       Pj[k] = w.P[(size_t)k * NPL + pt] * gj;
     }
+  }
+  if (FIRST && sp.passes >= 2) {  // the later passes' P = 0 shortcut assumes finite P
+    bool fin = true;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) fin = fin && finite(Pi[k]) && finite(Pj[k]);
+    if (!fin) atomicOr(w.err, ERR_NONFINITE_P);
   }
   // The last pass q >= 1 leaves P_(q-1) and min(l) of pass q-1 in place: k_final
   // forms the same product P_(q-1) (1 - min l) itself, which saves the largest
@@ -681,8 +711,18 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_PASS(D), D)) k_row_
     for (int k = 0; k < NV; ++k) upd[k] = upd[k] + ml * w.P[(size_t)k * NPL + p];
   }
   const double lam = m.lam[i];
+  double Un[NV];
 #pragma unroll
-  for (int k = 0; k < NV; ++k) w.Unext[k * NP + i] = w.Unext[k * NP + i] + lam * upd[k];
+  for (int k = 0; k < NV; ++k) {
+    Un[k] = w.Unext[k * NP + i] + lam * upd[k];
+    w.Unext[k * NP + i] = Un[k];
+  }
+  if (EF_ZSKIP) {  // the next pass's factor of the rows' P = 0 edges (see k_edge_lim)
+    double z[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) z[k] = 0.0;
+    w.lz[i] = limiter<D>(Un, z, w.bounds[i], w.bounds[NP + i], w.bounds[2 * NP + i], sp.newton, g);
+  }
 }
 
 template <int D>
@@ -709,8 +749,11 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_FINAL(D), D)) k_fin
     for (int s = 0; s < card; ++s) {
       if (s == dg) continue;
       const int p = base + s * 32;
-      const double ml = w.ml2[p];
       const double gp = rescale ? 1.0 - w.ml[p] : 1.0;
+      // gp == 0: the term is ml2 * (P * 0) = +-0 (P finite), and adding +-0 to a
+      // sum that starts at +0 never changes it (it cannot become -0)
+      if (EF_ZSKIP && gp == 0.0) continue;
+      const double ml = w.ml2[p];
 #pragma unroll
       for (int k = 0; k < NV; ++k) {
         const double Pk = rescale ? w.P[(size_t)k * NPL + p] * gp : w.P[(size_t)k * NPL + p];

@@ -80,6 +80,8 @@ struct Work {
   double* ml;        // [NP*L] min(l_ij, l_ji) of the current non-final limiter pass
   double* ml2;       // [NP*L] min(l_ij, l_ji) of the last limiter pass
   double* P;         // [NV][NP*L] correction fluxes P_ij, rescaled in place per pass
+  double* lz;        // [NP] limiter(U^L_i, P = 0, bounds_i) after a non-final update: the
+                     // factor of every edge whose previous min(l) was 1 (P then rescales to 0)
   unsigned long long* tau_min_bits;  // CFL min over owned rows
   double* tau;       // tau of the current RK step / Euler step
   int* err;          // bit0 projection/entropy, bit1 inadmissible result, bit2 tau unbounded
@@ -87,7 +89,7 @@ struct Work {
 };
 
 enum TauMode { TAU_CFL = 0, TAU_GIVEN = 1, TAU_DEVICE = 2 };
-enum ErrBits { ERR_PROJECT = 1, ERR_BAD_STATE = 2, ERR_TAU_UNBOUNDED = 4 };
+enum ErrBits { ERR_PROJECT = 1, ERR_BAD_STATE = 2, ERR_TAU_UNBOUNDED = 4, ERR_NONFINITE_P = 8 };
 
 struct StageParams {
   int tau_mode;

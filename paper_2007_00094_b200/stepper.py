@@ -292,13 +292,13 @@ class Solver:
         _lib.load().ef_phase_times(self._h, s.ctypes.data)
         return {name: float(v) for name, v in zip(STEP_NAMES, s)}
 
-    _FIELDS = {"d": 0, "alpha": 1, "R": 2, "bounds": 3, "l": 4, "eor": 5, "phi": 6, "U": 7, "U_next": 8}
+    _FIELDS = {"d": 0, "alpha": 1, "R": 2, "bounds": 3, "l": 4, "eor": 5, "phi": 6, "U": 7, "U_next": 8, "l_prev": 9}
 
     def fetch(self, which: str, pass_index: int = 0) -> np.ndarray:
         """Internal arrays (rows = local rows in global CM order; slots in stencil order)."""
         n, L, nv = self.n_local, self.pad_width, self.nvar
         shapes = {"d": (n, L), "alpha": (n,), "R": (n, nv), "bounds": (n, 3), "l": (n, L),
-                  "eor": (n,), "phi": (n,), "U": (n, nv), "U_next": (n, nv)}
+                  "eor": (n,), "phi": (n,), "U": (n, nv), "U_next": (n, nv), "l_prev": (n, L)}
         out = np.empty(shapes[which])
         _raise(_lib.load().ef_debug_fetch(self._h, self._FIELDS[which], int(pass_index), out.ctypes.data))
         return out
