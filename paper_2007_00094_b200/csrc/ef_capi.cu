@@ -140,7 +140,12 @@ struct ef_solver {
     int err;
     int pad;
     unsigned long long bad;
+    unsigned long long n_same[ef::kSameSlots];
   }* rb = nullptr;
+  // identical-state shortcuts: on while the last synchronised step saw at least
+  // 2% identical-state edges (EF_UNIFORM=0/1 forces them off/on)
+  bool uni_on = true;
+  int uni_force = -1;
   double tau_last = 0.0;
   int64_t bad_node = -1;
   bool timing = false;
@@ -154,10 +159,10 @@ struct ef_solver {
   // ~25 kernels and memsets of an RK step.  Keyed by everything the captured
   // launches depend on; a few entries cover the rotating U buffers.
   struct GraphKey {
-    int rk3, cur, has_tau;
+    int rk3, cur, has_tau, uni;
     double tau, tau_max;
     bool operator==(const GraphKey& o) const {
-      return rk3 == o.rk3 && cur == o.cur && has_tau == o.has_tau &&
+      return rk3 == o.rk3 && cur == o.cur && has_tau == o.has_tau && uni == o.uni &&
              std::memcmp(&tau, &o.tau, sizeof tau) == 0 && std::memcmp(&tau_max, &o.tau_max, sizeof tau_max) == 0;
     }
   };
@@ -535,12 +540,16 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
   EF_TRY(h->alloc(&w.ml, NPL));
   EF_TRY(h->alloc(&w.ml2, NPL));
   EF_TRY(h->alloc(&w.P, (size_t)NV * NPL));
+  EF_TRY(h->alloc(&w.nonuni, NP));
+  EF_CUDA(cudaMemset(w.nonuni, 1, NP));
   EF_TRY(h->alloc(&w.lz, NP));
   EF_CUDA(cudaMemset(w.lz, 0, sizeof(double) * NP));
   EF_TRY(h->alloc(&w.tau_min_bits, 1));
   EF_TRY(h->alloc(&w.tau, 1));
   EF_TRY(h->alloc(&w.err, 1));
   EF_TRY(h->alloc(&w.bad_gid, 1));
+  EF_TRY(h->alloc(&w.n_same, ef::kSameSlots));
+  EF_CUDA(cudaMemset(w.n_same, 0, sizeof(unsigned long long) * ef::kSameSlots));
   EF_CUDA(cudaMemset(w.d, 0, sizeof(double) * NPL));
   EF_CUDA(cudaMemset(w.ml, 0, sizeof(double) * NPL));
   EF_CUDA(cudaMemset(w.ml2, 0, sizeof(double) * NPL));
@@ -707,10 +716,11 @@ static int run_stage(Driver& d, const std::vector<StageIO>& io, StageParams sp) 
   };
   EF_TRY(mark(t, 0));
   EF_TRY(mark(t, 1));  // step0 is fused into the previous stage's final kernel
-  each([&](ef_solver* h, const StageIO& x) { ef::launch_edge_visc(h->dim, h->lay, h->gas, x.U, h->w, want_tau, st); });
+  each([&](ef_solver* h, const StageIO& x) { ef::launch_edge_visc(h->dim, h->lay, h->gas, x.U, h->w, want_tau, sp.uni != 0,
+                                                                   sp.tau_mode != ef::TAU_DEVICE, st); });
   EF_TRY(mark(t, 2));
   EF_TRY(produce([&](ef_solver* h, const StageIO& x, ef::RowSet rs) {
-    ef::launch_row_visc(h->dim, h->lay, h->gas, x.U, h->w, want_tau, rs, st);
+    ef::launch_row_visc(h->dim, h->lay, h->gas, x.U, h->w, want_tau, sp.uni != 0, rs, st);
   }, {fld(&Work::alpha, 1)}));
   if (want_tau) EF_TRY(allreduce_tau(d, st));
   EF_TRY(mark(t, 3));
@@ -760,6 +770,7 @@ static StageParams stage_params(ef_solver* h, int mode, double tau, double tau_m
   sp.newton = h->newton;
   sp.passes = h->passes;
   sp.rk_a = rk_a;
+  sp.uni = h->uni_on ? 1 : 0;
   return sp;
 }
 
@@ -767,6 +778,7 @@ static int reset_flags(Driver& d) {
   for (ef_solver* h : d.hs) {
     EF_CUDA(cudaMemsetAsync(h->w.err, 0, sizeof(int), h->st));
     EF_CUDA(cudaMemsetAsync(h->w.bad_gid, 0xff, sizeof(unsigned long long), h->st));
+    EF_CUDA(cudaMemsetAsync(h->w.n_same, 0, sizeof(unsigned long long) * ef::kSameSlots, h->st));
   }
   return EF_OK;
 }
@@ -807,7 +819,8 @@ static int step_async(Driver& d, bool rk3, int32_t has_tau, double tau, double t
     return rk3 ? rk3_async(d, has_tau, tau, tau_max, out_buf) : euler_async(d, has_tau, tau, tau_max, out_buf);
   };
   if (!h->use_graphs || h->timing || d.group || h->nranks > 1) return body();
-  const ef_solver::GraphKey key{rk3 ? 1 : 0, h->cur, has_tau ? 1 : 0, has_tau ? tau : 0.0, tau_max};
+  const ef_solver::GraphKey key{rk3 ? 1 : 0, h->cur, has_tau ? 1 : 0, h->uni_on ? 1 : 0, has_tau ? tau : 0.0,
+                                tau_max};
   for (auto& g : h->graphs)
     if (g.key == key) {
       g.used = ++h->graph_clock;
@@ -846,6 +859,8 @@ static int readback(ef_solver* h) {
   EF_CUDA(cudaMemcpyAsync(&h->rb->tau, h->w.tau, sizeof(double), cudaMemcpyDeviceToHost, h->st));
   EF_CUDA(cudaMemcpyAsync(&h->rb->err, h->w.err, sizeof(int), cudaMemcpyDeviceToHost, h->st));
   EF_CUDA(cudaMemcpyAsync(&h->rb->bad, h->w.bad_gid, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
+  EF_CUDA(cudaMemcpyAsync(h->rb->n_same, h->w.n_same, sizeof(unsigned long long) * ef::kSameSlots,
+                          cudaMemcpyDeviceToHost, h->st));
   EF_CUDA(cudaStreamSynchronize(h->st));
   EF_CUDA(cudaGetLastError());
   return EF_OK;
@@ -880,6 +895,14 @@ static int finish(Driver& d, int out_buf, double* tau_used) {
   for (ef_solver* h : d.hs) {
     h->cur = out_buf;
     h->tau_last = h0->rb->tau;
+    if (h->uni_force >= 0) {
+      h->uni_on = h->uni_force != 0;
+    } else {  // counted over the step's stages: uniform rows (on) or identical-state edges (off)
+      unsigned long long c = 0;
+      for (int k = 0; k < ef::kSameSlots; ++k) c += h->rb->n_same[k];
+      const double base = h->uni_on ? (double)h->n_owned : (double)h->lay.n_edges;
+      h->uni_on = 8.0 * (double)c >= 0.02 * base;  // 1-in-8 block sample of the first stage
+    }
   }
   if (tau_used) *tau_used = h0->rb->tau;
   return EF_OK;
@@ -997,6 +1020,9 @@ int ef_create(const ef_matrices* mat, const ef_params* prm, const ef_boundary* b
   {
     const char* ge = std::getenv("EF_GRAPHS");
     h->use_graphs = !(ge && ge[0] == '0');
+    const char* ue = std::getenv("EF_UNIFORM");
+    if (ue && (ue[0] == '0' || ue[0] == '1')) h->uni_force = ue[0] - '0';
+    h->uni_on = h->uni_force != 0;
   }
   int rc = build(h, mat, bc, dist);
   if (rc != EF_OK) return bail(rc);

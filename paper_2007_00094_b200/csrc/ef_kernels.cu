@@ -125,6 +125,25 @@ __device__ __forceinline__ void load_node(const double* __restrict__ U, int64_t 
 #ifndef EF_PF_DIST
 #define EF_PF_DIST 0
 #endif
+// Rows whose whole stencil holds the row's own state (bitwise; w.nonuni == 0)
+// take exact closed forms in k_row_visc (alpha = 0), k_low_order (no neighbour
+// loads) and k_edge_lim's first pass (P = 0) -- EF_UNIFORM_ROWS, default on.
+#ifndef EF_UNIFORM_ROWS
+#define EF_UNIFORM_ROWS 1
+#endif
+// warp-aggregated count into one of kSameSlots counters (spread: no hot address)
+__device__ __forceinline__ void count_hits(bool hit, unsigned long long* slots) {
+  const unsigned act = __activemask(), hits = __ballot_sync(act, hit);
+  if ((threadIdx.x & 31) == (unsigned)(__ffs(act) - 1) && hits)
+    atomicAdd(slots + ((blockIdx.x * 7 + (threadIdx.x >> 5)) & (kSameSlots - 1)), (unsigned long long)__popc(hits));
+}
+template <int N>
+__device__ __forceinline__ bool all_finite(const double* x) {
+  bool ok = true;
+#pragma unroll
+  for (int k = 0; k < N; ++k) ok = ok && finite(x[k]);
+  return ok;
+}
 // P = 0 shortcut of the limiter passes after the first (EF_ZSKIP, default on)
 #ifndef EF_ZSKIP
 #define EF_ZSKIP 1
@@ -175,6 +194,7 @@ __device__ __forceinline__ void nodal_one(const double* Ui, const Gas& g, Work& 
 #pragma unroll
   for (int a = 0; a < D; ++a) w.vp[a * NP + i] = qdiv(Ui[1 + a], rr);  // physics.py:157
   w.vp[D * NP + i] = g.gm1 * eps;                                        // physics.py:94
+  w.nonuni[i] = 0;  // k_edge_visc of the stage marks rows with a differing neighbour
 }
 
 template <int D>
@@ -191,12 +211,12 @@ __global__ void k_nodal(Layout m, Gas g, const double* __restrict__ U, Work w, i
 // slot after the diagonal; stepper.py:211, 415).  The edge list holds SELL
 // positions in ascending order, so a warp reads 32 consecutive positions of
 // one slot row (coalesced) and the row / slot are recovered from the position.
-template <int D>
+template <int D, bool UNI>
 __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_EDGE(D), D)) k_edge_visc(Layout m, Gas g, const double* __restrict__ U,
-                                                   Work w, int reset_tau) {
+                                                   Work w, int flags) {  // 1: reset the CFL bound, 2: count
   constexpr int NV = D + 2;
   const int e = blockIdx.x * EF_TPB_D(D) + threadIdx.x;
-  if (reset_tau && e == 0) *w.tau_min_bits = 0x7ff0000000000000ULL;
+  if ((flags & 1) && e == 0) *w.tau_min_bits = 0x7ff0000000000000ULL;
   if (e >= m.n_edges) return;
   const int NP = (int)m.NP, NE = (int)m.n_edges;
   if (EF_PF_DIST > 0 && e + EF_PF_DIST < NE) {
@@ -221,13 +241,20 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_EDGE(D), D)) k_edge
   }
   const double norm_ij = m.egeo[(size_t)D * NE + e], norm_ji = m.egeo[(size_t)(2 * D + 1) * NE + e];
   bool bad = false;
-  const double dv = d_ij_geo<D>(Ui, Uj, nij, norm_ij, nji, norm_ji, g, bad);
+  const bool same = same_state<NV>(Ui, Uj);
+  if (UNI && !same) {
+    w.nonuni[i] = 1;
+    w.nonuni[j] = 1;
+  }
+  const double dv = d_ij_geo<D>(Ui, Uj, nij, norm_ij, nji, norm_ji, g, bad, UNI && same);
   // d is symmetric by construction (riemann.py:139-142): the value is also
   // the lower-triangle entry of row j, written straight to its slot (the
   // reference's mirror, stepper.py:427-434, without a gather)
   w.d[p] = dv;
   w.d[pt] = dv;
   if (bad) atomicOr(w.err, ERR_PROJECT);
+  // with the shortcuts off: sample (1 block in 8, first stage) how many would apply
+  if (!UNI && (flags & 2) && (blockIdx.x & 7) == 0) count_hits(same, w.n_same);
 }
 
 // ---------------------------------------------------------------- step1b + step2
@@ -305,7 +332,7 @@ __device__ __forceinline__ void node_flux(const double* Ui, const Work& w, int N
 
 template <int D>
 __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ROW(D), D)) k_row_visc(Layout m, Gas g, const double* __restrict__ U,
-                                                  Work w, int want_tau, RowSet rs) {
+                                                  Work w, int want_tau, int uni_on, RowSet rs) {
   constexpr int NV = D + 2;
   const int t0 = blockIdx.x * EF_TPB_D(D) + threadIdx.x;
   const bool act = t0 < rs.n;
@@ -326,6 +353,12 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ROW(D), D)) k_row_v
     double A = 0.0, B[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) B[k] = 0.0;
+    // Uniform stencil (every neighbour's state is U_i bit for bit, hence the
+    // same eor and flux): each slot adds (+0) * x = +-0 to sums that start at
+    // +0, which leaves them +0 -- the loop is skipped (finite values assumed,
+    // checked), and alpha_i = 0 follows from the unchanged tail.
+    const bool uni = EF_UNIFORM_ROWS && uni_on && !w.nonuni[i] && all_finite<NV>(Ui) &&
+                     all_finite<NV * D>(&fi[0][0]) && finite(eor_i);
     // one slot j != i (j == i contributes exact zeros), in slot order
     auto slot = [&](const double* Uj, const double* cc, double eor_j, const double* vpj) {
       double mc = 0.0;
@@ -368,8 +401,8 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ROW(D), D)) k_row_v
         for (int a = 0; a < NQ; ++a) vpj[a] = buf[st][NV + 1 + D + a][t];
         slot(Uj, cc, buf[st][NV][t], vpj);
       };
-      row_pipe(m.col, base, card, dg, issue, body);
-    } else {
+      if (!uni) row_pipe(m.col, base, card, dg, issue, body);
+    } else if (!uni) {
       EF_UNROLL_ROW
       for (int s = 0; s < card; ++s) {  // indicator: sequential over slots
         if (s == dg) continue;
@@ -495,6 +528,11 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_LOW(D), D)) k_low_o
   double rmin = Ui[0], rmax = Ui[0], pmin = w.phi[i];
   const int card = m.card[i], dg = m.diag[i];
   const int base = sidx32(i, 0, L);
+  // Uniform stencil: dU = +0 and f_j - f_i = +0 in every slot, so each slot adds
+  // +0 to sumL / sumR and leaves the bounds at (rho_i, rho_i, phi_i) (the bar
+  // state is 0.5 (rho_i + rho_i) - (+0) = rho_i): the loop is skipped.
+  const bool uni = EF_UNIFORM_ROWS && sp.uni && !w.nonuni[i] && all_finite<NV>(Ui) &&
+                   all_finite<NV * D>(&fi[0][0]) && finite(pmin) && fabs(Ui[0]) < 1e300;
   // one slot j != i of the row, in slot order (stepper.py:441-454)
   auto slot = [&](const double* Uj, const double* cc, double dv, double alj, double phij, const double* vpj) {
     double fj[NV][D];
@@ -548,8 +586,8 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_LOW(D), D)) k_low_o
       for (int a = 0; a < NQ; ++a) vpj[a] = buf[st][NV + 3 + D + a][t];
       slot(Uj, cc, buf[st][NV + 2 + D][t], buf[st][NV][t], buf[st][NV + 1][t], vpj);
     };
-    row_pipe(m.col, base, card, dg, issue, body);
-  } else {
+    if (!uni) row_pipe(m.col, base, card, dg, issue, body);
+  } else if (!uni) {
     EF_UNROLL_LOW
     for (int s = 0; s < card; ++s) {
       if (s == dg) continue;
@@ -573,6 +611,23 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_LOW(D), D)) k_low_o
   w.bounds[i] = rmin;
   w.bounds[NP + i] = rmax;
   w.bounds[2 * NP + i] = pmin;
+  if (EF_UNIFORM_ROWS && sp.uni && sp.passes > 0) {
+    // first-pass factor of the edges between two uniform rows (their P is +-0,
+    // R_i = R_j = +0 and U_j = U_i): limiter(U^L_i, 0, bounds_i); NaN = no shortcut
+    double lz = __longlong_as_double(0x7ff8000000000000LL);
+    if (uni) {
+      double Un[NV], z[NV];
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        Un[k] = Ui[k] + (fac * sumL[k]);
+        z[k] = 0.0;
+      }
+      lz = limiter<D>(Un, z, rmin, rmax, pmin, sp.newton, g);
+    }
+    w.lz[i] = lz;
+  }
+  // uniform rows (keep the shortcuts on): sampled like k_edge_visc's count
+  if (EF_UNIFORM_ROWS && sp.uni && sp.tau_mode != TAU_DEVICE && (blockIdx.x & 7) == 0) count_hits(uni, w.n_same);
 }
 
 // ---------------------------------------------------------------- steps 4-6
@@ -585,7 +640,7 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_LOW(D), D)) k_low_o
 // kernels then only stream their own slots.  Every operation is the
 // reference's, in its order; each side uses its own m_ij / m_ji, alpha sum and
 // factor, so nothing assumes symmetry that the inputs might not have.
-template <int D, bool FIRST>
+template <int D, bool FIRST, bool UNI>
 __device__ __forceinline__ void edge_lim_one(const Layout& m, const Gas& g, const double* __restrict__ U,
                                              const Work& w, const StageParams& sp, int q, int p, int j,
                                              int pt) {
@@ -594,6 +649,26 @@ __device__ __forceinline__ void edge_lim_one(const Layout& m, const Gas& g, cons
   const int NP = (int)m.NP;
   const size_t NPL = (size_t)NP * m.L;
   double Pi[NV], Pj[NV];
+  if (FIRST && UNI && EF_UNIFORM_ROWS) {
+    // both rows took k_low_order's uniform shortcut (lz not NaN; owned rows):
+    // R_i = R_j = +0 and U_j = U_i, so P_ij and P_ji are +-0 (stored as +0, the
+    // sign of a zero P never reaches a result) and each limiter is the row's lz
+    const int no = (int)m.n_owned;
+    if (i < no && j < no) {
+      const double li = w.lz[i], lj = w.lz[j];
+      if (li == li && lj == lj) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+          w.P[(size_t)k * NPL + p] = 0.0;
+          w.P[(size_t)k * NPL + pt] = 0.0;
+        }
+        double* __restrict__ mo = sp.passes == 1 ? w.ml2 : w.ml;
+        mo[p] = npmin(li, lj);
+        mo[pt] = npmin(lj, li);
+        return;
+      }
+    }
+  }
   if (FIRST) {  // q == 0
     const double tau = *w.tau;
     const double imi = m.inv_m[i], imj = m.inv_m[j];
@@ -669,7 +744,7 @@ __device__ __forceinline__ void edge_lim_one(const Layout& m, const Gas& g, cons
   ml[pt] = npmin(lj, li);  // row j: np.minimum(l_ji, l_ij)
 }
 
-template <int D, bool FIRST>
+template <int D, bool FIRST, bool UNI>
 __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ELIM(D, FIRST), D)) k_edge_lim(Layout m, Gas g,
                                                                         const double* __restrict__ U,
                                                                         Work w, StageParams sp, int q) {
@@ -682,7 +757,7 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ELIM(D, FIRST), D))
     pf_l2(m.edge_j + f);
     pf_l2(m.edge_pt + f);
   }
-  edge_lim_one<D, FIRST>(m, g, U, w, sp, q, m.edges[e], m.edge_j[e], m.edge_pt[e]);
+  edge_lim_one<D, FIRST, UNI>(m, g, U, w, sp, q, m.edges[e], m.edge_j[e], m.edge_pt[e]);
 }
 
 // step5 (non-final pass): U_next_i += lam_i * sum_s min(l) P in slot order
@@ -876,29 +951,40 @@ void launch_nodal(int dim, const Layout& m, const Gas& g, const double* U, Work 
   EF_DISPATCH(dim, k_nodal, grid_for(hi - lo), m, g, U, w, lo, hi);
 }
 void launch_edge_visc(int dim, const Layout& m, const Gas& g, const double* U, Work w,
-                      bool reset_tau, cudaStream_t st) {
-  EF_DISPATCH_STAGE(dim, k_edge_visc, m.n_edges > 0 ? m.n_edges : 1, m, g, U, w, reset_tau ? 1 : 0);
+                      bool reset_tau, bool uni, bool count, cudaStream_t st) {
+  const int64_t n = m.n_edges > 0 ? m.n_edges : 1;
+  const int r = (reset_tau ? 1 : 0) | (count ? 2 : 0);
+  if (dim == 2) {
+    if (uni) k_edge_visc<2, true><<<grid_d(2, n), EF_TPB2, 0, st>>>(m, g, U, w, r);
+    else k_edge_visc<2, false><<<grid_d(2, n), EF_TPB2, 0, st>>>(m, g, U, w, r);
+  } else {
+    if (uni) k_edge_visc<3, true><<<grid_d(3, n), EF_TPB3, 0, st>>>(m, g, U, w, r);
+    else k_edge_visc<3, false><<<grid_d(3, n), EF_TPB3, 0, st>>>(m, g, U, w, r);
+  }
 }
 void launch_row_visc(int dim, const Layout& m, const Gas& g, const double* U, Work w,
-                     bool want_tau, RowSet rs, cudaStream_t st) {
-  EF_DISPATCH_STAGE(dim, k_row_visc, rs.n > 0 ? rs.n : 1, m, g, U, w, want_tau ? 1 : 0, rs);
+                     bool want_tau, bool uni, RowSet rs, cudaStream_t st) {
+  EF_DISPATCH_STAGE(dim, k_row_visc, rs.n > 0 ? rs.n : 1, m, g, U, w, want_tau ? 1 : 0, uni ? 1 : 0, rs);
 }
 void launch_low_order(int dim, const Layout& m, const Gas& g, const double* U, Work w,
                       StageParams sp, RowSet rs, cudaStream_t st) {
   EF_DISPATCH_STAGE(dim, k_low_order, rs.n > 0 ? rs.n : 1, m, g, U, w, sp, rs);
 }
+template <int D>
+static void edge_lim_launch(const Layout& m, const Gas& g, const double* U, Work w, StageParams sp, int q,
+                            cudaStream_t st) {
+  constexpr int tb = D == 3 ? EF_TPB3 : EF_TPB2;
+  const unsigned grid = grid_d(D, m.n_edges);
+  if (q > 0) k_edge_lim<D, false, false><<<grid, tb, 0, st>>>(m, g, U, w, sp, q);
+  else if (sp.uni) k_edge_lim<D, true, true><<<grid, tb, 0, st>>>(m, g, U, w, sp, q);
+  else k_edge_lim<D, true, false><<<grid, tb, 0, st>>>(m, g, U, w, sp, q);
+}
+
 void launch_edge_lim(int dim, const Layout& m, const Gas& g, const double* U, Work w,
                      StageParams sp, int q, cudaStream_t st) {
   if (m.n_edges == 0) return;
-  if (dim == 2) {
-    const unsigned grid = grid_d(2, m.n_edges);
-    if (q == 0) k_edge_lim<2, true><<<grid, EF_TPB2, 0, st>>>(m, g, U, w, sp, q);
-    else k_edge_lim<2, false><<<grid, EF_TPB2, 0, st>>>(m, g, U, w, sp, q);
-  } else {
-    const unsigned grid = grid_d(3, m.n_edges);
-    if (q == 0) k_edge_lim<3, true><<<grid, EF_TPB3, 0, st>>>(m, g, U, w, sp, q);
-    else k_edge_lim<3, false><<<grid, EF_TPB3, 0, st>>>(m, g, U, w, sp, q);
-  }
+  if (dim == 2) edge_lim_launch<2>(m, g, U, w, sp, q, st);
+  else edge_lim_launch<3>(m, g, U, w, sp, q, st);
 }
 void launch_row_upd(int dim, const Layout& m, const Gas& g, const double* U, Work w,
                     StageParams sp, RowSet rs, cudaStream_t st) {
@@ -964,7 +1050,7 @@ __global__ void k_eval_dij(Gas g, int64_t n, const double* __restrict__ Ui, cons
     nji[k] = norm_ji > 0.0 ? cji[q * D + k] / norm_ji : (k == 0 ? 1.0 : 0.0);
   }
   bool bd = false;
-  out[q] = d_ij_geo<D>(a, b, nij, norm_ij, nji, norm_ji, g, bd);
+  out[q] = d_ij_geo<D>(a, b, nij, norm_ij, nji, norm_ji, g, bd, same_state<NV>(a, b));
   bad[q] = bd ? 1 : 0;
 }
 

@@ -80,14 +80,19 @@ struct Work {
   double* ml;        // [NP*L] min(l_ij, l_ji) of the current non-final limiter pass
   double* ml2;       // [NP*L] min(l_ij, l_ji) of the last limiter pass
   double* P;         // [NV][NP*L] correction fluxes P_ij, rescaled in place per pass
+  uint8_t* nonuni;   // [NP] 1 if some stencil neighbour's state differs from the row's
+                     // (bitwise); set by k_edge_visc, cleared by step0 (k_final / k_nodal)
   double* lz;        // [NP] limiter(U^L_i, P = 0, bounds_i) after a non-final update: the
                      // factor of every edge whose previous min(l) was 1 (P then rescales to 0)
   unsigned long long* tau_min_bits;  // CFL min over owned rows
   double* tau;       // tau of the current RK step / Euler step
   int* err;          // bit0 projection/entropy, bit1 inadmissible result, bit2 tau unbounded
   unsigned long long* bad_gid;       // min global CM id of an inadmissible row
+  unsigned long long* n_same;        // [kSameSlots] spread counters since the last reset:
+                                     // identical-state edges (shortcuts off) or uniform rows (on)
 };
 
+constexpr int kSameSlots = 128;
 enum TauMode { TAU_CFL = 0, TAU_GIVEN = 1, TAU_DEVICE = 2 };
 enum ErrBits { ERR_PROJECT = 1, ERR_BAD_STATE = 2, ERR_TAU_UNBOUNDED = 4, ERR_NONFINITE_P = 8 };
 
@@ -99,6 +104,8 @@ struct StageParams {
   int newton;
   int passes;
   double rk_a;  // < 0: Uout = Unew; else Uout = U0 + rk_a * (Unew - U0)   (stepper.py:632,635)
+  int uni;      // identical-state shortcuts on (k_edge_visc marks rows; the row kernels and
+                // the first limiter pass use the marks); chosen per step by the host
 };
 
 // Owned rows a row kernel covers: [r0, r0 + n0) then [r2, r2 + n - n0).  The
@@ -125,10 +132,10 @@ void launch_nodal(int dim, const Layout& m, const Gas& g, const double* U, Work 
                   int64_t hi, cudaStream_t st);
 // step1a: d_ij on every upper edge (one thread per edge)
 void launch_edge_visc(int dim, const Layout& m, const Gas& g, const double* U, Work w,
-                      bool reset_tau, cudaStream_t st);
+                      bool reset_tau, bool uni, bool count, cudaStream_t st);
 // step1b+2: per owned row, indicator alpha, mirror of d, d_ii, CFL bound
 void launch_row_visc(int dim, const Layout& m, const Gas& g, const double* U, Work w,
-                     bool want_tau, RowSet rs, cudaStream_t st);
+                     bool want_tau, bool uni, RowSet rs, cudaStream_t st);
 void launch_low_order(int dim, const Layout& m, const Gas& g, const double* U, Work w,
                       StageParams sp, RowSet rs, cudaStream_t st);
 // steps 4-5: P (q = 0) and min(l_ij, l_ji) of limiter pass q, one thread per edge

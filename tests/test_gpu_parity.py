@@ -100,3 +100,43 @@ def test_gpu_random_fields_3d():
     mat = P.assemble_q1(P.box_mesh(6, 5, 4, periodic=(True, True, True)))
     U = P.random_state(np.random.default_rng(2024), mat.n, dim=3)
     _compare(mat, U, None, 3)
+
+
+def _blocky_state(rng, mat, dim, nblocks, negzero=True):
+    """Piecewise-constant random states: many edges join identical states (the
+    identical-state and zero-correction shortcuts), the rest are block interfaces;
+    some blocks at rest with -0 momentum components."""
+    U = np.empty((mat.n, dim + 2))
+    lab = rng.integers(0, nblocks, mat.n)
+    # spatially coherent labels: smooth the random labels along the node order
+    lab = np.repeat(lab[:: max(1, mat.n // (4 * nblocks))], max(1, mat.n // (4 * nblocks)))[: mat.n]
+    lab = np.concatenate([lab, np.zeros(mat.n - len(lab), dtype=lab.dtype)])
+    states = P.random_state(rng, nblocks, dim=dim)
+    if negzero:
+        states[0, 1:-1] = -0.0
+        states[1, 1] = -0.0
+    U[:] = states[lab]
+    return U
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_gpu_blocky_states_bitwise(dim):
+    rng = np.random.default_rng(77 + dim)
+    mesh = P.rectangle_mesh(40, 30, periodic=(True, True)) if dim == 2 else \
+        P.box_mesh(12, 10, 8, periodic=(True, True, True))
+    mat = P.assemble_q1(mesh)
+    U = _blocky_state(rng, mat, dim, 6)
+    for passes in (2, 3):
+        _compare(mat, U, None, 4, passes=passes)
+
+
+@pytest.mark.parametrize("mode", ["0", "1"])
+def test_gpu_identical_state_shortcuts_forced(mode, monkeypatch):
+    """The identical-state shortcuts forced off and on give the oracle's bits
+    (the default chooses per step from the count of identical-state edges)."""
+    monkeypatch.setenv("EF_UNIFORM", mode)
+    ps = P.mach3_disc(20, seed=5)
+    _compare(ps.matrices, ps.U0, ps.boundary, 6)
+    rng = np.random.default_rng(5)
+    mat = P.assemble_q1(P.box_mesh(10, 8, 6, periodic=(True, True, True)))
+    _compare(mat, _blocky_state(rng, mat, 3, 5), None, 3)
