@@ -217,6 +217,27 @@ def run_ours(args, rank, world, local_rank):
     value = node_updates / (ms * 1e-3)
     ms_per_step = ms / args.steps
 
+    # the same steps with the identical-state shortcuts forced off:
+    # how much of `value` comes from uniform regions of the flow
+    general = None
+    if not dist:
+        gsteps = max(1, args.steps // 4)
+        solver.set_uniform_shortcuts(0)
+        for _ in range(2):
+            solver.ssp_rk3_step_async()
+        solver.sync()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(gsteps):
+            solver.ssp_rk3_step_async()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        solver.sync()
+        gms = e0.elapsed_time(e1)
+        solver.set_uniform_shortcuts(-1)
+        general = {"value": n_nodes * 3 * gsteps / (gms * 1e-3), "steps": gsteps,
+                   "note": "identical-state shortcuts off (exact either way); P=0 limiter skips stay on"}
+
     # per-phase kernel times: events between the kernels of every stage, no host
     # syncs inside the pass (the library folds them in when the timers are read)
     solver.enable_timers(True)
@@ -290,7 +311,7 @@ def run_ours(args, rank, world, local_rank):
            "h2d_bytes_per_step": int(n_nodes * nv * 8), "d2h_bytes_per_step": int(n_nodes * nv * 8),
            "steps": e2e_steps, "wall_s": wall}
 
-    kernels_per_stage = 3 + (1 + max(passes - 1, 0) + 1 if passes > 0 else 1)
+    kernels_per_stage = 3 + (1 + 2 * max(passes - 1, 0) + 1 if passes > 0 else 1)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -301,6 +322,7 @@ def run_ours(args, rank, world, local_rank):
                    "parallelism": f"cm-range partition x{world}, NCCL halo" if world > 1 else "single",
                    "l2": l2_note(nnz * (4 + 1 + 8 * (2 * dim + 1 + 1 + passes)) / 1e6)},
         "roofline": roofline,
+        "general_path": general,
         "e2e": e2e,
         "clocks": clocks,
         "gpu_launches": int(args.steps * 3 * kernels_per_stage),

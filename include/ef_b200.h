@@ -113,6 +113,11 @@ int ef_enable_timers(ef_solver* h, int32_t on);
 /* CUDA-graph replay of whole steps (single rank; on by default unless the
  * environment sets EF_GRAPHS=0).  Results are identical either way. */
 int ef_enable_graphs(ef_solver* h, int32_t on);
+/* Identical-state shortcuts (exact closed forms where U_i == U_j, uniform
+ * stencils, P = 0): -1 = automatic (default; on while the last synchronised step
+ * saw >= 2% of them, environment EF_UNIFORM=0/1 overrides), 0 = off, 1 = on.
+ * Results are identical in every mode. */
+int ef_set_uniform(ef_solver* h, int32_t mode);
 int ef_phase_times(ef_solver* h, double* seconds7);
 /* Solver.n_euler_steps, comm.sync_count, comm.sync_volume (doubles) */
 int ef_counters(ef_solver* h, int64_t* out3);

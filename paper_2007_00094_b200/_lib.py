@@ -59,6 +59,7 @@ SIGNATURES = {
     "ef_last_error": (ctypes.c_char_p, []),
     "ef_enable_timers": (_i32, [_p, _i32]),
     "ef_enable_graphs": (_i32, [_p, _i32]),
+    "ef_set_uniform": (_i32, [_p, _i32]),
     "ef_phase_times": (_i32, [_p, _p]),
     "ef_counters": (_i32, [_p, _p]),
     "ef_info": (_i32, [_p, _p]),

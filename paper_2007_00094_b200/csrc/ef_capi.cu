@@ -1125,6 +1125,14 @@ int ef_enable_timers(ef_solver* h, int32_t on) {
   return EF_OK;
 }
 
+int ef_set_uniform(ef_solver* h, int32_t mode) {
+  if (!h) return fail(EF_ERR_ARG, "null handle");
+  if (mode < -1 || mode > 1) return fail(EF_ERR_ARG, "mode must be -1 (auto), 0 (off) or 1 (on)");
+  h->uni_force = mode;
+  h->uni_on = mode != 0;
+  return EF_OK;
+}
+
 int ef_enable_graphs(ef_solver* h, int32_t on) {
   if (!h) return fail(EF_ERR_ARG, "null handle");
   h->use_graphs = on != 0;

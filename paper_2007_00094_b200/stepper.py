@@ -286,6 +286,11 @@ class Solver:
         for h in self._handles:
             _raise(_lib.load().ef_enable_graphs(h, 1 if on else 0))
 
+    def set_uniform_shortcuts(self, mode: int = -1):
+        """Identical-state shortcuts: -1 automatic (default), 0 off, 1 on; identical results."""
+        for h in self._handles:
+            _raise(_lib.load().ef_set_uniform(h, int(mode)))
+
     @property
     def timers(self) -> Dict[str, float]:
         s = np.zeros(7)

@@ -1,8 +1,8 @@
 """Per-kernel DRAM bytes per launch from an `ncu --set full` report -> profiles/ncu_traffic.json.
 
 python tools/ncu_traffic.py REPORT.ncu-rep CONFIG
-Keys are the short kernel names (`k_edge_lim` = its first launch in the report,
-i.e. pass 0; later launches of the same kernel get `#2`, `#3` suffixes)."""
+Keys are the short kernel names (`k_edge_lim` = the first limiter pass, which
+forms P; `k_edge_lim#2` = a later pass; repeated launches get `#2`, `#3`...)."""
 import csv
 import json
 import os
@@ -23,7 +23,11 @@ def val(r, name):
 
 res = {}
 for r in rows[2:]:
-    name = r[hdr.index("Kernel Name")].split("(")[0].replace("void ", "").split("<")[0]
+    full = r[hdr.index("Kernel Name")].split("(")[0].replace("void ", "")
+    name = full.split("<")[0]
+    targs = [a.strip() for a in full.split("<", 1)[1].rstrip(">").split(",")] if "<" in full else []
+    if name == "k_edge_lim" and len(targs) > 1 and targs[1] == "0":
+        name = "k_edge_lim#2"  # a later pass; the first pass (P) is `k_edge_lim`
     key, k = name, 2
     while key in res:
         key = f"{name}#{k}"
