@@ -542,6 +542,8 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
   EF_TRY(h->alloc(&w.P, (size_t)NV * NPL));
   EF_TRY(h->alloc(&w.nonuni, NP));
   EF_CUDA(cudaMemset(w.nonuni, 1, NP));
+  EF_TRY(h->alloc(&w.pnz, NP));
+  EF_CUDA(cudaMemset(w.pnz, 1, NP));
   EF_TRY(h->alloc(&w.lz, NP));
   EF_CUDA(cudaMemset(w.lz, 0, sizeof(double) * NP));
   EF_TRY(h->alloc(&w.tau_min_bits, 1));

@@ -625,6 +625,7 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_LOW(D), D)) k_low_o
       lz = limiter<D>(Un, z, rmin, rmax, pmin, sp.newton, g);
     }
     w.lz[i] = lz;
+    w.pnz[i] = 0;  // the first limiter pass marks the rows of every edge it computes
   }
   // uniform rows (keep the shortcuts on): sampled like k_edge_visc's count
   if (EF_UNIFORM_ROWS && sp.uni && sp.tau_mode != TAU_DEVICE && (blockIdx.x & 7) == 0) count_hits(uni, w.n_same);
@@ -668,6 +669,10 @@ __device__ __forceinline__ void edge_lim_one(const Layout& m, const Gas& g, cons
         return;
       }
     }
+  }
+  if (FIRST && UNI) {  // this edge's P is computed: both rows may carry a nonzero P
+    w.pnz[i] = 1;
+    w.pnz[j] = 1;
   }
   if (FIRST) {  // q == 0
     const double tau = *w.tau;
@@ -777,8 +782,11 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_PASS(D), D)) k_row_
   double upd[NV];
 #pragma unroll
   for (int k = 0; k < NV; ++k) upd[k] = 0.0;
+  // every P of the row is the first pass's stored +0 (kept zero by later
+  // passes): each term is +-0 and the sums stay +0, so the loop is skipped
+  const int nslots = (EF_UNIFORM_ROWS && sp.uni && !w.pnz[i]) ? 0 : card;
   EF_UNROLL_PASS1
-  for (int s = 0; s < card; ++s) {
+  for (int s = 0; s < nslots; ++s) {
     if (s == dg) continue;
     const int p = base + s * 32;
     const double ml = w.ml[p];
@@ -820,8 +828,9 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_FINAL(D), D)) k_fin
 #pragma unroll
     for (int k = 0; k < NV; ++k) upd[k] = 0.0;
     const bool rescale = sp.passes >= 2;  // P of the last pass = P_(q-1) (1 - min l_(q-1))
+    const int nslots = (EF_UNIFORM_ROWS && sp.uni && !w.pnz[i]) ? 0 : card;  // all P zero (k_row_upd)
     EF_UNROLL_FINAL
-    for (int s = 0; s < card; ++s) {
+    for (int s = 0; s < nslots; ++s) {
       if (s == dg) continue;
       const int p = base + s * 32;
       const double gp = rescale ? 1.0 - w.ml[p] : 1.0;
