@@ -115,7 +115,7 @@ int ef_enable_timers(ef_solver* h, int32_t on);
 int ef_enable_graphs(ef_solver* h, int32_t on);
 /* Identical-state shortcuts (exact closed forms where U_i == U_j, uniform
  * stencils, P = 0): -1 = automatic (default; on while the last synchronised step
- * saw >= 2% of them, environment EF_UNIFORM=0/1 overrides), 0 = off, 1 = on.
+ * saw >= 20% of them, environment EF_UNIFORM=0/1 overrides), 0 = off, 1 = on.
  * Results are identical in every mode. */
 int ef_set_uniform(ef_solver* h, int32_t mode);
 int ef_phase_times(ef_solver* h, double* seconds7);
