@@ -542,6 +542,8 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
   EF_TRY(h->alloc(&w.P, (size_t)NV * NPL));
   EF_TRY(h->alloc(&w.nonuni, NP));
   EF_CUDA(cudaMemset(w.nonuni, 1, NP));
+  EF_TRY(h->alloc(&w.chg, NP));
+  EF_CUDA(cudaMemset(w.chg, 1, NP));
   EF_TRY(h->alloc(&w.pnz, NP));
   EF_CUDA(cudaMemset(w.pnz, 1, NP));
   EF_TRY(h->alloc(&w.lz, NP));
@@ -882,6 +884,9 @@ static int finish(Driver& d, int out_buf, double* tau_used) {
     EF_TRY(readback(h));
     err |= h->rb->err;
     bad = std::min(bad, h->rb->bad);
+  }
+  if (err) {  // the state rolls back: nothing computed for the failed stages may be reused
+    for (ef_solver* h : d.hs) EF_CUDA(cudaMemsetAsync(h->w.chg, 1, h->NP, h->st));
   }
   if (err & ef::ERR_TAU_UNBOUNDED) return fail(EF_ERR_TAU_UNBOUNDED, "constant field, the time step bound is unbounded");
   if (err & ef::ERR_PROJECT) return fail(EF_ERR_INADMISSIBLE, "projected state requires rho > 0 and p > 0");

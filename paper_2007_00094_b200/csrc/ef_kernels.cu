@@ -144,6 +144,13 @@ __device__ __forceinline__ bool all_finite(const double* x) {
   for (int k = 0; k < N; ++k) ok = ok && finite(x[k]);
   return ok;
 }
+// d_ij memo across identical-state stages (EF_MEMO_D, default on)
+#ifndef EF_MEMO_D
+#define EF_MEMO_D 1
+#endif
+// min(l) slot tag: this slot's P is zero for the current and all later passes
+// (set instead of storing zero P; a genuine min(l) is in [0, 1])
+constexpr double kZeroP = -1.0;
 // P = 0 shortcut of the limiter passes after the first (EF_ZSKIP, default on)
 #ifndef EF_ZSKIP
 #define EF_ZSKIP 1
@@ -194,7 +201,6 @@ __device__ __forceinline__ void nodal_one(const double* Ui, const Gas& g, Work& 
 #pragma unroll
   for (int a = 0; a < D; ++a) w.vp[a * NP + i] = qdiv(Ui[1 + a], rr);  // physics.py:157
   w.vp[D * NP + i] = g.gm1 * eps;                                        // physics.py:94
-  w.nonuni[i] = 0;  // k_edge_visc of the stage marks rows with a differing neighbour
 }
 
 template <int D>
@@ -204,6 +210,8 @@ __global__ void k_nodal(Layout m, Gas g, const double* __restrict__ U, Work w, i
   double Ui[D + 2];
   load_node<D + 2>(U, m.NP, i, Ui);
   nodal_one<D>(Ui, g, w, (int)m.NP, (int)i);
+  w.nonuni[i] = 0;  // a new state (set_state, ghost rows): nothing of it is known
+  w.chg[i] = 1;
 }
 
 // ---------------------------------------------------------------- step1a
@@ -219,6 +227,14 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_EDGE(D), D)) k_edge
   if ((flags & 1) && e == 0) *w.tau_min_bits = 0x7ff0000000000000ULL;
   if (e >= m.n_edges) return;
   const int NP = (int)m.NP, NE = (int)m.n_edges;
+  if (UNI && EF_MEMO_D) {
+    // both rows unchanged since the previous identical-state stage: d_ij (a pure
+    // function of U_i, U_j and the static geometry) and the rows' uniformity
+    // marks are still those of the previous stage
+    const int p0 = m.edges[e];
+    const int i0 = (int)fdiv((uint32_t)p0, m.slab) * 32 + (p0 & 31);
+    if (!w.chg[i0] && !w.chg[m.edge_j[e]]) return;
+  }
   if (EF_PF_DIST > 0 && e + EF_PF_DIST < NE) {
     const int f = e + EF_PF_DIST;
     pf_l2(m.edges + f);
@@ -658,14 +674,11 @@ __device__ __forceinline__ void edge_lim_one(const Layout& m, const Gas& g, cons
     if (i < no && j < no) {
       const double li = w.lz[i], lj = w.lz[j];
       if (li == li && lj == lj) {
-#pragma unroll
-        for (int k = 0; k < NV; ++k) {
-          w.P[(size_t)k * NPL + p] = 0.0;
-          w.P[(size_t)k * NPL + pt] = 0.0;
-        }
+        // no P store: the slots are tagged kZeroP instead of min(l) (every later
+        // use of that factor multiplies the zero P; the next pass's factor is lz)
         double* __restrict__ mo = sp.passes == 1 ? w.ml2 : w.ml;
-        mo[p] = npmin(li, lj);
-        mo[pt] = npmin(lj, li);
+        mo[p] = kZeroP;
+        mo[pt] = kZeroP;
         return;
       }
     }
@@ -695,25 +708,23 @@ __device__ __forceinline__ void edge_lim_one(const Layout& m, const Gas& g, cons
       Pj[k] = fj * (((bj * Rik) - (bTj * Rjk)) + (ddj * (Uik - Ujk)));
     }
   } else {
-    const double gi = 1.0 - w.ml[p], gj = 1.0 - w.ml[pt];
-    if (EF_ZSKIP && gi == 0.0 && gj == 0.0) {
+    const double mli = w.ml[p], mlj = w.ml[pt];
+    const double gi = 1.0 - mli, gj = 1.0 - mlj;
+    if ((EF_ZSKIP && gi == 0.0 && gj == 0.0) || mli < 0.0) {  // (mli < 0: kZeroP, P already 0)
       // min(l) of the previous pass was 1: P rescales to (+-)0 on both sides
       // (P is finite, k_edge_lim<FIRST> checks), and limiter(U^L, +-0, bounds)
       // depends on the row alone -- k_row_upd stored it as lz (the sign of a
       // zero P cannot reach the result: V = U^L exactly, and the Newton branch
       // is never taken with P = 0).  The P loads, the two limiter evaluations
       // and (last pass) the P store are skipped; k_final skips the same slots.
-      if (q != sp.passes - 1) {
-#pragma unroll
-        for (int k = 0; k < NV; ++k) {
-          w.P[(size_t)k * NPL + p] = 0.0;
-          w.P[(size_t)k * NPL + pt] = 0.0;
-        }
-      }
       const double li = w.lz[i], lj = w.lz[j];
-      double* __restrict__ mo = q == sp.passes - 1 ? w.ml2 : w.ml;
-      mo[p] = npmin(li, lj);
-      mo[pt] = npmin(lj, li);
+      if (q == sp.passes - 1) {
+        w.ml2[p] = npmin(li, lj);
+        w.ml2[pt] = npmin(lj, li);
+      } else {  // P stays zero for the next passes: tag instead of storing zeros
+        w.ml[p] = kZeroP;
+        w.ml[pt] = kZeroP;
+      }
       return;
     }
 #pragma unroll
@@ -790,6 +801,7 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_PASS(D), D)) k_row_
     if (s == dg) continue;
     const int p = base + s * 32;
     const double ml = w.ml[p];
+    if (ml < 0.0) continue;  // kZeroP: the term is ml * (+-0)
 #pragma unroll
     for (int k = 0; k < NV; ++k) upd[k] = upd[k] + ml * w.P[(size_t)k * NPL + p];
   }
@@ -833,11 +845,14 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_FINAL(D), D)) k_fin
     for (int s = 0; s < nslots; ++s) {
       if (s == dg) continue;
       const int p = base + s * 32;
-      const double gp = rescale ? 1.0 - w.ml[p] : 1.0;
+      const double mlp = rescale ? w.ml[p] : 0.0;
+      const double gp = rescale ? 1.0 - mlp : 1.0;
       // gp == 0: the term is ml2 * (P * 0) = +-0 (P finite), and adding +-0 to a
-      // sum that starts at +0 never changes it (it cannot become -0)
-      if (EF_ZSKIP && gp == 0.0) continue;
+      // sum that starts at +0 never changes it (it cannot become -0); kZeroP
+      // slots (negative tag) carry a zero P
+      if ((EF_ZSKIP && gp == 0.0) || mlp < 0.0) continue;
       const double ml = w.ml2[p];
+      if (ml < 0.0) continue;  // kZeroP from a single-pass first limiter
 #pragma unroll
       for (int k = 0; k < NV; ++k) {
         const double Pk = rescale ? w.P[(size_t)k * NPL + p] * gp : w.P[(size_t)k * NPL + p];
@@ -883,6 +898,17 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_FINAL(D), D)) k_fin
 #pragma unroll
   for (int k = 0; k < NV; ++k) Uout[k * NP + i] = Uo[k];
   nodal_one<D>(Uo, g, w, NP, i);  // next stage's step0
+  // flags for the next stage: after an identical-state stage, an unchanged row
+  // keeps its d_ij memo and its uniformity mark (k_edge_visc recomputes every
+  // edge with a changed end); otherwise everything is recomputed
+  bool changed = true;
+  if (EF_UNIFORM_ROWS && sp.uni) {
+    double Ui[NV];
+    load_node<NV>(U, NP, i, Ui);
+    changed = !same_state<NV>(Uo, Ui);
+  }
+  w.chg[i] = changed ? 1 : 0;
+  if (changed) w.nonuni[i] = 0;
 }
 
 // ---------------------------------------------------------------- halo packing

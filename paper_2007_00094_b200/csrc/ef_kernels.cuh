@@ -82,6 +82,8 @@ struct Work {
   double* P;         // [NV][NP*L] correction fluxes P_ij, rescaled in place per pass
   uint8_t* nonuni;   // [NP] 1 if some stencil neighbour's state differs from the row's
                      // (bitwise); set by k_edge_visc, cleared by step0 (k_final / k_nodal)
+  uint8_t* chg;      // [NP] 1 unless the row's state is bitwise the one of the previous
+                     // (identical-state) stage: d_ij of two unchanged rows is kept
   uint8_t* pnz;      // [NP] (identical-state stages) 1 if some P_ij of the row may be nonzero;
                      // 0: every edge of the row took the first pass's P = 0 shortcut
   double* lz;        // [NP] limiter(U^L_i, P = 0, bounds_i) after a non-final update: the

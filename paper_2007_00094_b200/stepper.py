@@ -300,7 +300,9 @@ class Solver:
     _FIELDS = {"d": 0, "alpha": 1, "R": 2, "bounds": 3, "l": 4, "eor": 5, "phi": 6, "U": 7, "U_next": 8, "l_prev": 9}
 
     def fetch(self, which: str, pass_index: int = 0) -> np.ndarray:
-        """Internal arrays (rows = local rows in global CM order; slots in stencil order)."""
+        """Internal arrays (rows = local rows in global CM order; slots in stencil order).
+        "l" / "l_prev": min(l_ij, l_ji) of the last / the previous limiter pass; slots of
+        edges on the exact P = 0 fast path hold the tag -1 (their factor multiplies a zero P)."""
         n, L, nv = self.n_local, self.pad_width, self.nvar
         shapes = {"d": (n, L), "alpha": (n,), "R": (n, nv), "bounds": (n, 3), "l": (n, L),
                   "eor": (n,), "phi": (n,), "U": (n, nv), "U_next": (n, nv), "l_prev": (n, L)}
