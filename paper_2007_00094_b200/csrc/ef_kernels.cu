@@ -148,6 +148,12 @@ __device__ __forceinline__ bool all_finite(const double* x) {
 #ifndef EF_MEMO_D
 #define EF_MEMO_D 1
 #endif
+#ifndef EF_TAG_EXIT
+#define EF_TAG_EXIT 1
+#endif
+#ifndef EF_PF_VISC_UNI
+#define EF_PF_VISC_UNI 131072  // (the memo check makes the identical-state variant latency-bound: -6%)
+#endif
 // min(l) slot tag: this slot's P is zero for the current and all later passes
 // (set instead of storing zero P; a genuine min(l) is in [0, 1])
 constexpr double kZeroP = -1.0;
@@ -227,6 +233,10 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_EDGE(D), D)) k_edge
   if ((flags & 1) && e == 0) *w.tau_min_bits = 0x7ff0000000000000ULL;
   if (e >= m.n_edges) return;
   const int NP = (int)m.NP, NE = (int)m.n_edges;
+  if (UNI && EF_PF_VISC_UNI > 0 && e + EF_PF_VISC_UNI < NE) {
+    pf_l2(m.edges + e + EF_PF_VISC_UNI);
+    pf_l2(m.edge_j + e + EF_PF_VISC_UNI);
+  }
   if (UNI && EF_MEMO_D) {
     // both rows unchanged since the previous identical-state stage: d_ij (a pure
     // function of U_i, U_j and the static geometry) and the rows' uniformity
@@ -708,7 +718,11 @@ __device__ __forceinline__ void edge_lim_one(const Layout& m, const Gas& g, cons
       Pj[k] = fj * (((bj * Rik) - (bTj * Rjk)) + (ddj * (Uik - Ujk)));
     }
   } else {
-    const double mli = w.ml[p], mlj = w.ml[pt];
+    const double mli = w.ml[p];
+    // kZeroP: P stays zero, the tag stays in ml, and no later reader uses this
+    // slot's factor (k_final skips tagged slots), so there is nothing to do
+    if (EF_TAG_EXIT && mli < 0.0) return;
+    const double mlj = w.ml[pt];
     const double gi = 1.0 - mli, gj = 1.0 - mlj;
     if ((EF_ZSKIP && gi == 0.0 && gj == 0.0) || mli < 0.0) {  // (mli < 0: kZeroP, P already 0)
       // min(l) of the previous pass was 1: P rescales to (+-)0 on both sides

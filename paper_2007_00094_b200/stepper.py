@@ -302,7 +302,8 @@ class Solver:
     def fetch(self, which: str, pass_index: int = 0) -> np.ndarray:
         """Internal arrays (rows = local rows in global CM order; slots in stencil order).
         "l" / "l_prev": min(l_ij, l_ji) of the last / the previous limiter pass; slots of
-        edges on the exact P = 0 fast path hold the tag -1 (their factor multiplies a zero P)."""
+        edges on the exact P = 0 fast path hold the tag -1 in "l_prev" (their factor multiplies a
+        zero P and is not stored by later passes: "l" keeps an earlier value there)."""
         n, L, nv = self.n_local, self.pad_width, self.nvar
         shapes = {"d": (n, L), "alpha": (n,), "R": (n, nv), "bounds": (n, 3), "l": (n, L),
                   "eor": (n,), "phi": (n,), "U": (n, nv), "U_next": (n, nv), "l_prev": (n, L)}
