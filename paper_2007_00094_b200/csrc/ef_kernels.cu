@@ -640,17 +640,7 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_LOW(D), D)) k_low_o
   if (EF_UNIFORM_ROWS && sp.uni && sp.passes > 0) {
     // first-pass factor of the edges between two uniform rows (their P is +-0,
     // R_i = R_j = +0 and U_j = U_i): limiter(U^L_i, 0, bounds_i); NaN = no shortcut
-    double lz = __longlong_as_double(0x7ff8000000000000LL);
-    if (uni) {
-      double Un[NV], z[NV];
-#pragma unroll
-      for (int k = 0; k < NV; ++k) {
-        Un[k] = Ui[k] + (fac * sumL[k]);
-        z[k] = 0.0;
-      }
-      lz = limiter<D>(Un, z, rmin, rmax, pmin, sp.newton, g);
-    }
-    w.lz[i] = lz;
+    w.lz[i] = uni ? 0.0 : __longlong_as_double(0x7ff8000000000000LL);
     w.pnz[i] = 0;  // the first limiter pass marks the rows of every edge it computes
   }
   // uniform rows (keep the shortcuts on): sampled like k_edge_visc's count
@@ -678,14 +668,13 @@ __device__ __forceinline__ void edge_lim_one(const Layout& m, const Gas& g, cons
   double Pi[NV], Pj[NV];
   if (FIRST && UNI && EF_UNIFORM_ROWS) {
     // both rows took k_low_order's uniform shortcut (lz not NaN; owned rows):
-    // R_i = R_j = +0 and U_j = U_i, so P_ij and P_ji are +-0 (stored as +0, the
-    // sign of a zero P never reaches a result) and each limiter is the row's lz
+    // R_i = R_j = +0 and U_j = U_i, so P_ij and P_ji are +-0 and stay zero in
+    // every pass; each later use of the slots' factors multiplies a zero P
     const int no = (int)m.n_owned;
     if (i < no && j < no) {
       const double li = w.lz[i], lj = w.lz[j];
       if (li == li && lj == lj) {
-        // no P store: the slots are tagged kZeroP instead of min(l) (every later
-        // use of that factor multiplies the zero P; the next pass's factor is lz)
+        // no P store and no limiter: the slots are tagged kZeroP instead of min(l)
         double* __restrict__ mo = sp.passes == 1 ? w.ml2 : w.ml;
         mo[p] = kZeroP;
         mo[pt] = kZeroP;
@@ -718,27 +707,19 @@ __device__ __forceinline__ void edge_lim_one(const Layout& m, const Gas& g, cons
       Pj[k] = fj * (((bj * Rik) - (bTj * Rjk)) + (ddj * (Uik - Ujk)));
     }
   } else {
-    const double mli = w.ml[p];
-    // kZeroP: P stays zero, the tag stays in ml, and no later reader uses this
-    // slot's factor (k_final skips tagged slots), so there is nothing to do
-    if (EF_TAG_EXIT && mli < 0.0) return;
-    const double mlj = w.ml[pt];
+    // (kZeroP slots and, in the last pass, min(l) == 1 slots never get here: the
+    // kernel returns for them before loading anything else, see k_edge_lim)
+    const double mli = w.ml[p], mlj = w.ml[pt];
     const double gi = 1.0 - mli, gj = 1.0 - mlj;
-    if ((EF_ZSKIP && gi == 0.0 && gj == 0.0) || mli < 0.0) {  // (mli < 0: kZeroP, P already 0)
-      // min(l) of the previous pass was 1: P rescales to (+-)0 on both sides
-      // (P is finite, k_edge_lim<FIRST> checks), and limiter(U^L, +-0, bounds)
-      // depends on the row alone -- k_row_upd stored it as lz (the sign of a
-      // zero P cannot reach the result: V = U^L exactly, and the Newton branch
-      // is never taken with P = 0).  The P loads, the two limiter evaluations
-      // and (last pass) the P store are skipped; k_final skips the same slots.
-      const double li = w.lz[i], lj = w.lz[j];
-      if (q == sp.passes - 1) {
-        w.ml2[p] = npmin(li, lj);
-        w.ml2[pt] = npmin(lj, li);
-      } else {  // P stays zero for the next passes: tag instead of storing zeros
-        w.ml[p] = kZeroP;
-        w.ml[pt] = kZeroP;
-      }
+    if (EF_ZSKIP && gi == 0.0 && gj == 0.0) {
+      // non-last pass, min(l) of the previous pass was 1: P rescales to +-0 on
+      // both sides (P is finite, k_edge_lim<FIRST> checks) and stays zero, so
+      // every later use of this slot's factor multiplies a zero P (the row
+      // update adds +-0, the next P is +-0 again, k_final skips the slot): the
+      // slots are tagged kZeroP and the P loads, both limiter evaluations and
+      // the P store are skipped
+      w.ml[p] = kZeroP;
+      w.ml[pt] = kZeroP;
       return;
     }
 #pragma unroll
@@ -787,7 +768,15 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ELIM(D, FIRST), D))
     pf_l2(m.edge_j + f);
     pf_l2(m.edge_pt + f);
   }
-  edge_lim_one<D, FIRST, UNI>(m, g, U, w, sp, q, m.edges[e], m.edge_j[e], m.edge_pt[e]);
+  const int p = m.edges[e];
+  if (!FIRST) {
+    // kZeroP slot: P stays zero and nothing reads its factor again.  Last pass
+    // with min(l) == 1: P rescales to +-0 and k_final skips the slot (its term
+    // is ml2 * (+-0)), so neither the factor nor anything else is needed.
+    const double mli = w.ml[p];
+    if (mli < 0.0 || (EF_ZSKIP && mli == 1.0 && q == sp.passes - 1)) return;
+  }
+  edge_lim_one<D, FIRST, UNI>(m, g, U, w, sp, q, p, m.edge_j[e], m.edge_pt[e]);
 }
 
 // step5 (non-final pass): U_next_i += lam_i * sum_s min(l) P in slot order
@@ -825,12 +814,6 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_PASS(D), D)) k_row_
   for (int k = 0; k < NV; ++k) {
     Un[k] = w.Unext[k * NP + i] + lam * upd[k];
     w.Unext[k * NP + i] = Un[k];
-  }
-  if (EF_ZSKIP) {  // the next pass's factor of the rows' P = 0 edges (see k_edge_lim)
-    double z[NV];
-#pragma unroll
-    for (int k = 0; k < NV; ++k) z[k] = 0.0;
-    w.lz[i] = limiter<D>(Un, z, w.bounds[i], w.bounds[NP + i], w.bounds[2 * NP + i], sp.newton, g);
   }
 }
 

@@ -86,8 +86,8 @@ struct Work {
                      // (identical-state) stage: d_ij of two unchanged rows is kept
   uint8_t* pnz;      // [NP] (identical-state stages) 1 if some P_ij of the row may be nonzero;
                      // 0: every edge of the row took the first pass's P = 0 shortcut
-  double* lz;        // [NP] limiter(U^L_i, P = 0, bounds_i) after a non-final update: the
-                     // factor of every edge whose previous min(l) was 1 (P then rescales to 0)
+  double* lz;        // [NP] first-pass marker: not NaN if the row took k_low_order's uniform
+                     // shortcut (owned rows; an edge between two such rows has P = 0)
   unsigned long long* tau_min_bits;  // CFL min over owned rows
   double* tau;       // tau of the current RK step / Euler step
   int* err;          // bit0 projection/entropy, bit1 inadmissible result, bit2 tau unbounded
