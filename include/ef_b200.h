@@ -151,6 +151,9 @@ int ef_eval_limiter(const ef_params* prm, int32_t dim, int64_t n, const double* 
 
 void ef_pow_host(const double* x, double y, double* out, int64_t n);
 int ef_pow_device(const double* x, double y, double* out, int64_t n);
+/* The limiter's fast-accept upper bound of pow(x, y) (+inf outside its range),
+ * evaluated on the device: for tests of the bound. */
+int ef_pow_bound_device(const double* x, double y, double* out, int64_t n);
 
 /* Device pointer of the current state, (nvar, stride) structure-of-arrays in
  * local row order (benchmarks / zero-copy consumers). */

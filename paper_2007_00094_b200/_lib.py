@@ -67,6 +67,7 @@ SIGNATURES = {
     "ef_local_gids": (_i32, [_p, _p]),
     "ef_pow_host": (None, [_p, _d, _p, _i64]),
     "ef_pow_device": (_i32, [_p, _d, _p, _i64]),
+    "ef_pow_bound_device": (_i32, [_p, _d, _p, _i64]),
     "ef_state_device_ptr": (_i32, [_p, ctypes.POINTER(_p), ctypes.POINTER(_i64)]),
     "ef_nccl_unique_id": (_i32, [_p]),
     "ef_group_create": (_i32, [_p, _i32, ctypes.POINTER(_p)]),

@@ -1236,6 +1236,19 @@ int ef_pow_device(const double* x, double y, double* out, int64_t n) {
   return EF_OK;
 }
 
+int ef_pow_bound_device(const double* x, double y, double* out, int64_t n) {
+  if (n <= 0) return EF_OK;
+  if (!x || !out) return fail(EF_ERR_ARG, "null argument");
+  DevBufs b;
+  double *dx, *dy;
+  EF_TRY(b.get(&dx, (size_t)n, x));
+  EF_TRY(b.get(&dy, (size_t)n));
+  ef::launch_pow_ub(dx, y, dy, n, 0);
+  EF_CUDA(cudaGetLastError());
+  EF_CUDA(cudaMemcpy(out, dy, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  return EF_OK;
+}
+
 int ef_eval_dij(const ef_params* prm, int32_t dim, int64_t n, const double* Ui, const double* Uj,
                 const double* cij, const double* cji, double* out, int32_t* bad) {
   if (!prm || (dim != 2 && dim != 3) || n < 0) return fail(EF_ERR_ARG, "bad arguments");

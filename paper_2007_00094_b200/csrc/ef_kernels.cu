@@ -1047,6 +1047,13 @@ void launch_unpack_pos(double* arr, const int32_t* pos, int64_t count, const dou
 void launch_group_min(unsigned long long* const* bits_dev, int n, cudaStream_t st) {
   k_group_min<<<1, 1, 0, st>>>(bits_dev, n);
 }
+__global__ void k_pow_ub(const double* __restrict__ x, double y, double* __restrict__ out, int64_t n) {
+  const int64_t q = blockIdx.x * (int64_t)TPB + threadIdx.x;
+  if (q < n) out[q] = pow_ub(x[q], y);
+}
+void launch_pow_ub(const double* x, double y, double* out, int64_t n, cudaStream_t st) {
+  if (n > 0) k_pow_ub<<<grid_for(n), TPB, 0, st>>>(x, y, out, n);
+}
 void launch_pow(const double* x, double y, double* out, int64_t n, cudaStream_t st) {
   if (n <= 0) return;
   k_pow<<<grid_for(n), TPB, 0, st>>>(x, y, out, n);

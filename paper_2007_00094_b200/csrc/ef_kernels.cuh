@@ -151,6 +151,8 @@ void launch_row_upd(int dim, const Layout& m, const Gas& g, const double* U, Wor
 void launch_final(int dim, const Layout& m, const Gas& g, const double* U, const double* U0,
                   double* Uout, Work w, StageParams sp, RowSet rs, cudaStream_t st);
 void launch_pow(const double* x, double y, double* out, int64_t n, cudaStream_t st);
+// the limiter's fast-accept upper bound of pow (ef_math.cuh: pow_ub), for tests
+void launch_pow_ub(const double* x, double y, double* out, int64_t n, cudaStream_t st);
 // halo exchange helpers: buf[r * stride + coff + k] <-> field[k * NP + idx[r]]
 void launch_pack_rows(const double* field, int ncomp, int64_t NP, const int32_t* idx, int64_t count,
                       double* buf, int stride, int coff, cudaStream_t st);

@@ -101,3 +101,25 @@ def test_limiter_properties_and_parity(dim):
         assert np.all((l >= 0.0) & (l <= 1.0))
         r = rho + l * P[:, 0]
         assert np.all(r >= rmin * (1 - 1e-12)) and np.all(r <= rmax * (1 + 1e-12))
+
+
+def test_limiter_fast_accept_bound_is_an_upper_bound():
+    """The limiter's fast accept (ef_math.cuh: pow_ub) must bound the exact pow
+    from above on its whole range, and tightly (within 2^-12)."""
+    from paper_2007_00094_b200 import _lib
+    from paper_2007_00094_b200.stepper import shared_pow
+
+    rng = np.random.default_rng(11)
+    x = np.concatenate([2.0 ** rng.uniform(-20, 20, 2_000_000), 1.0 + rng.uniform(-1e-6, 1e-6, 200_000),
+                        np.nextafter(2.0 ** -20, 1.0) * (1 + rng.uniform(0, 1e-3, 1000)),
+                        np.nextafter(2.0 ** 20, 0.0) * (1 - rng.uniform(0, 1e-3, 1000))])
+    for y in (AIR.gamma + 1.0, AIR.gamma, 1.0, 4.0):
+        ub = np.empty_like(x)
+        assert _lib.load().ef_pow_bound_device(x.ctypes.data, float(y), ub.ctypes.data, x.size) == 0
+        exact = shared_pow(x, y)
+        assert np.all(ub >= exact), (y, np.min(ub / exact))
+        assert np.max(ub / exact) < 1.0 + 2.0 ** -12
+    out = np.empty(4)
+    xs = np.array([2.0 ** -21, 2.0 ** 21, 0.0, np.nan])
+    _lib.load().ef_pow_bound_device(xs.ctypes.data, 2.4, out.ctypes.data, 4)
+    assert np.all(np.isinf(out))
