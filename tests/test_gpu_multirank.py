@@ -80,3 +80,15 @@ def test_ranks_euler_and_roundtrip():
     for _ in range(3):
         assert s.euler_step() == o.euler_step()
     assert np.array_equal(s.get_state(), o.get_state())
+
+
+@pytest.mark.parametrize("mode", ["0", "1"])
+@pytest.mark.parametrize("case", ["c2", "c3"])
+def test_ranks_identical_state_shortcuts_forced(mode, case, monkeypatch):
+    """Shortcuts forced off / on: ghost rows never take them (their stencils are
+    truncated), the halo data are the same, so every rank count agrees."""
+    monkeypatch.setenv("EF_UNIFORM", mode)
+    ps = CASES[case]()
+    t1, U1, _ = _run(ps.matrices, ps.U0, ps.boundary, 1, 4, c_cfl=ps.c_cfl)
+    t3, U3, _ = _run(ps.matrices, ps.U0, ps.boundary, 3, 4, c_cfl=ps.c_cfl)
+    assert t1 == t3 and np.array_equal(U1, U3)
