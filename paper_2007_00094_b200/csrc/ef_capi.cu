@@ -531,6 +531,7 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
   EF_TRY(h->alloc(&w.eor, NP));
   EF_TRY(h->alloc(&w.phi, NP));
   EF_TRY(h->alloc(&w.vp, (size_t)(D + 1) * NP));
+  EF_TRY(h->alloc(&w.rinv, NP));
   EF_CUDA(cudaMemset(w.vp, 0, sizeof(double) * (D + 1) * NP));
   EF_TRY(h->alloc(&w.alpha, NP));
   EF_TRY(h->alloc(&w.R, (size_t)NV * NP));
@@ -885,8 +886,12 @@ static int finish(Driver& d, int out_buf, double* tau_used) {
     err |= h->rb->err;
     bad = std::min(bad, h->rb->bad);
   }
-  if (err) {  // the state rolls back: nothing computed for the failed stages may be reused
-    for (ef_solver* h : d.hs) EF_CUDA(cudaMemsetAsync(h->w.chg, 1, h->NP, h->st));
+  if (err) {  // the state rolls back: nothing computed for the failed stages may be reused --
+              // step0 of the current state again (it also clears the memo marks)
+    for (ef_solver* h : d.hs) {
+      ef::launch_nodal(h->dim, h->lay, h->gas, h->Ubuf[h->cur], h->w, 0, h->lay.n_local, h->st);
+      EF_CUDA(cudaGetLastError());
+    }
   }
   if (err & ef::ERR_TAU_UNBOUNDED) return fail(EF_ERR_TAU_UNBOUNDED, "constant field, the time step bound is unbounded");
   if (err & ef::ERR_PROJECT) return fail(EF_ERR_INADMISSIBLE, "projected state requires rho > 0 and p > 0");

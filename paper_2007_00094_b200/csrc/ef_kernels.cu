@@ -166,6 +166,11 @@ constexpr double kZeroP = -1.0;
 #endif
 __device__ __forceinline__ void pf_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
+// k_edge_visc reads RN(1/rho) of both rows from step0 instead of dividing
+#ifndef EF_RINV
+#define EF_RINV 0
+#endif
+
 // ---------------------------------------------------------------- state I/O
 template <int D>
 __global__ void k_gather_state(Layout m, const double* __restrict__ Uaos,
@@ -207,6 +212,7 @@ __device__ __forceinline__ void nodal_one(const double* Ui, const Gas& g, Work& 
 #pragma unroll
   for (int a = 0; a < D; ++a) w.vp[a * NP + i] = qdiv(Ui[1 + a], rr);  // physics.py:157
   w.vp[D * NP + i] = g.gm1 * eps;                                        // physics.py:94
+  if (EF_RINV) w.rinv[i] = rr.y;
 }
 
 template <int D>
@@ -272,7 +278,12 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_EDGE(D), D)) k_edge
     w.nonuni[i] = 1;
     w.nonuni[j] = 1;
   }
-  const double dv = d_ij_geo<D>(Ui, Uj, nij, norm_ij, nji, norm_ji, g, bad, UNI && same);
+  double yij[2];
+  if (EF_RINV) {
+    yij[0] = w.rinv[i];
+    yij[1] = w.rinv[j];
+  }
+  const double dv = d_ij_geo<D>(Ui, Uj, nij, norm_ij, nji, norm_ji, g, bad, UNI && same, EF_RINV ? yij : nullptr);
   // d is symmetric by construction (riemann.py:139-142): the value is also
   // the lower-triangle entry of row j, written straight to its slot (the
   // reference's mirror, stepper.py:427-434, without a gather)
@@ -469,9 +480,12 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ROW(D), D)) k_row_v
     if (want_tau && dii < 0.0) cand = m.m_i[i] / (-2.0 * dii);
     // IndicatorAccumulator.reset (harten_entropy_derivative, physics.py:133-148)
     double ep[NV];
+    const double re = Ui[0] * internal_energy<D>(Ui);
+    if (re <= 0.0) bad = true;
+    if (uni) {  // A = B = +0: numer = denom = +0, so alpha = 0 whatever eta' is
+      w.alpha[i] = 0.0;
+    } else {
     {
-      const double re = Ui[0] * internal_energy<D>(Ui);
-      if (re <= 0.0) bad = true;
       const double scale = dpow(re, g.neg_g_gp1_inv) * g.gp1_inv;  // physics.py:143
       ep[0] = scale * Ui[D + 1];
 #pragma unroll
@@ -493,6 +507,7 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ROW(D), D)) k_row_v
     const double safe = denom > kDenomFloor ? denom : 1.0;
     const double al = npclip(div0(numer, safe), 0.0, 1.0);
     w.alpha[i] = denom > kDenomFloor ? al : 0.0;
+    }
   }
   if (bad) atomicOr(w.err, ERR_PROJECT);
   if (!want_tau) return;
@@ -894,7 +909,6 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_FINAL(D), D)) k_fin
   }
 #pragma unroll
   for (int k = 0; k < NV; ++k) Uout[k * NP + i] = Uo[k];
-  nodal_one<D>(Uo, g, w, NP, i);  // next stage's step0
   // flags for the next stage: after an identical-state stage, an unchanged row
   // keeps its d_ij memo and its uniformity mark (k_edge_visc recomputes every
   // edge with a changed end); otherwise everything is recomputed
@@ -906,6 +920,9 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_FINAL(D), D)) k_fin
   }
   w.chg[i] = changed ? 1 : 0;
   if (changed) w.nonuni[i] = 0;
+  // next stage's step0; an unchanged row's eor, phi, v, p (pure functions of
+  // its state) are already in place
+  if (changed) nodal_one<D>(Uo, g, w, NP, i);
 }
 
 // ---------------------------------------------------------------- halo packing

@@ -72,6 +72,7 @@ struct Work {
   double* eor;       // [NP]
   double* phi;       // [NP]
   double* vp;        // [(D+1)*NP] v = m / rho (D comps), p = gm1 * eps: the flux inputs
+  double* rinv;      // [NP] RN(1 / rho) of step0 (k_edge_visc's shared reciprocal)
   double* alpha;     // [NP]
   double* R;         // [NV][NP]
   double* Unext;     // [NV][NP]

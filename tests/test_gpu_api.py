@@ -218,3 +218,23 @@ def test_graph_replay_is_bitwise_identical():
     assert np.array_equal(ta, tb)
     assert np.array_equal(Ua, Ub)
     assert na == nb == 4 * 3 + 3 + 3 + 5 * 3
+
+
+def test_stepping_after_an_error_restarts_from_the_kept_state():
+    """After an AdmissibilityError the state is the one before the call, and
+    the next steps equal those of a fresh solver from that state (nothing
+    computed for the failed stages -- step0 fields, memo marks -- is reused)."""
+    ps = P.make_config("c2", scale="small")
+    s = Solver(ps.matrices, c_cfl=ps.c_cfl, boundary=ps.boundary)
+    s.set_state(ps.U0)
+    for _ in range(3):
+        s.ssp_rk3_step()
+    U = s.get_state()
+    with pytest.raises(AdmissibilityError):
+        s.euler_step(tau=5.0)  # far beyond the CFL bound
+    assert np.array_equal(s.get_state(), U)
+    taus = [s.ssp_rk3_step() for _ in range(3)]
+    f = Solver(ps.matrices, c_cfl=ps.c_cfl, boundary=ps.boundary)
+    f.set_state(U)
+    assert taus == [f.ssp_rk3_step() for _ in range(3)]
+    assert np.array_equal(s.get_state(), f.get_state())
