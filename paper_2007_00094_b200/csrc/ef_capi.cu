@@ -531,7 +531,6 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
   EF_TRY(h->alloc(&w.eor, NP));
   EF_TRY(h->alloc(&w.phi, NP));
   EF_TRY(h->alloc(&w.vp, (size_t)(D + 1) * NP));
-  EF_TRY(h->alloc(&w.rinv, NP));
   EF_CUDA(cudaMemset(w.vp, 0, sizeof(double) * (D + 1) * NP));
   EF_TRY(h->alloc(&w.alpha, NP));
   EF_TRY(h->alloc(&w.R, (size_t)NV * NP));
@@ -547,6 +546,9 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
   EF_CUDA(cudaMemset(w.chg, 1, NP));
   EF_TRY(h->alloc(&w.pnz, NP));
   EF_CUDA(cudaMemset(w.pnz, 1, NP));
+  EF_TRY(h->alloc(&w.wl, std::max<int64_t>(h->lay.n_edges, 1)));
+  EF_TRY(h->alloc(&w.wl_n, 1));
+  EF_CUDA(cudaMemset(w.wl_n, 0, sizeof(int)));
   EF_TRY(h->alloc(&w.lz, NP));
   EF_CUDA(cudaMemset(w.lz, 0, sizeof(double) * NP));
   EF_TRY(h->alloc(&w.tau_min_bits, 1));
@@ -736,13 +738,21 @@ static int run_stage(Driver& d, const std::vector<StageIO>& io, StageParams sp) 
     ef::launch_low_order(h->dim, h->lay, h->gas, x.U, h->w, sp, rs, st);
   }, lo_flds));
   EF_TRY(mark(t, 4));
+  // the pass before the last fills the last pass's worklist
+  auto clear_wl = [&](int q) -> int {
+    if (ef::edge_lim_worklist() && q == t->passes - 2)
+      for (ef_solver* h : d.hs) EF_CUDA(cudaMemsetAsync(h->w.wl_n, 0, sizeof(int), st));
+    return EF_OK;
+  };
   if (t->passes > 0) {
+    EF_TRY(clear_wl(0));
     each([&](ef_solver* h, const StageIO& x) { ef::launch_edge_lim(h->dim, h->lay, h->gas, x.U, h->w, sp, 0, st); });
     EF_TRY(mark(t, 5));
     for (int p = 0; p + 1 < t->passes; ++p) {
       EF_TRY(produce([&](ef_solver* h, const StageIO& x, ef::RowSet rs) {
         ef::launch_row_upd(h->dim, h->lay, h->gas, x.U, h->w, sp, rs, st);
       }, {fld(&Work::Unext, NV)}));
+      EF_TRY(clear_wl(p + 1));
       each([&](ef_solver* h, const StageIO& x) { ef::launch_edge_lim(h->dim, h->lay, h->gas, x.U, h->w, sp, p + 1, st); });
     }
     EF_TRY(mark(t, 6));

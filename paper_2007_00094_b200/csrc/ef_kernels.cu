@@ -131,6 +131,17 @@ __device__ __forceinline__ void load_node(const double* __restrict__ U, int64_t 
 #ifndef EF_UNIFORM_ROWS
 #define EF_UNIFORM_ROWS 1
 #endif
+// warp-aggregated append of e to a worklist (order is irrelevant: each listed
+// edge's work is independent)
+__device__ __forceinline__ void wl_append(bool need, int e, int* __restrict__ wl, int* n) {
+  const unsigned act = __activemask(), bal = __ballot_sync(act, need);
+  if (!bal) return;
+  const int lane = threadIdx.x & 31, leader = __ffs(bal) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(n, __popc(bal));
+  base = __shfl_sync(act, base, leader);
+  if (need) wl[base + __popc(bal & ((1u << lane) - 1u))] = e;
+}
 // warp-aggregated count into one of kSameSlots counters (spread: no hot address)
 __device__ __forceinline__ void count_hits(bool hit, unsigned long long* slots) {
   const unsigned act = __activemask(), hits = __ballot_sync(act, hit);
@@ -147,6 +158,12 @@ __device__ __forceinline__ bool all_finite(const double* x) {
 // d_ij memo across identical-state stages (EF_MEMO_D, default on)
 #ifndef EF_MEMO_D
 #define EF_MEMO_D 1
+#endif
+#ifndef EF_WL
+#define EF_WL 1
+#endif
+#ifndef EF_WL_GRID
+#define EF_WL_GRID 1184  // 8 resident-size waves of 148 SMs
 #endif
 #ifndef EF_TAG_EXIT
 #define EF_TAG_EXIT 1
@@ -165,11 +182,6 @@ constexpr double kZeroP = -1.0;
 #define EF_PF_LIM 131072
 #endif
 __device__ __forceinline__ void pf_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
-
-// k_edge_visc reads RN(1/rho) of both rows from step0 instead of dividing
-#ifndef EF_RINV
-#define EF_RINV 0
-#endif
 
 // ---------------------------------------------------------------- state I/O
 template <int D>
@@ -212,7 +224,6 @@ __device__ __forceinline__ void nodal_one(const double* Ui, const Gas& g, Work& 
 #pragma unroll
   for (int a = 0; a < D; ++a) w.vp[a * NP + i] = qdiv(Ui[1 + a], rr);  // physics.py:157
   w.vp[D * NP + i] = g.gm1 * eps;                                        // physics.py:94
-  if (EF_RINV) w.rinv[i] = rr.y;
 }
 
 template <int D>
@@ -278,12 +289,7 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_EDGE(D), D)) k_edge
     w.nonuni[i] = 1;
     w.nonuni[j] = 1;
   }
-  double yij[2];
-  if (EF_RINV) {
-    yij[0] = w.rinv[i];
-    yij[1] = w.rinv[j];
-  }
-  const double dv = d_ij_geo<D>(Ui, Uj, nij, norm_ij, nji, norm_ji, g, bad, UNI && same, EF_RINV ? yij : nullptr);
+  const double dv = d_ij_geo<D>(Ui, Uj, nij, norm_ij, nji, norm_ji, g, bad, UNI && same);
   // d is symmetric by construction (riemann.py:139-142): the value is also
   // the lower-triangle entry of row j, written straight to its slot (the
   // reference's mirror, stepper.py:427-434, without a gather)
@@ -675,7 +681,7 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_LOW(D), D)) k_low_o
 template <int D, bool FIRST, bool UNI>
 __device__ __forceinline__ void edge_lim_one(const Layout& m, const Gas& g, const double* __restrict__ U,
                                              const Work& w, const StageParams& sp, int q, int p, int j,
-                                             int pt) {
+                                             int pt, int e) {
   constexpr int NV = D + 2;
   const int i = (int)fdiv((uint32_t)p, m.slab) * 32 + (p & 31);
   const int NP = (int)m.NP;
@@ -766,8 +772,11 @@ __device__ __forceinline__ void edge_lim_one(const Layout& m, const Gas& g, cons
   load_node<NV>(w.Unext, NP, j, Un);
   const double lj = limiter<D>(Un, Pj, w.bounds[j], w.bounds[NP + j], w.bounds[2 * NP + j], sp.newton, g);
   double* __restrict__ ml = last ? w.ml2 : w.ml;
-  ml[p] = npmin(li, lj);   // row i: np.minimum(l_ij, l_ji)
+  const double mlv = npmin(li, lj);
+  ml[p] = mlv;             // row i: np.minimum(l_ij, l_ji)
   ml[pt] = npmin(lj, li);  // row j: np.minimum(l_ji, l_ij)
+  // the pass before the last lists the edges the last pass has work for
+  if (EF_WL && q == sp.passes - 2) wl_append(mlv != 1.0, e, w.wl, w.wl_n);
 }
 
 template <int D, bool FIRST, bool UNI>
@@ -791,7 +800,20 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ELIM(D, FIRST), D))
     const double mli = w.ml[p];
     if (mli < 0.0 || (EF_ZSKIP && mli == 1.0 && q == sp.passes - 1)) return;
   }
-  edge_lim_one<D, FIRST, UNI>(m, g, U, w, sp, q, p, m.edge_j[e], m.edge_pt[e]);
+  edge_lim_one<D, FIRST, UNI>(m, g, U, w, sp, q, p, m.edge_j[e], m.edge_pt[e], e);
+}
+
+// The last limiter pass over the worklist (grid-stride over its device-side
+// count): every other edge has min(l) == 1 or a kZeroP tag from the pass before,
+// i.e. nothing to do in the last pass (see k_edge_lim).
+template <int D>
+__global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ELIM(D, false), D))
+    k_edge_lim_last(Layout m, Gas g, const double* __restrict__ U, Work w, StageParams sp, int q) {
+  const int n = *w.wl_n;
+  for (int t = blockIdx.x * EF_TPB_D(D) + threadIdx.x; t < n; t += gridDim.x * EF_TPB_D(D)) {
+    const int e = w.wl[t];
+    edge_lim_one<D, false, false>(m, g, U, w, sp, q, m.edges[e], m.edge_j[e], m.edge_pt[e], e);
+  }
 }
 
 // step5 (non-final pass): U_next_i += lam_i * sum_s min(l) P in slot order
@@ -1019,12 +1041,16 @@ void launch_low_order(int dim, const Layout& m, const Gas& g, const double* U, W
                       StageParams sp, RowSet rs, cudaStream_t st) {
   EF_DISPATCH_STAGE(dim, k_low_order, rs.n > 0 ? rs.n : 1, m, g, U, w, sp, rs);
 }
+bool edge_lim_worklist() { return EF_WL != 0; }
+
 template <int D>
 static void edge_lim_launch(const Layout& m, const Gas& g, const double* U, Work w, StageParams sp, int q,
                             cudaStream_t st) {
   constexpr int tb = D == 3 ? EF_TPB3 : EF_TPB2;
   const unsigned grid = grid_d(D, m.n_edges);
-  if (q > 0) k_edge_lim<D, false, false><<<grid, tb, 0, st>>>(m, g, U, w, sp, q);
+  if (EF_WL && q > 0 && q == sp.passes - 1)
+    k_edge_lim_last<D><<<grid < EF_WL_GRID ? grid : EF_WL_GRID, tb, 0, st>>>(m, g, U, w, sp, q);
+  else if (q > 0) k_edge_lim<D, false, false><<<grid, tb, 0, st>>>(m, g, U, w, sp, q);
   else if (sp.uni) k_edge_lim<D, true, true><<<grid, tb, 0, st>>>(m, g, U, w, sp, q);
   else k_edge_lim<D, true, false><<<grid, tb, 0, st>>>(m, g, U, w, sp, q);
 }

@@ -72,7 +72,6 @@ struct Work {
   double* eor;       // [NP]
   double* phi;       // [NP]
   double* vp;        // [(D+1)*NP] v = m / rho (D comps), p = gm1 * eps: the flux inputs
-  double* rinv;      // [NP] RN(1 / rho) of step0 (k_edge_visc's shared reciprocal)
   double* alpha;     // [NP]
   double* R;         // [NV][NP]
   double* Unext;     // [NV][NP]
@@ -87,6 +86,8 @@ struct Work {
                      // (identical-state) stage: d_ij of two unchanged rows is kept
   uint8_t* pnz;      // [NP] (identical-state stages) 1 if some P_ij of the row may be nonzero;
                      // 0: every edge of the row took the first pass's P = 0 shortcut
+  int* wl;           // [n_edges] worklist of the last limiter pass: the edges whose min(l)
+  int* wl_n;         // came out below 1 in the pass before it (count in wl_n)
   double* lz;        // [NP] first-pass marker: not NaN if the row took k_low_order's uniform
                      // shortcut (owned rows; an edge between two such rows has P = 0)
   unsigned long long* tau_min_bits;  // CFL min over owned rows
@@ -146,6 +147,9 @@ void launch_low_order(int dim, const Layout& m, const Gas& g, const double* U, W
 // steps 4-5: P (q = 0) and min(l_ij, l_ji) of limiter pass q, one thread per edge
 void launch_edge_lim(int dim, const Layout& m, const Gas& g, const double* U, Work w,
                      StageParams sp, int q, cudaStream_t st);
+// true if the last limiter pass runs over the worklist (EF_WL); the pass before it
+// then needs *wl_n cleared first
+bool edge_lim_worklist();
 // step5: non-final pass row update U_next += lam * sum min(l) P
 void launch_row_upd(int dim, const Layout& m, const Gas& g, const double* U, Work w,
                     StageParams sp, RowSet rs, cudaStream_t st);
