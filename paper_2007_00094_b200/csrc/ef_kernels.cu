@@ -776,7 +776,13 @@ __device__ __forceinline__ void edge_lim_one(const Layout& m, const Gas& g, cons
   ml[p] = mlv;             // row i: np.minimum(l_ij, l_ji)
   ml[pt] = npmin(lj, li);  // row j: np.minimum(l_ji, l_ij)
   // the pass before the last lists the edges the last pass has work for
-  if (EF_WL && q == sp.passes - 2) wl_append(mlv != 1.0, e, w.wl, w.wl_n);
+  if (EF_WL && q == sp.passes - 2) {
+    wl_append(mlv != 1.0, e, w.wl, w.wl_n);
+    if (mlv != 1.0) {
+      w.lrow[i] = 1;
+      w.lrow[j] = 1;
+    }
+  }
 }
 
 template <int D, bool FIRST, bool UNI>
@@ -874,7 +880,14 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_FINAL(D), D)) k_fin
 #pragma unroll
     for (int k = 0; k < NV; ++k) upd[k] = 0.0;
     const bool rescale = sp.passes >= 2;  // P of the last pass = P_(q-1) (1 - min l_(q-1))
-    const int nslots = (EF_UNIFORM_ROWS && sp.uni && !w.pnz[i]) ? 0 : card;  // all P zero (k_row_upd)
+    // all P zero (k_row_upd), or (worklist) no slot of the row has min(l) < 1
+    // in the pass before the last: every rescaled term is +-0 or a tagged zero
+    // (a zero-P row never gets an lrow mark: all its edges are tagged)
+    const bool zrow = EF_UNIFORM_ROWS && sp.uni && !w.pnz[i];
+    const bool lr = EF_WL && rescale && !zrow;
+    const bool need = !zrow && (!lr || w.lrow[i]);
+    if (lr && need) w.lrow[i] = 0;  // cleared for the next stage
+    const int nslots = need ? card : 0;
     EF_UNROLL_FINAL
     for (int s = 0; s < nslots; ++s) {
       if (s == dg) continue;

@@ -88,6 +88,8 @@ struct Work {
                      // 0: every edge of the row took the first pass's P = 0 shortcut
   int* wl;           // [n_edges] worklist of the last limiter pass: the edges whose min(l)
   int* wl_n;         // came out below 1 in the pass before it (count in wl_n)
+  uint8_t* lrow;     // [NP] 1 if the row is an end of a worklist edge (k_final's rescaled
+                     // slot terms are nonzero only there); cleared by k_final
   double* lz;        // [NP] first-pass marker: not NaN if the row took k_low_order's uniform
                      // shortcut (owned rows; an edge between two such rows has P = 0)
   unsigned long long* tau_min_bits;  // CFL min over owned rows
