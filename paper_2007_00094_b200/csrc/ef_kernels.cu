@@ -49,7 +49,7 @@ constexpr int TPB = EF_TPB;  // state I/O, halo and pow kernels
 #define EF_MINB 8
 #endif
 #ifndef EF_MINB_EDGE2
-#define EF_MINB_EDGE2 8
+#define EF_MINB_EDGE2 9
 #endif
 #ifndef EF_MINB_ROW2
 #define EF_MINB_ROW2 EF_MINB
