@@ -359,7 +359,10 @@ __device__ __forceinline__ void row_pipe(const int* __restrict__ col, int base, 
 #ifndef EF_VP
 #define EF_VP 1
 #endif
-#define EF_VP_ROW(D) (EF_VP && (D) == 2)
+#ifndef EF_VP_ROW3
+#define EF_VP_ROW3 0
+#endif
+#define EF_VP_ROW(D) (EF_VP && ((D) == 2 || EF_VP_ROW3))
 #define EF_VP_LOW(D) (EF_VP != 0)
 template <int D, bool USE>
 __device__ __forceinline__ void node_flux(const double* Ui, const Work& w, int NP, int i, const Gas& g,
