@@ -11,6 +11,7 @@
 //   k_edge_lim(q)  = step4 (q = 0: P_ij, P_ji built from R, U, d, alpha, m) and the
 //                    limiter of pass q for both rows of an edge + min(l_ij, l_ji)
 //                    (:456-474, :478-479, :485-491), one thread per edge
+//   k_edge_lim_last = the last pass over the worklist the pass before it built
 //   k_row_upd      = step5 non-final limited update (:480-481), one thread per row
 //   k_final        = step6 final pass + _k_boundary + _finish_step check
 //                    + SSP-RK3 combination + next stage's step0 (:493-504, :612-636, :399-405)
@@ -23,6 +24,14 @@
 // and k_nodal) caches v = m / rho and p for the neighbour fluxes.  Variants
 // measured slower (row groups, slot-parallel and row-owned limiters, half-edge
 // limiter, PDL, ...) are listed in DESIGN.md §6.
+// Exact fast paths (every one returns the bits of the full computation; DESIGN
+// §6): min(l) == 1 makes the next P zero (later passes tag such slots kZeroP
+// instead of limiting them, the last pass only visits a worklist of min(l) < 1
+// edges, k_final only rows that have one); identical states (U_i == U_j bit for
+// bit) give a closed-form lambda, uniform stencils skip the indicator and
+// low-order loops and zero the first pass's P, unchanged rows keep their d_ij
+// (the *<..., UNI> variants, chosen per step from a sampled count); in 3D the
+// limiter accepts t_R from an fp32 bound of the pow when the margin is clear.
 #include "ef_kernels.cuh"
 
 namespace ef {
