@@ -97,7 +97,10 @@ constexpr int TPB = EF_TPB;  // state I/O, halo and pow kernels
 #define EF_MINB_UPD 10
 #endif
 #define EF_MINB_PASS(D) EF_MINB_UPD
-#define EF_MINB_FINAL(D) ((D) == 3 ? 6 : EF_MINB)
+#ifndef EF_MINB_FINAL3
+#define EF_MINB_FINAL3 8  // 3D k_final at 8 resident blocks: -11% (from 6)
+#endif
+#define EF_MINB_FINAL(D) ((D) == 3 ? EF_MINB_FINAL3 : EF_MINB)
 // unroll factors of the per-row slot loops (lets ptxas hoist later slots' loads)
 #define EF_STR(x) #x
 #define EF_PRAGMA(x) _Pragma(EF_STR(x))
