@@ -186,6 +186,11 @@ __device__ __forceinline__ bool all_finite(const double* x) {
 // min(l) slot tag: this slot's P is zero for the current and all later passes
 // (set instead of storing zero P; a genuine min(l) is in [0, 1])
 constexpr double kZeroP = -1.0;
+// frozen rows (uniform and unchanged since the previous identical-state stage)
+// skip k_row_visc / k_low_order (EF_FROZEN, default on)
+#ifndef EF_FROZEN
+#define EF_FROZEN 1
+#endif
 // P = 0 shortcut of the limiter passes after the first (EF_ZSKIP, default on)
 #ifndef EF_ZSKIP
 #define EF_ZSKIP 1
@@ -397,7 +402,15 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ROW(D), D)) k_row_v
   const int i = act ? rs.row(t0) : 0;
   double cand = __longlong_as_double(0x7ff0000000000000LL);
   bool bad = false;
-  if (act) {
+  // frozen row: uniform stencil and state unchanged since the previous
+  // (identical-state) stage -- then so are all its neighbours, all its d_ij
+  // (memo), its alpha (0) and d_ii: only the CFL candidate is formed again
+  const bool frozen = act && EF_FROZEN && uni_on && !w.nonuni[i] && !w.chg[i];
+  if (frozen && want_tau) {
+    const double dii = w.d[sidx32(i, m.diag[i], m.L)];
+    if (dii < 0.0) cand = m.m_i[i] / (-2.0 * dii);
+  }
+  if (act && !frozen) {
     const int NP = (int)m.NP;
     const int L = m.L;
     const int NPL = NP * L;
@@ -575,6 +588,13 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_LOW(D), D)) k_low_o
   }
   if (t0 >= rs.n) return;
   const int i = rs.row(t0);
+  if (EF_FROZEN && sp.uni && !w.nonuni[i] && !w.chg[i]) {
+    // frozen row (see k_row_visc): U^L, R, bounds, the lz marker and the zero-P
+    // mark from the previous stage are this stage's values (U^L = U + (+0) does
+    // not depend on tau); only the shortcut count is kept up
+    if (sp.tau_mode != TAU_DEVICE && (blockIdx.x & 7) == 0) count_hits(true, w.n_same);
+    return;
+  }
   const int NP = (int)m.NP;
   const int L = m.L;
   const int NPL = NP * L;
