@@ -551,8 +551,8 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
   EF_TRY(h->alloc(&w.lrow, NP));
   EF_CUDA(cudaMemset(w.lrow, 0, NP));
   EF_CUDA(cudaMemset(w.wl_n, 0, sizeof(int)));
-  EF_TRY(h->alloc(&w.lz, NP));
-  EF_CUDA(cudaMemset(w.lz, 0, sizeof(double) * NP));
+  EF_TRY(h->alloc(&w.ust, NP));
+  EF_CUDA(cudaMemset(w.ust, 0, NP));
   EF_TRY(h->alloc(&w.tau_min_bits, 1));
   EF_TRY(h->alloc(&w.tau, 1));
   EF_TRY(h->alloc(&w.err, 1));

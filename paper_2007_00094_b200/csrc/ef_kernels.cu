@@ -589,10 +589,11 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_LOW(D), D)) k_low_o
   if (t0 >= rs.n) return;
   const int i = rs.row(t0);
   if (EF_FROZEN && sp.uni && !w.nonuni[i] && !w.chg[i]) {
-    // frozen row (see k_row_visc): U^L, R, bounds, the lz marker and the zero-P
-    // mark from the previous stage are this stage's values (U^L = U + (+0) does
-    // not depend on tau); only the shortcut count is kept up
+    // frozen row (see k_row_visc): U^L, R, bounds and the zero-P mark from the
+    // previous stage are this stage's values (U^L = U + (+0) does not depend on
+    // tau); only the shortcut count and the row status are kept up
     if (sp.tau_mode != TAU_DEVICE && (blockIdx.x & 7) == 0) count_hits(true, w.n_same);
+    w.ust[i] = 2;
     return;
   }
   const int NP = (int)m.NP;
@@ -696,7 +697,7 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_LOW(D), D)) k_low_o
   if (EF_UNIFORM_ROWS && sp.uni && sp.passes > 0) {
     // first-pass factor of the edges between two uniform rows (their P is +-0,
     // R_i = R_j = +0 and U_j = U_i): limiter(U^L_i, 0, bounds_i); NaN = no shortcut
-    w.lz[i] = uni ? 0.0 : __longlong_as_double(0x7ff8000000000000LL);
+    w.ust[i] = uni ? 1 : 0;
     w.pnz[i] = 0;  // the first limiter pass marks the rows of every edge it computes
   }
   // uniform rows (keep the shortcuts on): sampled like k_edge_visc's count
@@ -723,13 +724,15 @@ __device__ __forceinline__ void edge_lim_one(const Layout& m, const Gas& g, cons
   const size_t NPL = (size_t)NP * m.L;
   double Pi[NV], Pj[NV];
   if (FIRST && UNI && EF_UNIFORM_ROWS) {
-    // both rows took k_low_order's uniform shortcut (lz not NaN; owned rows):
+    // both rows took k_low_order's uniform shortcut (ust >= 1; owned rows):
     // R_i = R_j = +0 and U_j = U_i, so P_ij and P_ji are +-0 and stay zero in
     // every pass; each later use of the slots' factors multiplies a zero P
     const int no = (int)m.n_owned;
     if (i < no && j < no) {
-      const double li = w.lz[i], lj = w.lz[j];
-      if (li == li && lj == lj) {
+      const int si = w.ust[i], sj = w.ust[j];
+      if (si && sj) {
+        // two frozen rows: the previous stage already tagged the slots
+        if (si == 2 && sj == 2) return;
         // no P store and no limiter: the slots are tagged kZeroP instead of min(l)
         double* __restrict__ mo = sp.passes == 1 ? w.ml2 : w.ml;
         mo[p] = kZeroP;

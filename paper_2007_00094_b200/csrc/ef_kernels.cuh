@@ -90,8 +90,8 @@ struct Work {
   int* wl_n;         // came out below 1 in the pass before it (count in wl_n)
   uint8_t* lrow;     // [NP] 1 if the row is an end of a worklist edge (k_final's rescaled
                      // slot terms are nonzero only there); cleared by k_final
-  double* lz;        // [NP] first-pass marker: not NaN if the row took k_low_order's uniform
-                     // shortcut (owned rows; an edge between two such rows has P = 0)
+  uint8_t* ust;      // [NP] k_low_order's row status for the first limiter pass: 0 general,
+                     // 1 uniform-stencil shortcut (R = 0), 2 frozen (also unchanged)
   unsigned long long* tau_min_bits;  // CFL min over owned rows
   double* tau;       // tau of the current RK step / Euler step
   int* err;          // bit0 projection/entropy, bit1 inadmissible result, bit2 tau unbounded
