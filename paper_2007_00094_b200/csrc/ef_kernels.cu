@@ -177,9 +177,6 @@ __device__ __forceinline__ bool all_finite(const double* x) {
 #ifndef EF_WL_GRID
 #define EF_WL_GRID 1184  // 8 resident-size waves of 148 SMs
 #endif
-#ifndef EF_TAG_EXIT
-#define EF_TAG_EXIT 1
-#endif
 #ifndef EF_PF_VISC_UNI
 #define EF_PF_VISC_UNI 131072  // (the memo check makes the identical-state variant latency-bound: -6%)
 #endif
