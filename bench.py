@@ -1,6 +1,6 @@
 """Benchmark: fp64 Q1 node-updates per second per SSP-RK3 stage (BASELINE.json).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c1|c3|c5] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c1|c3|c3m|c4m|c5|c5m] [--impl ours|reference]
 
 Workload (config.workload): BASELINE.json configs[1], the 2D Mach-3 flow past
 a disc, ~1.24M Q1 nodes, seeded shuffled node ids (the solver applies RCM),
@@ -8,12 +8,14 @@ synthetic (generated mesh + free-stream initial state; no dataset exists).
 A step is one SSP-RK3 step (3 forward-Euler stages) over the whole mesh.
 
 value     device-resident throughput: N_nodes * 3 * K / (CUDA-event time of K
-          RK steps on the launching stream), max over ranks.
+          RK steps on the launching stream), max over ranks; the library's
+          default path (exact identical-state fast paths chosen per step).
+general_path  the same metric over K/4 steps with those fast paths forced off.
 e2e       the same metric through the public API with host buffers: every step
           set_state(pinned host U) -> ssp_rk3_step() -> get_state(pinned host U).
-roofline  dominant kernel (per-phase CUDA-event timing pass): algorithmic bytes
-          from the reference's traffic model (perf.py:47-89) / kernel time,
-          against MEASURED_PEAKS.json hbm_gbs.
+roofline  dominant kernel (per-phase CUDA-event timing pass on the general
+          path): algorithmic bytes from the reference's traffic model
+          (perf.py:47-89) / kernel time, against MEASURED_PEAKS.json hbm_gbs.
 cpu_baseline  the CPU oracle (C restatement of the reference stage, all host
           threads) on a bounded sample of the same workload.
 --impl reference  times that CPU port alone (the reference itself is pure
