@@ -548,8 +548,8 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
   EF_CUDA(cudaMemset(w.pnz, 1, NP));
   EF_TRY(h->alloc(&w.wl, std::max<int64_t>(h->lay.n_edges, 1)));
   EF_TRY(h->alloc(&w.wl_n, 1));
-  EF_TRY(h->alloc(&w.lrow, NP));
-  EF_CUDA(cudaMemset(w.lrow, 0, NP));
+  EF_TRY(h->alloc(&w.lmask, NP));
+  EF_CUDA(cudaMemset(w.lmask, 0, sizeof(unsigned long long) * NP));
   EF_CUDA(cudaMemset(w.wl_n, 0, sizeof(int)));
   EF_TRY(h->alloc(&w.ust, NP));
   EF_CUDA(cudaMemset(w.ust, 0, NP));

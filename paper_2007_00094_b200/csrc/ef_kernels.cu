@@ -813,9 +813,10 @@ __device__ __forceinline__ void edge_lim_one(const Layout& m, const Gas& g, cons
   // the pass before the last lists the edges the last pass has work for
   if (EF_WL && q == sp.passes - 2) {
     wl_append(mlv != 1.0, e, w.wl, w.wl_n);
-    if (mlv != 1.0) {
-      w.lrow[i] = 1;
-      w.lrow[j] = 1;
+    if (mlv != 1.0 && m.L <= 64) {  // the slots of this edge in rows i and j
+      const int sL = 32 * m.L;
+      atomicOr(w.lmask + i, 1ull << ((p - (i >> 5) * sL) >> 5));
+      atomicOr(w.lmask + j, 1ull << ((pt - (j >> 5) * sL) >> 5));
     }
   }
 }
@@ -915,31 +916,41 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_FINAL(D), D)) k_fin
 #pragma unroll
     for (int k = 0; k < NV; ++k) upd[k] = 0.0;
     const bool rescale = sp.passes >= 2;  // P of the last pass = P_(q-1) (1 - min l_(q-1))
-    // all P zero (k_row_upd), or (worklist) no slot of the row has min(l) < 1
-    // in the pass before the last: every rescaled term is +-0 or a tagged zero
-    // (a zero-P row never gets an lrow mark: all its edges are tagged)
+    // all P zero (k_row_upd), or (worklist) only the slots of the row's
+    // worklist edges -- min(l) < 1 in the pass before the last -- can carry a
+    // nonzero rescaled term; the others add +-0 or are tagged zeros.  Their
+    // bits are visited in increasing slot order, the order of the full loop.
+    // (a zero-P row never gets a mask bit: all its edges are tagged)
     const bool zrow = EF_UNIFORM_ROWS && sp.uni && !w.pnz[i];
-    const bool lr = EF_WL && rescale && !zrow;
-    const bool need = !zrow && (!lr || w.lrow[i]);
-    if (lr && need) w.lrow[i] = 0;  // cleared for the next stage
-    const int nslots = need ? card : 0;
-    EF_UNROLL_FINAL
-    for (int s = 0; s < nslots; ++s) {
-      if (s == dg) continue;
+    const bool lr = EF_WL && rescale && !zrow && L <= 64;
+    unsigned long long mk = 0;
+    if (lr) {
+      mk = w.lmask[i];
+      if (mk) w.lmask[i] = 0;  // cleared for the next stage
+    }
+    const int nslots = (zrow || lr) ? 0 : card;
+    auto term = [&](int s) {
       const int p = base + s * 32;
       const double mlp = rescale ? w.ml[p] : 0.0;
       const double gp = rescale ? 1.0 - mlp : 1.0;
       // gp == 0: the term is ml2 * (P * 0) = +-0 (P finite), and adding +-0 to a
       // sum that starts at +0 never changes it (it cannot become -0); kZeroP
       // slots (negative tag) carry a zero P
-      if ((EF_ZSKIP && gp == 0.0) || mlp < 0.0) continue;
+      if ((EF_ZSKIP && gp == 0.0) || mlp < 0.0) return;
       const double ml = w.ml2[p];
-      if (ml < 0.0) continue;  // kZeroP from a single-pass first limiter
+      if (ml < 0.0) return;  // kZeroP from a single-pass first limiter
 #pragma unroll
       for (int k = 0; k < NV; ++k) {
         const double Pk = rescale ? w.P[(size_t)k * NPL + p] * gp : w.P[(size_t)k * NPL + p];
         upd[k] = upd[k] + ml * Pk;
       }
+    };
+    EF_UNROLL_FINAL
+    for (int s = 0; s < nslots; ++s)
+      if (s != dg) term(s);
+    while (mk) {
+      term(__ffsll((long long)mk) - 1);
+      mk &= mk - 1;
     }
     const double lam = m.lam[i];
 #pragma unroll

@@ -88,8 +88,8 @@ struct Work {
                      // 0: every edge of the row took the first pass's P = 0 shortcut
   int* wl;           // [n_edges] worklist of the last limiter pass: the edges whose min(l)
   int* wl_n;         // came out below 1 in the pass before it (count in wl_n)
-  uint8_t* lrow;     // [NP] 1 if the row is an end of a worklist edge (k_final's rescaled
-                     // slot terms are nonzero only there); cleared by k_final
+  unsigned long long* lmask;  // [NP] bit s: slot s of the row belongs to a worklist edge (its
+                              // k_final rescaled term can be nonzero); cleared by k_final
   uint8_t* ust;      // [NP] k_low_order's row status for the first limiter pass: 0 general,
                      // 1 uniform-stencil shortcut (R = 0), 2 frozen (also unchanged)
   unsigned long long* tau_min_bits;  // CFL min over owned rows
