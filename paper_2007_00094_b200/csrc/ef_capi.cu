@@ -752,7 +752,7 @@ static int run_stage(Driver& d, const std::vector<StageIO>& io, StageParams sp) 
     EF_TRY(mark(t, 5));
     for (int p = 0; p + 1 < t->passes; ++p) {
       EF_TRY(produce([&](ef_solver* h, const StageIO& x, ef::RowSet rs) {
-        ef::launch_row_upd(h->dim, h->lay, h->gas, x.U, h->w, sp, rs, st);
+        ef::launch_row_upd(h->dim, h->lay, h->gas, x.U, h->w, sp, rs, p, st);
       }, {fld(&Work::Unext, NV)}));
       EF_TRY(clear_wl(p + 1));
       each([&](ef_solver* h, const StageIO& x) { ef::launch_edge_lim(h->dim, h->lay, h->gas, x.U, h->w, sp, p + 1, st); });

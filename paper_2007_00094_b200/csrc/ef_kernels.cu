@@ -862,7 +862,7 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ELIM(D, false), D))
 // (stepper.py:478-481); the rescale of P belongs to the next k_edge_lim.
 template <int D>
 __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_PASS(D), D)) k_row_upd(Layout m, Gas g, const double* __restrict__ U,
-                                                                Work w, StageParams sp, RowSet rs) {
+                                                                Work w, StageParams sp, RowSet rs, int use_mask) {
   constexpr int NV = D + 2;
   const int t0 = blockIdx.x * EF_TPB_D(D) + threadIdx.x;
   if (t0 >= rs.n) return;
@@ -878,11 +878,16 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_PASS(D), D)) k_row_
   // every P of the row is the first pass's stored +0 (kept zero by later
   // passes): each term is +-0 and the sums stay +0, so the loop is skipped
   const int nslots = (EF_UNIFORM_ROWS && sp.uni && !w.pnz[i]) ? 0 : card;
+  // use_mask: the pass just done built the slot masks (k_final's) and left no
+  // kZeroP tags (first of two passes, no identical-state shortcuts): a slot
+  // outside the mask has min(l) == 1 exactly, and 1.0 * P == P, so its factor
+  // is not loaded
+  const unsigned long long mk = use_mask ? w.lmask[i] : 0ull;
   EF_UNROLL_PASS1
   for (int s = 0; s < nslots; ++s) {
     if (s == dg) continue;
     const int p = base + s * 32;
-    const double ml = w.ml[p];
+    const double ml = (use_mask && !((mk >> s) & 1ull)) ? 1.0 : w.ml[p];
     if (ml < 0.0) continue;  // kZeroP: the term is ml * (+-0)
 #pragma unroll
     for (int k = 0; k < NV; ++k) upd[k] = upd[k] + ml * w.P[(size_t)k * NPL + p];
@@ -1121,9 +1126,12 @@ void launch_edge_lim(int dim, const Layout& m, const Gas& g, const double* U, Wo
   else edge_lim_launch<3>(m, g, U, w, sp, q, st);
 }
 void launch_row_upd(int dim, const Layout& m, const Gas& g, const double* U, Work w,
-                    StageParams sp, RowSet rs, cudaStream_t st) {
+                    StageParams sp, RowSet rs, int q, cudaStream_t st) {
   if (rs.n == 0) return;
-  EF_DISPATCH_STAGE(dim, k_row_upd, rs.n, m, g, U, w, sp, rs);
+  // (two passes: the mask-building pass is the first, which tags only in the
+  // identical-state mode; a middle pass of three or more tags its P = 0 slots)
+  const int use_mask = (EF_WL && !sp.uni && sp.passes == 2 && q == 0 && m.L <= 64) ? 1 : 0;
+  EF_DISPATCH_STAGE(dim, k_row_upd, rs.n, m, g, U, w, sp, rs, use_mask);
 }
 void launch_final(int dim, const Layout& m, const Gas& g, const double* U, const double* U0,
                   double* Uout, Work w, StageParams sp, RowSet rs, cudaStream_t st) {

@@ -154,7 +154,7 @@ void launch_edge_lim(int dim, const Layout& m, const Gas& g, const double* U, Wo
 bool edge_lim_worklist();
 // step5: non-final pass row update U_next += lam * sum min(l) P
 void launch_row_upd(int dim, const Layout& m, const Gas& g, const double* U, Work w,
-                    StageParams sp, RowSet rs, cudaStream_t st);
+                    StageParams sp, RowSet rs, int q, cudaStream_t st);
 void launch_final(int dim, const Layout& m, const Gas& g, const double* U, const double* U0,
                   double* Uout, Work w, StageParams sp, RowSet rs, cudaStream_t st);
 void launch_pow(const double* x, double y, double* out, int64_t n, cudaStream_t st);
