@@ -112,3 +112,20 @@ def test_c5_full_size_conservation_and_bounds():
     s.euler_step()
     _stage_bounds_hold(s, 3)
     s.close()
+
+
+def test_c2_full_run_fast_paths_are_exact(c2):
+    """Full C2 over the benchmark's 200 steps: the default path (identical-state
+    fast paths, frozen rows, d_ij memo, zero-P tags) and the general path give
+    the same tau sequence and the same final state, bit for bit."""
+    ps = c2
+    runs = []
+    for mode in (-1, 0):
+        s = Solver(ps.matrices, c_cfl=ps.c_cfl, boundary=ps.boundary)
+        s.set_uniform_shortcuts(mode)
+        s.set_state(ps.U0)
+        taus = [s.ssp_rk3_step() for _ in range(200)]
+        runs.append((taus, s.get_state()))
+        s.close()
+    assert runs[0][0] == runs[1][0]
+    assert np.array_equal(runs[0][1], runs[1][1])
