@@ -227,6 +227,8 @@ static Gas make_gas(const ef_params* p) {
   g.neg_gamma = -gamma;
   g.neg_g_gp1_inv = (-gamma) * p->gp1_inv;
   g.sqrt2 = std::sqrt(2.0);
+  const char* fa = std::getenv("EF_FAST_ACCEPT");  // results are identical either way
+  g.fast_accept = (fa && fa[0] == '0') ? 0 : 1;
   return g;
 }
 

@@ -129,3 +129,20 @@ def test_c2_full_run_fast_paths_are_exact(c2):
         s.close()
     assert runs[0][0] == runs[1][0]
     assert np.array_equal(runs[0][1], runs[1][1])
+
+
+@pytest.mark.parametrize("cfg,steps", [("c5m", 20), ("c3m", 20)])
+def test_3d_limiter_fast_accept_is_exact(cfg, steps, monkeypatch):
+    """3D: the limiter's fast accept (fp32 bound of the pow) on and off give the
+    same run bit for bit (160^3 periodic box, 1.05M-node Sod box)."""
+    ps = P.make_config(cfg)
+    runs = []
+    for fa in ("1", "0"):
+        monkeypatch.setenv("EF_FAST_ACCEPT", fa)
+        s = Solver(ps.matrices, c_cfl=ps.c_cfl, boundary=ps.boundary)
+        s.set_state(ps.U0)
+        taus = [s.ssp_rk3_step() for _ in range(steps)]
+        runs.append((taus, s.get_state()))
+        s.close()
+    assert runs[0][0] == runs[1][0]
+    assert np.array_equal(runs[0][1], runs[1][1])
