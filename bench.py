@@ -160,8 +160,8 @@ def run_reference(args, rank, world):
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus,
         "steps": steps, "warmup": 1, "ms_per_step": 1e3 * dt / steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": CONFIG_NAMES[args.config], "nodes": int(ps.matrices.n),
-                   "nnz": int(ps.matrices.nnz), "steps_per_sample": steps},
+        "config": {"workload": CONFIG_NAMES[args.config], "sample_nodes": int(ps.matrices.n),
+                   "sample_nnz": int(ps.matrices.nnz), "steps_per_sample": steps},
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"{steps} SSP-RK3 steps of the {CPU_SAMPLE_OF.get(args.config, args.config)} mesh "
                                    f"({ps.matrices.n} nodes), oracle/idp_oracle.c, {threads} threads"},
