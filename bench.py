@@ -1,16 +1,21 @@
 """Benchmark: fp64 Q1 node-updates per second per SSP-RK3 stage (BASELINE.json).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c1|c3|c3m|c4m|c5|c5m] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5|c5w|c1|c2|c3|c3m|c4m|c5m] [--impl ours|reference]
 
-Workload (config.workload): BASELINE.json configs[1], the 2D Mach-3 flow past
-a disc, ~1.24M Q1 nodes, seeded shuffled node ids (the solver applies RCM),
-synthetic (generated mesh + free-stream initial state; no dataset exists).
+Workload (config.workload): at N = 1 the largest single-GPU configuration of
+BASELINE.json, configs[4] at its 1-GPU point: the 3D periodic Q1 hex box 320^3
+(32.8M nodes, 885M stencil entries, 27-point stencil), seeded smooth random
+state from 8 Fourier modes, synthetic (generated mesh; no dataset exists).
+At N > 1 the default is the same config's weak-scaling series (`c5w`,
+n = round(320 N^(1/3)) per side: 403^3 / 508^3 / 640^3 at N = 2 / 4 / 8).
 A step is one SSP-RK3 step (3 forward-Euler stages) over the whole mesh.
 
 value     device-resident throughput: N_nodes * 3 * K / (CUDA-event time of K
           RK steps on the launching stream), max over ranks; the library's
-          default path (exact identical-state fast paths chosen per step).
-general_path  the same metric over K/4 steps with those fast paths forced off.
+          default path (exact identical-state fast paths chosen per step; on
+          C5 no state is ever bitwise identical to a neighbour's, so this is
+          the general path).
+general_path  the same metric over K/2 steps with those fast paths forced off.
 e2e       the same metric through the public API with host buffers: every step
           set_state(pinned host U) -> ssp_rk3_step() -> get_state(pinned host U).
 roofline  dominant kernel (per-phase CUDA-event timing pass on the general
@@ -42,6 +47,7 @@ sys.path.insert(0, os.path.join(ROOT, "oracle"))
 METRIC = "fp64 Q1 node-updates/sec per SSP-RK3 stage"
 UNIT = "node-updates/s"
 CONFIG_NAMES = {
+    "c5w": "C5 3D periodic Fourier box, weak scaling: round(320 N^(1/3))^3 nodes (~32.8M per GPU)",
     "c1": "C1 2D isentropic vortex 129x129, CFL 0.5",
     "c2": "C2 2D Mach-3 flow past a disc, ~1.24M Q1 nodes, shuffled ids + RCM",
     "c3": "C3 3D Sod box 512x128x128 (jittered)",
@@ -124,10 +130,28 @@ CPU_MAX_NODES = 5_000_000
 CPU_SAMPLE_OF = {"c3": "c3m", "c4": "c4m", "c5": "c5m"}
 
 
-def build_problem(name: str):
+def weak_side(world: int) -> int:
+    """C5 weak scaling (BASELINE configs[4]): 320^3 nodes per GPU."""
+    return int(round(320 * world ** (1.0 / 3.0)))
+
+
+def build_problem(name: str, world: int = 1):
     from paper_2007_00094_b200 import problems as P
 
+    if name == "c5w":
+        return P.periodic_fourier_box(weak_side(world))
     return P.make_config(name)
+
+
+def cpu_info() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def cpu_oracle_rate(ps, budget_s: float, threads: int, max_steps: int = 1000):
@@ -148,26 +172,63 @@ def cpu_oracle_rate(ps, budget_s: float, threads: int, max_steps: int = 1000):
     return ps.matrices.n * 3 * steps / dt, steps, dt
 
 
+def cpu_sample_problem(config: str):
+    """The bounded CPU sample of a config: the same generator at a size the
+    C port's host arrays (~3 KB/node) and a few minutes of CPU time allow."""
+    from paper_2007_00094_b200 import problems as P
+
+    if config in ("c5", "c5w", "c5m"):
+        return "the c5 generator at 128^3 (periodic Fourier box)", P.periodic_fourier_box(128)
+    name = CPU_SAMPLE_OF.get(config, config)
+    return f"the {name} mesh", build_problem(name)
+
+
 def run_reference(args, rank, world):
+    """--impl reference: the CPU port of the reference stage (oracle/idp_oracle.c;
+    the reference itself is pure Python and cannot travel to the GPU box) on all
+    host threads, W warm-up + K timed SSP-RK3 steps of the bounded sample, each
+    leg capped at ~2 minutes of wall time."""
     if rank != 0:
         return
-    ps = build_problem(CPU_SAMPLE_OF.get(args.config, args.config) if args.config in CPU_SAMPLE_OF
-                       else args.config)
+    import oracle as O
+
+    label, ps = cpu_sample_problem(args.config)
     threads = os.cpu_count() or 1
-    budget = max(10.0, min(120.0, 2.0 * args.steps))
-    rate, steps, dt = cpu_oracle_rate(ps, budget, threads, max_steps=max(1, args.steps))
+    o = O.OracleSolver(ps.matrices, c_cfl=ps.c_cfl, boundary=ps.boundary, threads=threads)
+    o.set_state(ps.U0)
+    warm = 0
+    t0 = time.perf_counter()
+    while warm < args.warmup and time.perf_counter() - t0 < 60.0:
+        o.ssp_rk3_step()
+        warm += 1
+    steps = 0
+    t0 = time.perf_counter()
+    while steps < max(1, args.steps):
+        o.ssp_rk3_step()
+        steps += 1
+        if time.perf_counter() - t0 >= 120.0:
+            break
+    dt = time.perf_counter() - t0
+    rate = ps.matrices.n * 3 * steps / dt
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": steps, "warmup": 1, "ms_per_step": 1e3 * dt / steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": CONFIG_NAMES[args.config], "sample_nodes": int(ps.matrices.n),
-                   "sample_nnz": int(ps.matrices.nnz), "steps_per_sample": steps},
-        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{steps} SSP-RK3 steps of the {CPU_SAMPLE_OF.get(args.config, args.config)} mesh "
-                                   f"({ps.matrices.n} nodes), oracle/idp_oracle.c, {threads} threads"},
+        "steps": steps, "warmup": warm, "ms_per_step": 1e3 * dt / steps, "higher_is_better": True,
+        "scaling": "weak" if args.config == "c5w" else "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": CONFIG_NAMES[args.config], "nodes": int(ps.matrices.n),
+                   "nnz": int(ps.matrices.nnz), "sample": label},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "port", "cpu": cpu_info(),
+                         "sample": f"{steps} SSP-RK3 steps of {label} ({ps.matrices.n} nodes) after {warm} "
+                                   f"warm-up steps, oracle/idp_oracle.c, {threads} threads"},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def kernel_launches() -> int:
+    from paper_2007_00094_b200 import _lib
+
+    return int(_lib.load().ef_kernel_launches())
 
 
 def run_ours(args, rank, world, local_rank):
@@ -178,7 +239,7 @@ def run_ours(args, rank, world, local_rank):
 
     dist = world > 1
     torch.cuda.set_device(local_rank)
-    ps = build_problem(args.config)
+    ps = build_problem(args.config, world)
     mat = ps.matrices
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
@@ -208,10 +269,12 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    launches0 = kernel_launches()
     e0.record(stream)
     for _ in range(args.steps):
         solver.ssp_rk3_step_async()
     e1.record(stream)
+    launches = kernel_launches() - launches0
     torch.cuda.synchronize()
     if dist:
         torch.distributed.barrier()
@@ -226,29 +289,29 @@ def run_ours(args, rank, world, local_rank):
     value = node_updates / (ms * 1e-3)
     ms_per_step = ms / args.steps
 
-    # the same steps with the identical-state shortcuts forced off:
-    # how much of `value` comes from uniform regions of the flow
-    general = None
-    if True:
-        gsteps = max(1, args.steps // 4)
-        solver.set_uniform_shortcuts(0)
-        for _ in range(2):
-            solver.ssp_rk3_step_async()
-        solver.sync()
-        torch.cuda.synchronize()
-        e0.record(stream)
-        for _ in range(gsteps):
-            solver.ssp_rk3_step_async()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        solver.sync()
-        gms = e0.elapsed_time(e1)
-        if dist:
-            t = torch.tensor([gms], device="cuda")
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            gms = float(t.item())
-        general = {"value": n_nodes * 3 * gsteps / (gms * 1e-3), "steps": gsteps,
-                   "note": "identical-state shortcuts off (exact either way); P=0 limiter skips stay on"}
+    # the same metric with the identical-state shortcuts forced off:
+    # how much of `value` comes from bitwise-uniform regions of the flow
+    gsteps = max(1, args.steps // 2)
+    solver.set_uniform_shortcuts(0)
+    for _ in range(2):
+        solver.ssp_rk3_step_async()
+    solver.sync()
+    if dist:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(gsteps):
+        solver.ssp_rk3_step_async()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    solver.sync()
+    gms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([gms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        gms = float(t.item())
+    general = {"value": n_nodes * 3 * gsteps / (gms * 1e-3), "steps": gsteps,
+               "note": "identical-state shortcuts off (exact either way); P=0 limiter skips stay on"}
 
     # per-phase kernel times: events between the kernels of every stage, no host
     # syncs inside the pass (the library folds them in when the timers are read).
@@ -279,7 +342,7 @@ def run_ours(args, rank, world, local_rank):
     achieved = phase_bytes[dom] / per_launch[dom] / 1e9
     stage_bytes = 8.0 * stage_doubles_per_nnz(dim, card, passes) * nnz
     stage_s = (ms * 1e-3) / (3 * args.steps)
-    gstage_s = 1.0 / (general["value"] / n_nodes) if general else stage_s  # seconds per stage
+    gstage_s = 1.0 / (general["value"] / n_nodes)  # seconds per stage
     traffic = None  # dram read + write bytes per launch from the committed ncu --set full capture
     prof = {}
     try:
@@ -299,7 +362,9 @@ def run_ours(args, rank, world, local_rank):
         "path": "general (identical-state shortcuts off; zero-P limiter skips and the 3D fast accept stay on)",
         "stage": {"algorithmic_bytes": stage_bytes, "achieved": stage_bytes / gstage_s / 1e9,
                   "frac": stage_bytes / gstage_s / 1e9 / peak, "timing": "general_path steps",
-                  "doubles_per_nnz": stage_doubles_per_nnz(dim, card, passes)},
+                  "doubles_per_nnz": stage_doubles_per_nnz(dim, card, passes),
+                  # the same model bytes over the headline `value`'s own stage time
+                  "frac_of_value": stage_bytes / stage_s / 1e9 / peak},
     }
 
     # e2e through the public API with pinned host buffers
@@ -322,7 +387,6 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     e2e_ms = e0.elapsed_time(e1)
-    e2e_ms = max(e2e_ms, wall * 1e3 * 0.0)
     if dist:
         t = torch.tensor([e2e_ms], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -331,11 +395,11 @@ def run_ours(args, rank, world, local_rank):
            "h2d_bytes_per_step": int(n_nodes * nv * 8), "d2h_bytes_per_step": int(n_nodes * nv * 8),
            "steps": e2e_steps, "wall_s": wall}
 
-    kernels_per_stage = 3 + (1 + 2 * max(passes - 1, 0) + 1 if passes > 0 else 1)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "weak" if args.config == "c5w" else "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
         "config": {"workload": CONFIG_NAMES[args.config], "nodes": int(n_nodes), "nnz_rank0": int(nnz),
                    "dim": dim, "pad_width": solver.pad_width, "standard_card": card,
                    "c_cfl": ps.c_cfl, "limiter_passes": passes, "newton_steps": solver.newton_steps,
@@ -345,22 +409,29 @@ def run_ours(args, rank, world, local_rank):
         "general_path": general,
         "e2e": e2e,
         "clocks": clocks,
-        "gpu_launches": int(args.steps * 3 * kernels_per_stage),
+        "gpu_launches": int(launches),
     }
     solver.close()
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
-        cfg = args.config
-        if n_nodes > CPU_MAX_NODES:  # the oracle's host memory: the same generator at mid size
-            del ps
-            cfg = CPU_SAMPLE_OF.get(args.config, args.config)
-            ps = build_problem(cfg)
+        if n_nodes > CPU_MAX_NODES:  # the oracle's host memory: the same generator at a bounded size
+            del ps, mat
+            label, ps = cpu_sample_problem(args.config)
+        else:
+            label = f"the {args.config} mesh"
         rate, steps, dt = cpu_oracle_rate(ps, args.cpu_seconds, threads, max_steps=args.steps)
+        # one host thread on a small instance of the same generator (the reference's
+        # default Solver(workers=1), stepper.py:96)
+        from paper_2007_00094_b200 import problems as P
+        small = P.periodic_fourier_box(48) if args.config.startswith("c5") else build_problem(
+            args.config if args.config == "c1" else "c1")
+        rate1, steps1, _ = cpu_oracle_rate(small, 0.5 * args.cpu_seconds, 1, max_steps=args.steps)
         line["cpu_baseline"] = {
-            "value": rate, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{steps} SSP-RK3 steps of the {cfg} mesh ({ps.matrices.n} nodes"
-                      f"{'' if cfg == args.config else ', the ' + args.config + ' generator at mid size'}) after 1 "
-                      f"warm-up step, oracle/idp_oracle.c (C restatement of the reference stage)"}
+            "value": rate, "unit": UNIT, "cores": threads, "kind": "port", "cpu": cpu_info(),
+            "sample": f"{steps} SSP-RK3 steps of {label} ({ps.matrices.n} nodes) after 1 warm-up step, "
+                      f"oracle/idp_oracle.c (C restatement of the reference stage), {threads} threads",
+            "workers_1": {"value": rate1, "cores": 1,
+                          "sample": f"{steps1} SSP-RK3 steps, {small.matrices.n} nodes, 1 thread"}}
     if rank == 0:
         print(json.dumps(line), flush=True)
 
@@ -368,9 +439,10 @@ def run_ours(args, rank, world, local_rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIG_NAMES))
+    ap.add_argument("--config", default=None, choices=sorted(CONFIG_NAMES),
+                    help="default: c5 (320^3) at N = 1, c5w (weak scaling) at N > 1")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
@@ -380,6 +452,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.config is None:
+        args.config = "c5" if world == 1 else "c5w"
     if args.impl == "reference":
         run_reference(args, rank, world)
         return

@@ -106,6 +106,9 @@ int ef_sync(ef_solver* h, double* tau_used);
 /* original id of the inadmissible node behind the last EF_ERR_INADMISSIBLE */
 int64_t ef_bad_node(const ef_solver* h);
 const char* ef_last_error(void);
+/* Number of kernels this process has launched through the library (all handles;
+ * a CUDA-graph replay counts the kernels it contains).  bench.py's gpu_launches. */
+int64_t ef_kernel_launches(void);
 
 /* Solver.timers (stepper.py:37, 515-607): seconds per phase step0..step6,
  * accumulated while timing is enabled (adds a sync per phase). */

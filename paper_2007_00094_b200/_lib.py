@@ -57,6 +57,7 @@ SIGNATURES = {
     "ef_sync": (_i32, [_p, ctypes.POINTER(_d)]),
     "ef_bad_node": (_i64, [_p]),
     "ef_last_error": (ctypes.c_char_p, []),
+    "ef_kernel_launches": (_i64, []),
     "ef_enable_timers": (_i32, [_p, _i32]),
     "ef_enable_graphs": (_i32, [_p, _i32]),
     "ef_set_uniform": (_i32, [_p, _i32]),

@@ -138,7 +138,7 @@ struct ef_solver {
   struct Readback {
     double tau;
     int err;
-    int pad;
+    int err_first;
     unsigned long long bad;
     unsigned long long n_same[ef::kSameSlots];
   }* rb = nullptr;
@@ -158,18 +158,19 @@ struct ef_solver {
   // CUDA graphs of whole steps (single rank, timers off): one launch replays the
   // ~25 kernels and memsets of an RK step.  Keyed by everything the captured
   // launches depend on; a few entries cover the rotating U buffers.
+  // (tau and tau_max are read by the kernels from Work::tau_arg, written before
+  // every launch, so they are not part of the key)
   struct GraphKey {
     int rk3, cur, has_tau, uni;
-    double tau, tau_max;
     bool operator==(const GraphKey& o) const {
-      return rk3 == o.rk3 && cur == o.cur && has_tau == o.has_tau && uni == o.uni &&
-             std::memcmp(&tau, &o.tau, sizeof tau) == 0 && std::memcmp(&tau_max, &o.tau_max, sizeof tau_max) == 0;
+      return rk3 == o.rk3 && cur == o.cur && has_tau == o.has_tau && uni == o.uni;
     }
   };
   struct GraphEntry {
     GraphKey key;
     cudaGraphExec_t exec;
     uint64_t used;
+    long long launches;  // kernels captured (added to the launch count per replay)
   };
   std::vector<GraphEntry> graphs;
   uint64_t graph_clock = 0;
@@ -558,7 +559,13 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
   EF_TRY(h->alloc(&w.tau_min_bits, 1));
   EF_TRY(h->alloc(&w.tau, 1));
   EF_TRY(h->alloc(&w.err, 1));
+  EF_TRY(h->alloc(&w.err_first, 1));
   EF_TRY(h->alloc(&w.bad_gid, 1));
+  EF_TRY(h->alloc(&w.tau_arg, 2));
+  EF_CUDA(cudaMemset(w.tau_arg, 0, 2 * sizeof(double)));
+  EF_CUDA(cudaMemset(w.err, 0, sizeof(int)));
+  EF_CUDA(cudaMemset(w.err_first, 0x7f, sizeof(int)));
+  EF_CUDA(cudaMemset(w.bad_gid, 0xff, sizeof(unsigned long long)));
   EF_TRY(h->alloc(&w.n_same, ef::kSameSlots));
   EF_CUDA(cudaMemset(w.n_same, 0, sizeof(unsigned long long) * ef::kSameSlots));
   EF_CUDA(cudaMemset(w.d, 0, sizeof(double) * NPL));
@@ -727,11 +734,11 @@ static int run_stage(Driver& d, const std::vector<StageIO>& io, StageParams sp) 
   };
   EF_TRY(mark(t, 0));
   EF_TRY(mark(t, 1));  // step0 is fused into the previous stage's final kernel
-  each([&](ef_solver* h, const StageIO& x) { ef::launch_edge_visc(h->dim, h->lay, h->gas, x.U, h->w, want_tau, sp.uni != 0,
+  each([&](ef_solver* h, const StageIO& x) { ef::launch_edge_visc(h->dim, h->lay, h->gas, x.U, h->w, sp.stage, want_tau, sp.uni != 0,
                                                                    sp.tau_mode != ef::TAU_DEVICE, st); });
   EF_TRY(mark(t, 2));
   EF_TRY(produce([&](ef_solver* h, const StageIO& x, ef::RowSet rs) {
-    ef::launch_row_visc(h->dim, h->lay, h->gas, x.U, h->w, want_tau, sp.uni != 0, rs, st);
+    ef::launch_row_visc(h->dim, h->lay, h->gas, x.U, h->w, sp.stage, want_tau, sp.uni != 0, rs, st);
   }, {fld(&Work::alpha, 1)}));
   if (want_tau) EF_TRY(allreduce_tau(d, st));
   EF_TRY(mark(t, 3));
@@ -780,11 +787,10 @@ static int run_stage(Driver& d, const std::vector<StageIO>& io, StageParams sp) 
   return EF_OK;
 }
 
-static StageParams stage_params(ef_solver* h, int mode, double tau, double tau_max, double rk_a) {
+static StageParams stage_params(ef_solver* h, int mode, int stage, double rk_a) {
   StageParams sp;
   sp.tau_mode = mode;
-  sp.tau_given = tau;
-  sp.tau_max = tau_max;
+  sp.stage = stage;
   sp.c_cfl = h->c_cfl;
   sp.newton = h->newton;
   sp.passes = h->passes;
@@ -793,37 +799,44 @@ static StageParams stage_params(ef_solver* h, int mode, double tau, double tau_m
   return sp;
 }
 
-static int reset_flags(Driver& d) {
-  for (ef_solver* h : d.hs) {
-    EF_CUDA(cudaMemsetAsync(h->w.err, 0, sizeof(int), h->st));
-    EF_CUDA(cudaMemsetAsync(h->w.bad_gid, 0xff, sizeof(unsigned long long), h->st));
+// Per step: the identical-state sample counters.  The error flags are NOT reset
+// here: they latch across a chain of async steps and are cleared only after
+// they have been read (finish) or by set_state (clear_err).
+static int reset_counters(Driver& d) {
+  for (ef_solver* h : d.hs)
     EF_CUDA(cudaMemsetAsync(h->w.n_same, 0, sizeof(unsigned long long) * ef::kSameSlots, h->st));
-  }
   return EF_OK;
 }
 
-static int euler_async(Driver& d, int32_t has_tau, double tau, double tau_max, int* out_buf) {
+static int clear_err(ef_solver* h) {
+  EF_CUDA(cudaMemsetAsync(h->w.err, 0, sizeof(int), h->st));
+  EF_CUDA(cudaMemsetAsync(h->w.err_first, 0x7f, sizeof(int), h->st));  // 0x7f7f7f7f > every code
+  EF_CUDA(cudaMemsetAsync(h->w.bad_gid, 0xff, sizeof(unsigned long long), h->st));
+  return EF_OK;
+}
+
+static int euler_async(Driver& d, int32_t has_tau, int* out_buf) {
   const int in = d.h0()->cur, out = (in + 1) % 3;
-  EF_TRY(reset_flags(d));
+  EF_TRY(reset_counters(d));
   std::vector<StageIO> io;
   for (ef_solver* h : d.hs) io.push_back({h->Ubuf[in], h->Ubuf[in], h->Ubuf[out]});
-  StageParams sp = stage_params(d.h0(), has_tau ? ef::TAU_GIVEN : ef::TAU_CFL, tau, tau_max, -1.0);
+  StageParams sp = stage_params(d.h0(), has_tau ? ef::TAU_GIVEN : ef::TAU_CFL, 0, -1.0);
   EF_TRY(run_stage(d, io, sp));
   *out_buf = out;
   return EF_OK;
 }
 
-static int rk3_async(Driver& d, int32_t has_tau, double tau, double tau_max, int* out_buf) {
+static int rk3_async(Driver& d, int32_t has_tau, int* out_buf) {
   const int u0 = d.h0()->cur, a = (u0 + 1) % 3, b = (u0 + 2) % 3;
-  EF_TRY(reset_flags(d));
+  EF_TRY(reset_counters(d));
   auto io_of = [&](int in, int out) {
     std::vector<StageIO> io;
     for (ef_solver* h : d.hs) io.push_back({h->Ubuf[in], h->Ubuf[u0], h->Ubuf[out]});
     return io;
   };
-  EF_TRY(run_stage(d, io_of(u0, a), stage_params(d.h0(), has_tau ? ef::TAU_GIVEN : ef::TAU_CFL, tau, tau_max, -1.0)));
-  EF_TRY(run_stage(d, io_of(a, b), stage_params(d.h0(), ef::TAU_DEVICE, 0.0, 0.0, 0.25)));        // stepper.py:632
-  EF_TRY(run_stage(d, io_of(b, a), stage_params(d.h0(), ef::TAU_DEVICE, 0.0, 0.0, 2.0 / 3.0)));   // stepper.py:635
+  EF_TRY(run_stage(d, io_of(u0, a), stage_params(d.h0(), has_tau ? ef::TAU_GIVEN : ef::TAU_CFL, 0, -1.0)));
+  EF_TRY(run_stage(d, io_of(a, b), stage_params(d.h0(), ef::TAU_DEVICE, 1, 0.25)));        // stepper.py:632
+  EF_TRY(run_stage(d, io_of(b, a), stage_params(d.h0(), ef::TAU_DEVICE, 2, 2.0 / 3.0)));   // stepper.py:635
   *out_buf = a;
   return EF_OK;
 }
@@ -834,21 +847,27 @@ static int rk3_async(Driver& d, int32_t has_tau, double tau, double tau_max, int
 // capture that fails turns graphs off for the handle and runs the step directly.
 static int step_async(Driver& d, bool rk3, int32_t has_tau, double tau, double tau_max, int* out_buf) {
   ef_solver* h = d.h0();
+  // the step's tau arguments: a pageable-source copy is staged at the call, so the
+  // host values may change before the copy executes (async chains)
+  const double targ[2] = {has_tau ? tau : 0.0, tau_max};
+  for (ef_solver* r : d.hs)
+    EF_CUDA(cudaMemcpyAsync(r->w.tau_arg, targ, sizeof targ, cudaMemcpyHostToDevice, r->st));
   auto body = [&]() {
-    return rk3 ? rk3_async(d, has_tau, tau, tau_max, out_buf) : euler_async(d, has_tau, tau, tau_max, out_buf);
+    return rk3 ? rk3_async(d, has_tau, out_buf) : euler_async(d, has_tau, out_buf);
   };
   if (!h->use_graphs || h->timing || d.group || h->nranks > 1) return body();
-  const ef_solver::GraphKey key{rk3 ? 1 : 0, h->cur, has_tau ? 1 : 0, h->uni_on ? 1 : 0, has_tau ? tau : 0.0,
-                                tau_max};
+  const ef_solver::GraphKey key{rk3 ? 1 : 0, h->cur, has_tau ? 1 : 0, h->uni_on ? 1 : 0};
   for (auto& g : h->graphs)
     if (g.key == key) {
       g.used = ++h->graph_clock;
       EF_CUDA(cudaGraphLaunch(g.exec, h->st));
+      ef::add_kernel_launches(g.launches);
       *out_buf = (h->cur + 1) % 3;  // euler: in + 1; rk3: u0 + 1
       h->n_euler += rk3 ? 3 : 1;
       return EF_OK;
     }
   const int64_t n0 = h->n_euler;
+  const long long l0 = ef::kernel_launches();
   cudaError_t e = cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal);
   int rc = e == cudaSuccess ? body() : EF_ERR_CUDA;
   cudaGraph_t graph = nullptr;
@@ -869,7 +888,7 @@ static int step_async(Driver& d, bool rk3, int32_t has_tau, double tau, double t
     cudaGraphExecDestroy(old->exec);
     h->graphs.erase(old);
   }
-  h->graphs.push_back({key, exec, ++h->graph_clock});
+  h->graphs.push_back({key, exec, ++h->graph_clock, ef::kernel_launches() - l0});
   EF_CUDA(cudaGraphLaunch(exec, h->st));  // n_euler was advanced by the captured body
   return EF_OK;
 }
@@ -877,6 +896,7 @@ static int step_async(Driver& d, bool rk3, int32_t has_tau, double tau, double t
 static int readback(ef_solver* h) {
   EF_CUDA(cudaMemcpyAsync(&h->rb->tau, h->w.tau, sizeof(double), cudaMemcpyDeviceToHost, h->st));
   EF_CUDA(cudaMemcpyAsync(&h->rb->err, h->w.err, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+  EF_CUDA(cudaMemcpyAsync(&h->rb->err_first, h->w.err_first, sizeof(int), cudaMemcpyDeviceToHost, h->st));
   EF_CUDA(cudaMemcpyAsync(&h->rb->bad, h->w.bad_gid, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
   EF_CUDA(cudaMemcpyAsync(h->rb->n_same, h->w.n_same, sizeof(unsigned long long) * ef::kSameSlots,
                           cudaMemcpyDeviceToHost, h->st));
@@ -891,26 +911,46 @@ static int finish(Driver& d, int out_buf, double* tau_used) {
   ef_solver* h0 = d.h0();
   if (d.multi() && !d.group) {
     EF_NCCL(nccl().AllReduce(h0->w.err, h0->w.err, 1, ncclInt32, ncclMax, h0->comm, h0->st));
+    EF_NCCL(nccl().AllReduce(h0->w.err_first, h0->w.err_first, 1, ncclInt32, ncclMin, h0->comm, h0->st));
     EF_NCCL(nccl().AllReduce(h0->w.bad_gid, h0->w.bad_gid, 1, ncclUint64, ncclMin, h0->comm, h0->st));
   }
-  int err = 0;
+  int err = 0, first = ef::kErrNone;
   unsigned long long bad = ~0ull;
   for (ef_solver* h : d.hs) {
     EF_TRY(readback(h));
     err |= h->rb->err;
+    first = std::min(first, h->rb->err_first);
     bad = std::min(bad, h->rb->bad);
   }
   if (err) {  // the state rolls back: nothing computed for the failed stages may be reused --
               // step0 of the current state again (it also clears the memo marks)
     for (ef_solver* h : d.hs) {
+      EF_TRY(clear_err(h));
       ef::launch_nodal(h->dim, h->lay, h->gas, h->Ubuf[h->cur], h->w, 0, h->lay.n_local, h->st);
       EF_CUDA(cudaGetLastError());
     }
   }
-  if (err & ef::ERR_TAU_UNBOUNDED) return fail(EF_ERR_TAU_UNBOUNDED, "constant field, the time step bound is unbounded");
-  if (err & ef::ERR_PROJECT) return fail(EF_ERR_INADMISSIBLE, "projected state requires rho > 0 and p > 0");
-  if (err & ef::ERR_NONFINITE_P) return fail(EF_ERR_INADMISSIBLE, "non-finite correction flux P_ij (overflow)");
-  if (err & ef::ERR_BAD_STATE) {
+  // report the error the reference would have raised first: the earliest stage,
+  // and inside it the earliest check (kernels latch min(stage * 8 + phase))
+  int which = 0;
+  if (err) {
+    switch (first == ef::kErrNone ? -1 : first % 8) {
+      case ef::PH_VISC:
+      case ef::PH_INDICATOR: which = ef::ERR_PROJECT; break;
+      case ef::PH_TAU: which = ef::ERR_TAU_UNBOUNDED; break;
+      case ef::PH_P: which = ef::ERR_NONFINITE_P; break;
+      case ef::PH_STATE: which = ef::ERR_BAD_STATE; break;
+      default:
+        which = (err & ef::ERR_TAU_UNBOUNDED) ? ef::ERR_TAU_UNBOUNDED
+              : (err & ef::ERR_PROJECT)       ? ef::ERR_PROJECT
+              : (err & ef::ERR_NONFINITE_P)   ? ef::ERR_NONFINITE_P
+                                              : ef::ERR_BAD_STATE;
+    }
+  }
+  if (which == ef::ERR_TAU_UNBOUNDED) return fail(EF_ERR_TAU_UNBOUNDED, "constant field, the time step bound is unbounded");
+  if (which == ef::ERR_PROJECT) return fail(EF_ERR_INADMISSIBLE, "projected state requires rho > 0 and p > 0");
+  if (which == ef::ERR_NONFINITE_P) return fail(EF_ERR_INADMISSIBLE, "non-finite correction flux P_ij (overflow)");
+  if (which == ef::ERR_BAD_STATE) {
     int64_t orig = -1;  // original id of the smallest inadmissible CM id (any local copy)
     for (ef_solver* h : d.hs)
       for (int64_t i = 0; i < h->n_local && orig < 0; ++i)
@@ -940,13 +980,18 @@ static int finish(Driver& d, int out_buf, double* tau_used) {
 static int set_state_all(Driver& d, const double* U) {
   int bad = 0;
   for (ef_solver* h : d.hs) {
+    if (h->pending_out >= 0) {  // a new state replaces an unchecked async result
+      EF_CUDA(cudaStreamSynchronize(h->st));
+      h->pending_out = -1;
+    }
     const int spare = (h->cur + 1) % 3;
-    EF_CUDA(cudaMemsetAsync(h->w.err, 0, sizeof(int), h->st));
+    EF_TRY(clear_err(h));
     EF_CUDA(cudaMemcpyAsync(h->aos_dev, U, sizeof(double) * h->nvar * h->n_global, cudaMemcpyHostToDevice, h->st));
     ef::launch_gather_state(h->dim, h->lay, h->aos_dev, h->orig_dev, h->Ubuf[spare], h->w.err, h->st);
     EF_TRY(readback(h));
     bad |= h->rb->err;
   }
+  for (ef_solver* h : d.hs) EF_TRY(clear_err(h));  // (the gather used w.err for its check)
   if (bad) return fail(EF_ERR_INADMISSIBLE, "initial state is not admissible");
   for (ef_solver* h : d.hs) {
     h->cur = (h->cur + 1) % 3;
@@ -996,8 +1041,11 @@ struct DevBufs {
 };
 
 extern "C" {
+int ef_sync(ef_solver* h, double* tau_used);
 
 const char* ef_last_error(void) { return g_err.c_str(); }
+
+int64_t ef_kernel_launches(void) { return (int64_t)ef::kernel_launches(); }
 
 int ef_nccl_unique_id(void* out128) {
   if (!out128) return fail(EF_ERR_ARG, "null argument");
@@ -1101,15 +1149,24 @@ int ef_set_state(ef_solver* h, const double* U) {
   return set_state_all(d, U);
 }
 
+// A synchronous call after ef_ssp_rk3_step_async first settles the pending
+// chain (ef_sync: its latched errors are reported by this call).
+static int settle(ef_solver* h) {
+  if (h->pending_out < 0) return EF_OK;
+  return ef_sync(h, nullptr);
+}
+
 int ef_get_state(ef_solver* h, double* U) {
   if (!h || !U) return fail(EF_ERR_ARG, "null argument");
   cudaSetDevice(h->device);
+  EF_TRY(settle(h));
   return get_state_one(h, U);
 }
 
 int ef_euler_step(ef_solver* h, int32_t has_tau, double tau, double tau_max, double* tau_used) {
   Driver d;
   EF_TRY(single_driver(h, d));
+  EF_TRY(settle(h));
   int out;
   EF_TRY(step_async(d, false, has_tau, tau, tau_max, &out));
   return finish(d, out, tau_used);
@@ -1118,6 +1175,7 @@ int ef_euler_step(ef_solver* h, int32_t has_tau, double tau, double tau_max, dou
 int ef_ssp_rk3_step(ef_solver* h, int32_t has_tau, double tau, double tau_max, double* tau_used) {
   Driver d;
   EF_TRY(single_driver(h, d));
+  EF_TRY(settle(h));
   int out;
   EF_TRY(step_async(d, true, has_tau, tau, tau_max, &out));
   return finish(d, out, tau_used);

@@ -32,6 +32,8 @@
 // low-order loops and zero the first pass's P, unchanged rows keep their d_ij
 // (the *<..., UNI> variants, chosen per step from a sampled count); in 3D the
 // limiter accepts t_R from an fp32 bound of the pow when the margin is clear.
+#include <atomic>
+
 #include "ef_kernels.cuh"
 
 namespace ef {
@@ -195,6 +197,11 @@ constexpr double kZeroP = -1.0;
 #ifndef EF_PF_LIM
 #define EF_PF_LIM 131072
 #endif
+// latch an error: its bit, and its position in the reference's order of checks
+__device__ __forceinline__ void raise_err(const Work& w, int bit, int stage, int phase) {
+  atomicOr(w.err, bit);
+  atomicMin(w.err_first, stage * 8 + phase);
+}
 __device__ __forceinline__ void pf_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
 // ---------------------------------------------------------------- state I/O
@@ -252,16 +259,115 @@ __global__ void k_nodal(Layout m, Gas g, const double* __restrict__ U, Work w, i
 }
 
 // ---------------------------------------------------------------- step1a
+// d_ij in two phases per block (the general path, EF_VISC_Q): every thread
+// projects its edge's states and tries lambda_fast for both directions; the
+// edges it cannot decide (two-shock or pressure-dominated waves: about half on
+// a smooth 3D field) are queued in shared memory with their four projections
+// and then evaluated exactly (lambda_max2: the four pows) by the first threads
+// of the block.  The exact work runs on densely packed warps instead of on
+// whichever lanes happen to need it.  Results are the reference's bits either way.
+#ifndef EF_VISC_Q
+#define EF_VISC_Q 1
+#endif
+template <int D>
+__device__ __forceinline__ void edge_visc_queued(const Layout& m, const Gas& g, const double* __restrict__ U,
+                                                 const Work& w, int flags, int e) {
+  constexpr int NV = D + 2;
+  constexpr int NT = EF_TPB_D(D);
+  constexpr int QF = 18;  // 4 projections x (rho, u, p, c), |c_ij|, |c_ji|
+  __shared__ double qv[QF][NT];
+  __shared__ int qp[2][NT];
+  __shared__ int qn;
+  if (threadIdx.x == 0) qn = 0;
+  __syncthreads();
+  const int NP = (int)m.NP, NE = (int)m.n_edges;
+  bool bad = false;
+  if (e < NE) {
+    const int p = m.edges[e];
+    const int i = (int)fdiv((uint32_t)p, m.slab) * 32 + (p & 31);
+    const int j = m.edge_j[e];
+    const int pt = m.edge_pt[e];
+    double Ui[NV], Uj[NV], nij[D], nji[D];
+    load_node<NV>(U, NP, i, Ui);
+    load_node<NV>(U, NP, j, Uj);
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      nij[a] = m.egeo[(size_t)a * NE + e];
+      nji[a] = m.egeo[(size_t)(D + 1 + a) * NE + e];
+    }
+    const double norm_ij = m.egeo[(size_t)D * NE + e], norm_ji = m.egeo[(size_t)(2 * D + 1) * NE + e];
+    const Recip ri = recip(Ui[0]), rj = recip(Uj[0]);
+    // both directions (a zero |c| direction is projected on n = e_1 and then
+    // discarded with its status, as the reference discards it; d_ij_geo)
+    Proj La, Ra, Lb, Rb;
+    const bool ba = project<D>(Ui, ri, nij, g, La) | project<D>(Uj, rj, nij, g, Ra);
+    const bool bb = project<D>(Uj, rj, nji, g, Lb) | project<D>(Ui, ri, nji, g, Rb);
+    bad = (norm_ij > 0.0 && ba) || (norm_ji > 0.0 && bb);
+    double la = 0.0, lb = 0.0;
+    const bool da = !(norm_ij > 0.0) || (EF_LAM_FAST && lambda_fast(La, Ra, g, la));
+    const bool db = !(norm_ji > 0.0) || (EF_LAM_FAST && lambda_fast(Lb, Rb, g, lb));
+    if (da && db) {
+      const double v_ij = norm_ij > 0.0 ? la * norm_ij : 0.0;
+      const double v_ji = norm_ji > 0.0 ? lb * norm_ji : 0.0;
+      const double dv = npmax(v_ij, v_ji);
+      w.d[p] = dv;
+      w.d[pt] = dv;
+    } else {
+      const int k = atomicAdd(&qn, 1);
+      const Proj* pr[4] = {&La, &Ra, &Lb, &Rb};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        qv[4 * q + 0][k] = pr[q]->rho;
+        qv[4 * q + 1][k] = pr[q]->u;
+        qv[4 * q + 2][k] = pr[q]->p;
+        qv[4 * q + 3][k] = pr[q]->c;
+      }
+      qv[16][k] = norm_ij;
+      qv[17][k] = norm_ji;
+      qp[0][k] = p;
+      qp[1][k] = pt;
+    }
+    // with the shortcuts off: sample (1 block in 8, first stage) how many would apply
+    if ((flags & 2) && (blockIdx.x & 7) == 0) count_hits(same_state<NV>(Ui, Uj), w.n_same);
+  }
+  if (bad) raise_err(w, ERR_PROJECT, flags >> 4, PH_VISC);
+  __syncthreads();
+  const int k = threadIdx.x;
+  if (k < qn) {
+    Proj P4[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      P4[q].rho = qv[4 * q + 0][k];
+      P4[q].u = qv[4 * q + 1][k];
+      P4[q].p = qv[4 * q + 2][k];
+      P4[q].c = qv[4 * q + 3][k];
+    }
+    const double norm_ij = qv[16][k], norm_ji = qv[17][k];
+    double la, lb;
+    lambda_max2(P4[0], P4[1], P4[2], P4[3], g, la, lb);
+    const double v_ij = norm_ij > 0.0 ? la * norm_ij : 0.0;
+    const double v_ji = norm_ji > 0.0 ? lb * norm_ji : 0.0;
+    const double dv = npmax(v_ij, v_ji);
+    w.d[qp[0][k]] = dv;
+    w.d[qp[1][k]] = dv;
+  }
+}
+
 // One thread per upper edge (global id of the column above the row's, i.e. a
 // slot after the diagonal; stepper.py:211, 415).  The edge list holds SELL
 // positions in ascending order, so a warp reads 32 consecutive positions of
 // one slot row (coalesced) and the row / slot are recovered from the position.
 template <int D, bool UNI>
 __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_EDGE(D), D)) k_edge_visc(Layout m, Gas g, const double* __restrict__ U,
-                                                   Work w, int flags) {  // 1: reset the CFL bound, 2: count
+                                                   Work w, int flags) {  // 1: reset the CFL bound, 2: count,
+                                                                         // bits 4-5: stage
   constexpr int NV = D + 2;
   const int e = blockIdx.x * EF_TPB_D(D) + threadIdx.x;
   if ((flags & 1) && e == 0) *w.tau_min_bits = 0x7ff0000000000000ULL;
+  if constexpr (EF_VISC_Q && D == 3 && !UNI) {
+    edge_visc_queued<D>(m, g, U, w, flags, e);
+    return;
+  }
   if (e >= m.n_edges) return;
   const int NP = (int)m.NP, NE = (int)m.n_edges;
   if (UNI && EF_PF_VISC_UNI > 0 && e + EF_PF_VISC_UNI < NE) {
@@ -309,7 +415,7 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_EDGE(D), D)) k_edge
   // reference's mirror, stepper.py:427-434, without a gather)
   w.d[p] = dv;
   w.d[pt] = dv;
-  if (bad) atomicOr(w.err, ERR_PROJECT);
+  if (bad) raise_err(w, ERR_PROJECT, flags >> 4, PH_VISC);
   // with the shortcuts off: sample (1 block in 8, first stage) how many would apply
   if (!UNI && (flags & 2) && (blockIdx.x & 7) == 0) count_hits(same, w.n_same);
 }
@@ -392,7 +498,7 @@ __device__ __forceinline__ void node_flux(const double* Ui, const Work& w, int N
 
 template <int D>
 __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ROW(D), D)) k_row_visc(Layout m, Gas g, const double* __restrict__ U,
-                                                  Work w, int want_tau, int uni_on, RowSet rs) {
+                                                  Work w, int want_tau, int uni_on, RowSet rs, int stage) {
   constexpr int NV = D + 2;
   const int t0 = blockIdx.x * EF_TPB_D(D) + threadIdx.x;
   const bool act = t0 < rs.n;
@@ -402,7 +508,9 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ROW(D), D)) k_row_v
   // frozen row: uniform stencil and state unchanged since the previous
   // (identical-state) stage -- then so are all its neighbours, all its d_ij
   // (memo), its alpha (0) and d_ii: only the CFL candidate is formed again
-  const bool frozen = act && EF_FROZEN && uni_on && !w.nonuni[i] && !w.chg[i];
+  // (and no P of the row's edges was formed in the previous stage: a limited pass
+  // then added to U^L in place, so the stored U^L is not this stage's)
+  const bool frozen = act && EF_FROZEN && uni_on && !w.nonuni[i] && !w.chg[i] && !w.pnz[i];
   if (frozen && want_tau) {
     const double dii = w.d[sidx32(i, m.diag[i], m.L)];
     if (dii < 0.0) cand = m.m_i[i] / (-2.0 * dii);
@@ -540,7 +648,7 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ROW(D), D)) k_row_v
     w.alpha[i] = denom > kDenomFloor ? al : 0.0;
     }
   }
-  if (bad) atomicOr(w.err, ERR_PROJECT);
+  if (bad) raise_err(w, ERR_PROJECT, stage, PH_INDICATOR);
   if (!want_tau) return;
   __shared__ double red[EF_TPB_D(D) / 32];
   cand = warp_min(cand);
@@ -559,13 +667,14 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ROW(D), D)) k_row_v
 __device__ __forceinline__ double stage_tau(const Work& w, const StageParams& sp) {
   double tau;
   if (sp.tau_mode == TAU_GIVEN) {
-    tau = sp.tau_given;
+    tau = w.tau_arg[0];
   } else if (sp.tau_mode == TAU_DEVICE) {
     tau = *w.tau;
   } else {  // stepper.py:538-548
     const double tmin = __longlong_as_double((long long)*w.tau_min_bits);
     const double a = sp.c_cfl * tmin;
-    tau = (sp.tau_max < a) ? sp.tau_max : a;
+    const double tau_max = w.tau_arg[1];
+    tau = (tau_max < a) ? tau_max : a;
   }
   return tau;
 }
@@ -581,11 +690,11 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_LOW(D), D)) k_low_o
     *w.tau = tau;
     if (sp.tau_mode == TAU_CFL &&
         !(__longlong_as_double((long long)*w.tau_min_bits) < __longlong_as_double(0x7ff0000000000000LL)))
-      atomicOr(w.err, ERR_TAU_UNBOUNDED);
+      raise_err(w, ERR_TAU_UNBOUNDED, sp.stage, PH_TAU);
   }
   if (t0 >= rs.n) return;
   const int i = rs.row(t0);
-  if (EF_FROZEN && sp.uni && !w.nonuni[i] && !w.chg[i]) {
+  if (EF_FROZEN && sp.uni && !w.nonuni[i] && !w.chg[i] && !w.pnz[i]) {  // as k_row_visc decides
     // frozen row (see k_row_visc): U^L, R, bounds and the zero-P mark from the
     // previous stage are this stage's values (U^L = U + (+0) does not depend on
     // tau); only the shortcut count and the row status are kept up
@@ -788,7 +897,7 @@ __device__ __forceinline__ void edge_lim_one(const Layout& m, const Gas& g, cons
     bool fin = true;
 #pragma unroll
     for (int k = 0; k < NV; ++k) fin = fin && finite(Pi[k]) && finite(Pj[k]);
-    if (!fin) atomicOr(w.err, ERR_NONFINITE_P);
+    if (!fin) raise_err(w, ERR_NONFINITE_P, sp.stage, PH_P);
   }
   // The last pass q >= 1 leaves P_(q-1) and min(l) of pass q-1 in place: k_final
   // forms the same product P_(q-1) (1 - min l) itself, which saves the largest
@@ -979,7 +1088,7 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_FINAL(D), D)) k_fin
   }
   // _finish_step admissibility, stepper.py:612-621
   if (!((Un[0] > 0.0) && (internal_energy<D>(Un) > 0.0))) {
-    atomicOr(w.err, ERR_BAD_STATE);
+    raise_err(w, ERR_BAD_STATE, sp.stage, PH_STATE);
     atomicMin(w.bad_gid, (unsigned long long)m.gid[i]);
   }
   double Uo[NV];
@@ -1054,8 +1163,15 @@ __global__ void k_pow(const double* __restrict__ x, double y, double* __restrict
 }
 
 // ---------------------------------------------------------------- launchers
+// process-wide count of kernel launches issued through the launchers below
+// (a CUDA-graph replay adds the count its capture recorded; ef_capi.cu)
+static std::atomic<long long> g_launches{0};
+long long kernel_launches() { return g_launches.load(std::memory_order_relaxed); }
+void add_kernel_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+#define EF_COUNT() g_launches.fetch_add(1, std::memory_order_relaxed)
 #define EF_DISPATCH(dim, KERNEL, GRID, ...)                                   \
   do {                                                                        \
+    EF_COUNT();                                                               \
     if ((dim) == 2) KERNEL<2><<<(GRID), TPB, 0, st>>>(__VA_ARGS__);          \
     else KERNEL<3><<<(GRID), TPB, 0, st>>>(__VA_ARGS__);                     \
   } while (0)
@@ -1066,6 +1182,7 @@ static inline unsigned grid_d(int dim, int64_t n) {
 }
 #define EF_DISPATCH_STAGE(dim, KERNEL, N, ...)                                                      \
   do {                                                                                              \
+    EF_COUNT();                                                                                     \
     if ((dim) == 2) KERNEL<2><<<grid_d(2, (N)), EF_TPB2, 0, st>>>(__VA_ARGS__);                     \
     else KERNEL<3><<<grid_d(3, (N)), EF_TPB3, 0, st>>>(__VA_ARGS__);                                \
   } while (0)
@@ -1085,10 +1202,11 @@ void launch_nodal(int dim, const Layout& m, const Gas& g, const double* U, Work 
   if (hi <= lo) return;
   EF_DISPATCH(dim, k_nodal, grid_for(hi - lo), m, g, U, w, lo, hi);
 }
-void launch_edge_visc(int dim, const Layout& m, const Gas& g, const double* U, Work w,
+void launch_edge_visc(int dim, const Layout& m, const Gas& g, const double* U, Work w, int stage,
                       bool reset_tau, bool uni, bool count, cudaStream_t st) {
   const int64_t n = m.n_edges > 0 ? m.n_edges : 1;
-  const int r = (reset_tau ? 1 : 0) | (count ? 2 : 0);
+  const int r = (reset_tau ? 1 : 0) | (count ? 2 : 0) | (stage << 4);
+  EF_COUNT();
   if (dim == 2) {
     if (uni) k_edge_visc<2, true><<<grid_d(2, n), EF_TPB2, 0, st>>>(m, g, U, w, r);
     else k_edge_visc<2, false><<<grid_d(2, n), EF_TPB2, 0, st>>>(m, g, U, w, r);
@@ -1097,9 +1215,9 @@ void launch_edge_visc(int dim, const Layout& m, const Gas& g, const double* U, W
     else k_edge_visc<3, false><<<grid_d(3, n), EF_TPB3, 0, st>>>(m, g, U, w, r);
   }
 }
-void launch_row_visc(int dim, const Layout& m, const Gas& g, const double* U, Work w,
+void launch_row_visc(int dim, const Layout& m, const Gas& g, const double* U, Work w, int stage,
                      bool want_tau, bool uni, RowSet rs, cudaStream_t st) {
-  EF_DISPATCH_STAGE(dim, k_row_visc, rs.n > 0 ? rs.n : 1, m, g, U, w, want_tau ? 1 : 0, uni ? 1 : 0, rs);
+  EF_DISPATCH_STAGE(dim, k_row_visc, rs.n > 0 ? rs.n : 1, m, g, U, w, want_tau ? 1 : 0, uni ? 1 : 0, rs, stage);
 }
 void launch_low_order(int dim, const Layout& m, const Gas& g, const double* U, Work w,
                       StageParams sp, RowSet rs, cudaStream_t st) {
@@ -1112,6 +1230,7 @@ static void edge_lim_launch(const Layout& m, const Gas& g, const double* U, Work
                             cudaStream_t st) {
   constexpr int tb = D == 3 ? EF_TPB3 : EF_TPB2;
   const unsigned grid = grid_d(D, m.n_edges);
+  EF_COUNT();
   if (EF_WL && q > 0 && q == sp.passes - 1)
     k_edge_lim_last<D><<<grid < EF_WL_GRID ? grid : EF_WL_GRID, tb, 0, st>>>(m, g, U, w, sp, q);
   else if (q > 0) k_edge_lim<D, false, false><<<grid, tb, 0, st>>>(m, g, U, w, sp, q);
@@ -1140,12 +1259,12 @@ void launch_final(int dim, const Layout& m, const Gas& g, const double* U, const
 }
 void launch_pack_rows(const double* field, int ncomp, int64_t NP, const int32_t* idx, int64_t count,
                       double* buf, int stride, int coff, cudaStream_t st) {
-  if (count > 0)
+  if (count > 0 && EF_COUNT() >= 0)
     k_pack_rows<<<grid_for(count * ncomp), TPB, 0, st>>>(field, ncomp, NP, idx, count, buf, stride, coff);
 }
 void launch_unpack_rows(double* field, int ncomp, int64_t NP, const int32_t* idx, int64_t count,
                         const double* buf, int stride, int coff, cudaStream_t st) {
-  if (count > 0)
+  if (count > 0 && EF_COUNT() >= 0)
     k_unpack_rows<<<grid_for(count * ncomp), TPB, 0, st>>>(field, ncomp, NP, idx, count, buf, stride, coff);
 }
 void launch_pack_pos(const double* arr, const int32_t* pos, int64_t count, double* buf, cudaStream_t st) {
@@ -1155,6 +1274,7 @@ void launch_unpack_pos(double* arr, const int32_t* pos, int64_t count, const dou
   if (count > 0) k_unpack_pos<<<grid_for(count), TPB, 0, st>>>(arr, pos, count, buf);
 }
 void launch_group_min(unsigned long long* const* bits_dev, int n, cudaStream_t st) {
+  EF_COUNT();
   k_group_min<<<1, 1, 0, st>>>(bits_dev, n);
 }
 __global__ void k_pow_ub(const double* __restrict__ x, double y, double* __restrict__ out, int64_t n) {
@@ -1199,7 +1319,25 @@ __global__ void k_eval_dij(Gas g, int64_t n, const double* __restrict__ Ui, cons
     nji[k] = norm_ji > 0.0 ? cji[q * D + k] / norm_ji : (k == 0 ? 1.0 : 0.0);
   }
   bool bd = false;
-  out[q] = d_ij_geo<D>(a, b, nij, norm_ij, nji, norm_ji, g, bd, same_state<NV>(a, b));
+  if (EF_VISC_Q && D == 3) {  // the stage kernel's general path: lambda_fast, else exact
+    const Recip ri = recip(a[0]), rj = recip(b[0]);
+    Proj La, Ra, Lb, Rb;
+    const bool ba = project<D>(a, ri, nij, g, La) | project<D>(b, rj, nij, g, Ra);
+    const bool bb = project<D>(b, rj, nji, g, Lb) | project<D>(a, ri, nji, g, Rb);
+    bd = (norm_ij > 0.0 && ba) || (norm_ji > 0.0 && bb);
+    double la = 0.0, lb = 0.0, ea, eb;
+    const bool da = lambda_fast(La, Ra, g, la), db = lambda_fast(Lb, Rb, g, lb);
+    if (!da || !db) {
+      lambda_max2(La, Ra, Lb, Rb, g, ea, eb);
+      if (!da) la = ea;
+      if (!db) lb = eb;
+    }
+    const double v_ij = norm_ij > 0.0 ? la * norm_ij : 0.0;
+    const double v_ji = norm_ji > 0.0 ? lb * norm_ji : 0.0;
+    out[q] = npmax(v_ij, v_ji);
+  } else {
+    out[q] = d_ij_geo<D>(a, b, nij, norm_ij, nji, norm_ji, g, bd, same_state<NV>(a, b));
+  }
   bad[q] = bd ? 1 : 0;
 }
 

@@ -94,7 +94,12 @@ struct Work {
                      // 1 uniform-stencil shortcut (R = 0), 2 frozen (also unchanged)
   unsigned long long* tau_min_bits;  // CFL min over owned rows
   double* tau;       // tau of the current RK step / Euler step
-  int* err;          // bit0 projection/entropy, bit1 inadmissible result, bit2 tau unbounded
+  double* tau_arg;   // [2] the step's tau (TAU_GIVEN) and tau_max, written before every step
+                     // (kept out of the kernel arguments so one CUDA graph serves every tau)
+  int* err;          // ErrBits of every error since the flags were last read (ef_sync /
+                     // a synchronous step / set_state): errors latch across async steps
+  int* err_first;    // min over the errors of (stage * 8 + phase): the one the reference
+                     // would have raised first (stepper.py:508-622 order of the checks)
   unsigned long long* bad_gid;       // min global CM id of an inadmissible row
   unsigned long long* n_same;        // [kSameSlots] spread counters since the last reset:
                                      // identical-state edges (shortcuts off) or uniform rows (on)
@@ -103,11 +108,15 @@ struct Work {
 constexpr int kSameSlots = 128;
 enum TauMode { TAU_CFL = 0, TAU_GIVEN = 1, TAU_DEVICE = 2 };
 enum ErrBits { ERR_PROJECT = 1, ERR_BAD_STATE = 2, ERR_TAU_UNBOUNDED = 4, ERR_NONFINITE_P = 8 };
+// phase of a check inside a stage, in the reference's order: d_ij projections
+// (step1), the indicator's entropy derivative (step1), tau (step2/3), P (step4),
+// the admissibility of the result (_finish_step)
+enum ErrPhase { PH_VISC = 0, PH_INDICATOR = 1, PH_TAU = 2, PH_P = 3, PH_STATE = 4 };
+constexpr int kErrNone = 0x7fffffff;
 
 struct StageParams {
   int tau_mode;
-  double tau_given;
-  double tau_max;
+  int stage;  // 0..2: stage of the RK step (error ordering)
   double c_cfl;
   int newton;
   int passes;
@@ -139,10 +148,10 @@ void launch_scatter_state(int dim, const Layout& m, const double* U, const int64
 void launch_nodal(int dim, const Layout& m, const Gas& g, const double* U, Work w, int64_t lo,
                   int64_t hi, cudaStream_t st);
 // step1a: d_ij on every upper edge (one thread per edge)
-void launch_edge_visc(int dim, const Layout& m, const Gas& g, const double* U, Work w,
+void launch_edge_visc(int dim, const Layout& m, const Gas& g, const double* U, Work w, int stage,
                       bool reset_tau, bool uni, bool count, cudaStream_t st);
 // step1b+2: per owned row, indicator alpha, mirror of d, d_ii, CFL bound
-void launch_row_visc(int dim, const Layout& m, const Gas& g, const double* U, Work w,
+void launch_row_visc(int dim, const Layout& m, const Gas& g, const double* U, Work w, int stage,
                      bool want_tau, bool uni, RowSet rs, cudaStream_t st);
 void launch_low_order(int dim, const Layout& m, const Gas& g, const double* U, Work w,
                       StageParams sp, RowSet rs, cudaStream_t st);
@@ -152,6 +161,8 @@ void launch_edge_lim(int dim, const Layout& m, const Gas& g, const double* U, Wo
 // true if the last limiter pass runs over the worklist (EF_WL); the pass before it
 // then needs *wl_n cleared first
 bool edge_lim_worklist();
+long long kernel_launches();
+void add_kernel_launches(long long n);
 // step5: non-final pass row update U_next += lam * sum min(l) P
 void launch_row_upd(int dim, const Layout& m, const Gas& g, const double* U, Work w,
                     StageParams sp, RowSet rs, int q, cudaStream_t st);

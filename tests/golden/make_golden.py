@@ -261,6 +261,74 @@ def c1_full():
     print("c1_full_100", rec["output_sha256"], rec["min_rho"])
 
 
+def input_digest(mat, U0, bc) -> str:
+    """sha256 over the inputs in a fixed order (tests/stated.py recomputes it)."""
+    h = hashlib.sha256()
+    arrs = [mat.indptr, mat.indices, mat.m, mat.c, mat.m_lumped, mat.inv_m, U0]
+    if bc is not None:
+        for a in (bc.inflow_nodes, bc.farfield, bc.slip_nodes, bc.slip_normals):
+            if a is not None:
+                arrs.append(a)
+    for a in arrs:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+def state_digest(U) -> str:
+    return hashlib.sha256(np.ascontiguousarray(U).tobytes()).hexdigest()
+
+
+# BASELINE configs at the step counts BASELINE.json states, at the sizes the
+# reference finishes in minutes here (SURVEY.md §8(c) "Recommended" column).
+# Generator calls are this package's (problems.py), default seeds.
+STATED = {
+    "c2_full_20": dict(gen="mach3_disc", args=(550,), steps=20, every=5,
+                       note="C2 at full size (1.23M nodes), 20-step prefix of the 200"),
+    "c3_128x32x32_100": dict(gen="sod_box", args=(127, 31, 31), steps=100, every=10,
+                             note="C3 Sod box at 128x32x32 nodes (jittered), 100 steps (stated)"),
+    "c4_210k_50": dict(gen="mach3_cylinder", args=(40, 30), steps=50, every=10,
+                       note="C4 extruded O-grid at 0.21M nodes, 50 steps (stated)"),
+    "c5_64_50": dict(gen="periodic_fourier_box", args=(64,), steps=50, every=10,
+                     note="C5 periodic Fourier box at 64^3, 50 steps (stated)"),
+}
+
+
+def stated_case(name, workers):
+    """Run the UNMODIFIED reference Solver for the stated number of SSP-RK3 steps
+    and record digests: input sha256, tau of every step, sha256 of U every
+    `every` steps and at the end, plus norms.  The GPU test and the oracle test
+    regenerate the inputs with problems.py, check the input digest and compare
+    their own digests bit for bit (tests/test_gpu_stated.py)."""
+    import time
+    spec = STATED[name]
+    ps = getattr(P, spec["gen"])(*spec["args"])
+    mat = ps.matrices
+    t0 = time.time()
+    s = RefSolver(to_ref_matrices(mat), boundary=to_ref_bc(ps.boundary), c_cfl=ps.c_cfl,
+                  limiter_passes=2, newton_steps=2, workers=workers)
+    s.set_state(ps.U0)
+    t_setup = time.time() - t0
+    taus, digests = [], {}
+    t0 = time.time()
+    for k in range(1, spec["steps"] + 1):
+        taus.append(s.ssp_rk3_step())
+        if k % spec["every"] == 0 or k == spec["steps"]:
+            U = s.get_state()
+            digests[str(k)] = state_digest(U)
+            print(f"  {name} step {k}: {digests[str(k)][:16]} ({time.time() - t0:.0f} s)", flush=True)
+    U = s.get_state()
+    rec = dict(config=name, note=spec["note"], generator=spec["gen"], args=list(spec["args"]),
+               n=int(mat.n), nnz=int(mat.nnz), dim=int(mat.dim), c_cfl=ps.c_cfl, limiter_passes=2,
+               newton_steps=2, steps=spec["steps"], input_sha256=input_digest(mat, ps.U0, ps.boundary),
+               taus=taus, state_sha256=digests, min_rho=float(U[:, 0].min()),
+               sum_state=np.asarray(U.sum(axis=0)).tolist(),
+               reference=dict(workers=workers, setup_s=round(t_setup, 1),
+                              steps_s=round(time.time() - t0, 1), numpy=np.__version__))
+    with open(os.path.join(HERE, f"stated_{name}.json"), "w") as fh:
+        json.dump(rec, fh, indent=1)
+    print(name, "done", rec["reference"], flush=True)
+
+
 def default_pow_divergence():
     """Report-only: reference with numpy's default pow vs the shared pow."""
     ps = P.isentropic_vortex(32)
@@ -286,9 +354,15 @@ if __name__ == "__main__":
     ap.add_argument("--only-c1-full", action="store_true")
     ap.add_argument("--only-c4", action="store_true")
     ap.add_argument("--only-functions", action="store_true")
+    ap.add_argument("--stated", nargs="*", metavar="CASE",
+                    help=f"reference digests at the stated step counts: {', '.join(STATED)}")
+    ap.add_argument("--workers", type=int, default=os.cpu_count() or 1)
     args = ap.parse_args()
     r_physics.set_power_function(O.shared_pow)
-    if args.only_c4:
+    if args.stated is not None:
+        for name in args.stated or list(STATED):
+            stated_case(name, args.workers)
+    elif args.only_c4:
         c4_case()
     elif args.only_functions:
         function_cases()

@@ -238,3 +238,68 @@ def test_stepping_after_an_error_restarts_from_the_kept_state():
     f.set_state(U)
     assert taus == [f.ssp_rk3_step() for _ in range(3)]
     assert np.array_equal(s.get_state(), f.get_state())
+
+
+def test_async_chain_reports_an_error_of_a_middle_step():
+    """Errors latch across a chain of async steps: a step in the middle of the
+    chain that produces an inadmissible state is reported by sync(), even though
+    the steps after it ran (and reset nothing).  The next set_state starts clean."""
+    ps = P.make_config("c2", scale="small")
+    s = Solver(ps.matrices, c_cfl=ps.c_cfl, boundary=ps.boundary)
+    s.set_state(ps.U0)
+    for _ in range(2):
+        s.ssp_rk3_step()
+    tau = s.tau_last
+    U = s.get_state()
+    s.ssp_rk3_step_async(tau=tau)
+    s.ssp_rk3_step_async(tau=5.0)  # far beyond the CFL bound: inadmissible
+    for _ in range(3):
+        s.ssp_rk3_step_async(tau=tau)
+    with pytest.raises(ValueError):  # AdmissibilityError (projection or bad state)
+        s.sync()
+    s.set_state(U)
+    taus = [s.ssp_rk3_step() for _ in range(2)]
+    f = Solver(ps.matrices, c_cfl=ps.c_cfl, boundary=ps.boundary)
+    f.set_state(U)
+    assert taus == [f.ssp_rk3_step() for _ in range(2)]
+    assert np.array_equal(s.get_state(), f.get_state())
+
+
+def test_synchronous_calls_settle_a_pending_async_step():
+    """ssp_rk3_step / euler_step / get_state after ssp_rk3_step_async continue
+    from the async step's result (no step is lost or recomputed)."""
+    ps = P.make_config("c1", scale="small")
+    a = Solver(ps.matrices, c_cfl=ps.c_cfl, boundary=ps.boundary)
+    a.set_state(ps.U0)
+    a.ssp_rk3_step_async()
+    a.ssp_rk3_step()
+    a.ssp_rk3_step_async()
+    a.euler_step()
+    a.ssp_rk3_step_async()
+    Ua = a.get_state()
+    b = Solver(ps.matrices, c_cfl=ps.c_cfl, boundary=ps.boundary)
+    b.set_state(ps.U0)
+    b.ssp_rk3_step()
+    b.ssp_rk3_step()
+    b.ssp_rk3_step()
+    b.euler_step()
+    b.ssp_rk3_step()
+    assert np.array_equal(Ua, b.get_state())
+    assert a.n_euler_steps == b.n_euler_steps == 13
+
+
+def test_advance_with_changing_tau_max_replays_one_graph():
+    """advance() passes a different tau_max every step; tau and tau_max are
+    kernel inputs in device memory, so graph replay stays bitwise identical to
+    direct launches (and the captured graph is reused: one capture per key)."""
+    ps = P.make_config("c1", scale="small")
+    out = []
+    for graphs in (True, False):
+        s = Solver(ps.matrices, c_cfl=ps.c_cfl, boundary=ps.boundary)
+        s.enable_graphs(graphs)
+        s.set_state(ps.U0)
+        t = []
+        s.advance(0.2, on_step=lambda k, tt: t.append(tt))
+        out.append((t, s.get_state()))
+    assert out[0][0] == out[1][0]
+    assert np.array_equal(out[0][1], out[1][1])

@@ -46,6 +46,39 @@ def _states(rng, n, dim):
     return U
 
 
+@pytest.mark.parametrize("scale", [0.3, 3e-2, 1e-3, 1e-6, 1e-12])
+def test_device_dij_near_states_equals_oracle(scale):
+    """Neighbouring states of a smooth flow: U_j = U_i perturbed by `scale`
+    (relative) in density, velocity and pressure, with c_ji = -c_ij perturbed.
+    Here the 3D path decides most pairs without the exact two-rarefaction p*
+    (lambda_fast: certified enclosure of p*, wave-dominance test), and many pairs
+    sit at the decision boundaries (p* ~ p_i ~ p_j, psi(p_max) ~ 0).  Bitwise
+    equal to the oracle (the reference's operation sequence)."""
+    dim = 3
+    rng = np.random.default_rng(int(1e6 * scale) + 5)
+    n = 400000
+    rho = np.exp(rng.uniform(np.log(0.1), np.log(10.0), n))
+    u = rng.normal(0.0, 1.0, (n, dim))
+    p = np.exp(rng.uniform(np.log(0.1), np.log(10.0), n))
+
+    def cons(rho, u, p):
+        U = np.empty((len(rho), dim + 2))
+        U[:, 0] = rho
+        U[:, 1:-1] = rho[:, None] * u
+        U[:, -1] = p / AIR.gm1 + 0.5 * rho * (u * u).sum(axis=1)
+        return U
+
+    Ui = cons(rho, u, p)
+    Uj = cons(rho * (1 + scale * rng.normal(size=n)), u + scale * rng.normal(size=(n, dim)),
+              p * (1 + scale * rng.normal(size=n)))
+    cij = rng.normal(0.0, 1.0, (n, dim))
+    cji = -cij * (1 + 1e-3 * rng.normal(size=(n, 1)))
+    d, bad = eval_dij(Ui, Uj, cij, cji)
+    do, bo = O.eval_dij(Ui, Uj, cij, cji)
+    assert np.array_equal(bad, bo)
+    assert np.array_equal(d, do)
+
+
 @pytest.mark.parametrize("dim", [2, 3])
 def test_device_dij_equals_oracle_on_random_batches(dim):
     rng = np.random.default_rng(11 + dim)
