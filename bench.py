@@ -239,20 +239,32 @@ def run_ours(args, rank, world, local_rank):
 
     dist = world > 1
     torch.cuda.set_device(local_rank)
-    ps = build_problem(args.config, world)
-    mat = ps.matrices
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
-    if dist:  # one rank per GPU: contiguous CM ranges, NCCL halo exchange + tau allreduce
-        from paper_2007_00094_b200.distributed import DistributedSolver
+    if args.config == "c5w":
+        # per-rank setup: each rank generates only its rows (x-slab of the box in its
+        # lexicographic order) and its ghost layer; NCCL halos for N > 1
+        from paper_2007_00094_b200 import problems as P
+        from paper_2007_00094_b200.distributed import ShardedSolver
 
-        solver = DistributedSolver(mat, c_cfl=ps.c_cfl, boundary=ps.boundary, device=local_rank,
-                                   stream=stream.cuda_stream)
+        ps = P.periodic_fourier_box_local(weak_side(world), rank, world)
+        solver = ShardedSolver(ps.local, c_cfl=ps.c_cfl, device=local_rank, stream=stream.cuda_stream,
+                               nccl=dist)
+        n_nodes, dim = ps.local.n_global, ps.local.dim
+        mat = None
     else:
-        solver = Solver(mat, c_cfl=ps.c_cfl, boundary=ps.boundary, device=local_rank,
-                        stream=stream.cuda_stream)
-    n_nodes = mat.n
-    dim = mat.dim
+        ps = build_problem(args.config, world)
+        mat = ps.matrices
+        if dist:  # one rank per GPU: contiguous CM ranges, NCCL halo exchange + tau allreduce
+            from paper_2007_00094_b200.distributed import DistributedSolver
+
+            solver = DistributedSolver(mat, c_cfl=ps.c_cfl, boundary=ps.boundary, device=local_rank,
+                                       stream=stream.cuda_stream)
+        else:
+            solver = Solver(mat, c_cfl=ps.c_cfl, boundary=ps.boundary, device=local_rank,
+                            stream=stream.cuda_stream)
+        n_nodes = mat.n
+        dim = mat.dim
     card = solver.standard_card
     nnz = solver.nnz_owned
     solver.set_state(ps.U0)
@@ -270,11 +282,13 @@ def run_ours(args, rank, world, local_rank):
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     launches0 = kernel_launches()
+    vol0 = solver.comm.sync_volume
     e0.record(stream)
     for _ in range(args.steps):
         solver.ssp_rk3_step_async()
     e1.record(stream)
     launches = kernel_launches() - launches0
+    halo_bytes = 8.0 * (solver.comm.sync_volume - vol0) / (3 * args.steps)  # received per stage, this rank
     torch.cuda.synchronize()
     if dist:
         torch.distributed.barrier()
@@ -369,7 +383,8 @@ def run_ours(args, rank, world, local_rank):
 
     # e2e through the public API with pinned host buffers
     nv = dim + 2
-    host = torch.empty((n_nodes, nv), dtype=torch.float64).pin_memory()
+    io_rows = ps.local.n_owned if args.config == "c5w" else n_nodes  # a rank's state I/O
+    host = torch.empty((io_rows, nv), dtype=torch.float64).pin_memory()
     Uh = host.numpy()
     solver.set_state(ps.U0)
     solver.get_state(out=Uh)
@@ -392,7 +407,7 @@ def run_ours(args, rank, world, local_rank):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_ms = float(t.item())
     e2e = {"value": n_nodes * 3 * e2e_steps / (e2e_ms * 1e-3), "unit": UNIT,
-           "h2d_bytes_per_step": int(n_nodes * nv * 8), "d2h_bytes_per_step": int(n_nodes * nv * 8),
+           "h2d_bytes_per_step": int(io_rows * nv * 8), "d2h_bytes_per_step": int(io_rows * nv * 8),
            "steps": e2e_steps, "wall_s": wall}
 
     line = {
@@ -403,7 +418,10 @@ def run_ours(args, rank, world, local_rank):
         "config": {"workload": CONFIG_NAMES[args.config], "nodes": int(n_nodes), "nnz_rank0": int(nnz),
                    "dim": dim, "pad_width": solver.pad_width, "standard_card": card,
                    "c_cfl": ps.c_cfl, "limiter_passes": passes, "newton_steps": solver.newton_steps,
-                   "parallelism": f"cm-range partition x{world}, NCCL halo" if world > 1 else "single",
+                   "parallelism": (f"{'x-slab (per-rank setup)' if args.config == 'c5w' else 'cm-range'} "
+                                   f"partition x{world}, NCCL halo" if world > 1 else "single"),
+                   "ghost_fraction_rank0": (solver.n_local - solver.n_owned) / max(solver.n_owned, 1),
+                   "halo_bytes_per_stage_rank0": halo_bytes,
                    "l2": l2_note(nnz * (4 + 1 + 8 * (2 * dim + 1 + 1 + passes)) / 1e6)},
         "roofline": roofline,
         "general_path": general,

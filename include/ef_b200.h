@@ -70,12 +70,12 @@ typedef struct {
   const double* slip_normals;/* (n_slip, dim) unit outward normals */
 } ef_boundary;
 
-/* Partition (exchange.partition, exchange.py:393-445) and device binding. */
+/* Partition (exchange.partition, exchange.py:52-104) and device binding. */
 typedef struct {
   int32_t rank, nranks;      /* contiguous ranges of the global CM order      */
   int32_t device;            /* CUDA device ordinal                           */
   const int64_t* cm_perm;    /* (n) original id -> global Cuthill-McKee id    */
-  const int64_t* ranges;     /* (nranks + 1) CM-id range bounds, or NULL (even split as exchange.py:405-411) */
+  const int64_t* ranges;     /* (nranks + 1) CM-id range bounds, or NULL (even split as exchange.py:64-70) */
   const void* nccl_id;       /* 128-byte ncclUniqueId shared by all ranks (nranks > 1), else NULL */
   void* stream;              /* cudaStream_t to launch on, or NULL for a library-owned stream */
 } ef_dist;
@@ -162,7 +162,7 @@ int ef_pow_bound_device(const double* x, double y, double* out, int64_t n);
  * local row order (benchmarks / zero-copy consumers). */
 int ef_state_device_ptr(ef_solver* h, void** dev_ptr, int64_t* stride);
 
-/* ---- multi-rank (exchange.partition / Communicator, exchange.py:393-222) ----
+/* ---- multi-rank (exchange.partition / Communicator, exchange.py:52-222) ----
  * One process per GPU: rank 0 calls ef_nccl_unique_id, broadcasts the 128
  * bytes, every rank passes them in ef_dist.nccl_id to ef_create; halo syncs are
  * NCCL send/recv, the CFL bound an NCCL allreduce(min).  Ranks created with
@@ -177,16 +177,59 @@ int ef_group_get_state(ef_group* g, double* U);
 int ef_group_euler_step(ef_group* g, int32_t has_tau, double tau, double tau_max, double* tau_used);
 int ef_group_ssp_rk3_step(ef_group* g, int32_t has_tau, double tau, double tau_max, double* tau_used);
 
+/* ---- per-rank setup: no rank holds the global matrix ----
+ * A rank passes only its rows, in a GLOBAL node order chosen by the caller
+ * (its "CM order": the Cuthill-McKee order of exchange.partition,
+ * exchange.py:58-62, or any bandwidth-limited order such as the lexicographic
+ * order of a structured box).  Rank r owns the contiguous global ids
+ * [ranges[r], ranges[r+1]) (exchange.py:64-70) with their full stencils, then
+ * its ghost layer = the off-range columns of its owned rows (exchange.py:78-81),
+ * each ghost row carrying its stencil truncated to local columns
+ * (stepper.py:175-181).  Columns are global ids, ascending per row; values are
+ * those of PrecomputedMatrices (assembly.py:22-50) for the same entries. */
+typedef struct {
+  int64_t n_global;          /* nodes of the whole mesh                        */
+  int32_t dim;               /* 2 or 3                                         */
+  int32_t pad_width;         /* global max stencil cardinality (stepper.py:128-131) */
+  int32_t standard_card;     /* global most frequent cardinality               */
+  int64_t n_owned;           /* = ranges[rank + 1] - ranges[rank]              */
+  int64_t n_ghost;
+  const int64_t* ghost_gid;  /* (n_ghost) ascending global ids                 */
+  const int64_t* rowptr;     /* (n_owned + n_ghost + 1): owned rows, then ghosts */
+  const int64_t* col_gid;    /* (nnz_local) global column ids                  */
+  const double* m;           /* (nnz_local) m_ij  (NULL: plan only)            */
+  const double* c;           /* (nnz_local, dim) c_ij                          */
+  const double* m_lumped;    /* (n_owned + n_ghost)                            */
+  const double* inv_m;       /* (n_owned + n_ghost)                            */
+  const int32_t* full_card;  /* (n_owned + n_ghost) row cardinality in the global matrix */
+} ef_local_matrices;
+
+/* Solver.__init__ for one rank from its own rows.  bc: global ids (rows this
+ * rank does not own are ignored); dist: rank, nranks, device, ranges
+ * (required), nccl_id (one process per GPU) or NULL (same-device group),
+ * stream; dist.cm_perm is not read. */
+int ef_create_local(const ef_local_matrices* lm, const ef_params* prm, const ef_boundary* bc,
+                    const ef_dist* dist, ef_solver** out);
+/* set_state / get_state of a per-rank handle: U is (n_owned, dim+2), the owned
+ * rows in global-id order.  set_state is collective over the ranks (ghost rows
+ * come from their owners; every rank accepts or every rank rejects). */
+int ef_set_state_owned(ef_solver* h, const double* U);
+int ef_get_state_owned(ef_solver* h, double* U);
+int ef_group_set_state_owned(ef_group* g, const double* const* U);  /* U[r]: rank r's rows */
+int ef_group_get_state_owned(ef_group* g, double* const* U);
+
 /* Host-only partition plan of one rank (no CUDA): sizes = {n_owned, n_local,
  * L, nranks}; rows: global CM ids of the rows sent to / received from a peer
- * (recv = 0 / 1) in message order; slots: (row CM id, column CM id) pairs of
- * the limiter-factor messages.  Return the count (-1 on a bad peer). */
+ * (recv = 0 / 1) in message order.  Every exchanged quantity is per row (the
+ * edge kernel recomputes ghost-side limiter factors), so there are no slot
+ * messages.  Return the count (-1 on a bad peer).  ef_plan_build_local builds
+ * the same plan from the rank's own rows (lm->m / lm->c may be NULL). */
 typedef struct ef_plan ef_plan;
 int ef_plan_build(const ef_matrices* mat, const ef_dist* dist, ef_plan** out);
+int ef_plan_build_local(const ef_local_matrices* lm, const ef_dist* dist, ef_plan** out);
 int ef_plan_destroy(ef_plan* p);
 int ef_plan_sizes(const ef_plan* p, int64_t* out4);
 int64_t ef_plan_rows(const ef_plan* p, int32_t peer, int32_t recv, int64_t* out_gids, int64_t cap);
-int64_t ef_plan_slots(const ef_plan* p, int32_t peer, int32_t recv, int64_t* out_pairs, int64_t cap);
 
 #ifdef __cplusplus
 }

@@ -6,7 +6,7 @@ bench.py's cpu_baseline / --impl reference legs, never by the product.
 `OracleSolver` mirrors the reference `Solver` API
 (/root/reference/pkg/src/eulerflow/stepper.py:87-649) for a single rank.  Its
 setup restates the reference's global ordering independently of the product:
-the Cuthill-McKee permutation of `exchange.partition` (exchange.py:393-403),
+the Cuthill-McKee permutation of `exchange.partition` (exchange.py:58-62),
 the CM-permuted CSR of `Solver._permute_matrices` (stepper.py:143-161) and the
 global pad width (stepper.py:128-131).  Slot order inside a row is ascending
 CM id (stepper.py:195), which fixes every floating-point reduction order.
@@ -89,7 +89,7 @@ def shared_pow(x, y):
 
 
 def cm_permutation(matrices):
-    """Global Cuthill-McKee order exactly as exchange.partition (exchange.py:397-403)."""
+    """Global Cuthill-McKee order exactly as exchange.partition (exchange.py:58-62)."""
     n = matrices.n
     conn = sp.csr_matrix(
         (np.ones(len(matrices.indices), dtype=np.int8), matrices.indices, matrices.indptr),
@@ -107,7 +107,10 @@ class OracleSolver:
     """Single-rank CPU restatement of the reference Solver (test infrastructure)."""
 
     def __init__(self, matrices, c_cfl=0.9, limiter_passes=2, newton_steps=2,
-                 boundary=None, gas=None, threads=1):
+                 boundary=None, gas=None, threads=1, cm_perm=None):
+        """cm_perm: original id -> global order id replacing the Cuthill-McKee order
+        (the per-rank setup's generator order, e.g. a box's lexicographic order);
+        slots are sorted by it like the reference sorts them by CM id."""
         if not 0.0 < c_cfl <= 1.0:
             raise ValueError("c_cfl must lie in (0, 1]")
         if limiter_passes < 0:
@@ -121,7 +124,12 @@ class OracleSolver:
         self.dim = int(matrices.dim)
         self.nvar = self.dim + 2
         n, d = self.n, self.dim
-        self.cm_perm, self.cm_inv = cm_permutation(matrices)
+        if cm_perm is None:
+            self.cm_perm, self.cm_inv = cm_permutation(matrices)
+        else:
+            self.cm_perm = np.asarray(cm_perm, dtype=np.int64)
+            self.cm_inv = np.empty_like(self.cm_perm)
+            self.cm_inv[self.cm_perm] = np.arange(n)
         indptr = np.asarray(matrices.indptr, dtype=np.int64)
         indices = np.asarray(matrices.indices, dtype=np.int64)
         card_o = np.diff(indptr)

@@ -37,6 +37,12 @@ class EfBoundary(ctypes.Structure):
                 ("slip", _p), ("slip_normals", _p)]
 
 
+class EfLocalMatrices(ctypes.Structure):
+    _fields_ = [("n_global", _i64), ("dim", _i32), ("pad_width", _i32), ("standard_card", _i32),
+                ("n_owned", _i64), ("n_ghost", _i64), ("ghost_gid", _p), ("rowptr", _p), ("col_gid", _p),
+                ("m", _p), ("c", _p), ("m_lumped", _p), ("inv_m", _p), ("full_card", _p)]
+
+
 class EfDist(ctypes.Structure):
     _fields_ = [("rank", _i32), ("nranks", _i32), ("device", _i32), ("cm_perm", _p), ("ranges", _p),
                 ("nccl_id", _p), ("stream", _p)]
@@ -81,7 +87,13 @@ SIGNATURES = {
     "ef_plan_destroy": (_i32, [_p]),
     "ef_plan_sizes": (_i32, [_p, _p]),
     "ef_plan_rows": (_i64, [_p, _i32, _i32, _p, _i64]),
-    "ef_plan_slots": (_i64, [_p, _i32, _i32, _p, _i64]),
+    "ef_plan_build_local": (_i32, [ctypes.POINTER(EfLocalMatrices), ctypes.POINTER(EfDist), ctypes.POINTER(_p)]),
+    "ef_create_local": (_i32, [ctypes.POINTER(EfLocalMatrices), ctypes.POINTER(EfParams),
+                               ctypes.POINTER(EfBoundary), ctypes.POINTER(EfDist), ctypes.POINTER(_p)]),
+    "ef_set_state_owned": (_i32, [_p, _p]),
+    "ef_get_state_owned": (_i32, [_p, _p]),
+    "ef_group_set_state_owned": (_i32, [_p, _p]),
+    "ef_group_get_state_owned": (_i32, [_p, _p]),
 }
 
 _lib = None

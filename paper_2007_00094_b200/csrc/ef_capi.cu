@@ -121,10 +121,11 @@ struct ef_solver {
   int64_t* orig_dev = nullptr;
   std::vector<int64_t> orig_host, gid_host;
   // halo plans (per peer rank): counts and offsets in rows / slots, device index lists
-  std::vector<int64_t> xs_rows, xr_rows, xs_slots, xr_slots;   // counts
-  std::vector<int64_t> os_rows, or_rows, os_slots, or_slots;   // offsets
-  int32_t *send_rows = nullptr, *recv_rows = nullptr, *send_pos = nullptr, *recv_pos = nullptr;
-  int64_t n_send_rows = 0, n_recv_rows = 0, n_send_pos = 0, n_recv_pos = 0;
+  std::vector<int64_t> xs_rows, xr_rows;   // counts
+  std::vector<int64_t> os_rows, or_rows;   // offsets
+  int32_t *send_rows = nullptr, *recv_rows = nullptr;
+  int64_t n_send_rows = 0, n_recv_rows = 0;
+  bool local_io = false;  // per-rank setup: state I/O over the owned rows (ef_*_state_owned)
   double *sendbuf = nullptr, *recvbuf = nullptr;
   int64_t sync_count = 0, sync_volume = 0;  // Solver.comm counters (exchange.py:131-157)
   // communication overlap (stepper.py Alg. 4, exchange.py:168-222): rows other
@@ -155,8 +156,8 @@ struct ef_solver {
   // into phase_s when the ring fills or the timers are read
   std::vector<std::array<cudaEvent_t, 8>> ring;
   int ring_used = 0;
-  // CUDA graphs of whole steps (single rank, timers off): one launch replays the
-  // ~25 kernels and memsets of an RK step.  Keyed by everything the captured
+  // CUDA graphs of whole steps (timers off; a group's graph lives on rank 0's
+  // handle): one launch replays the ~25 kernels and memsets of an RK step.  Keyed by everything the captured
   // launches depend on; a few entries cover the rotating U buffers.
   // (tau and tau_max are read by the kernels from Work::tau_arg, written before
   // every launch, so they are not part of the key)
@@ -171,6 +172,7 @@ struct ef_solver {
     cudaGraphExec_t exec;
     uint64_t used;
     long long launches;  // kernels captured (added to the launch count per replay)
+    std::vector<std::pair<int64_t, int64_t>> syncs;  // per rank: halo syncs, volume per replay
   };
   std::vector<GraphEntry> graphs;
   uint64_t graph_clock = 0;
@@ -234,13 +236,75 @@ static Gas make_gas(const ef_params* p) {
 }
 
 // ---------------------------------------------------------------- setup
+// Values behind a plan's local rows: entry values indexed by Plan::src(k), and
+// per local row the lumped mass, the full-stencil cardinality and the caller's
+// node id (state I/O and boundary lists).
+struct Src {
+  const double* m = nullptr;
+  const double* c = nullptr;
+  std::vector<double> m_lumped, inv_m;
+  std::vector<uint8_t> cardf;
+  std::vector<int64_t> orig;
+  const int64_t* cm_perm = nullptr;  // caller id -> global id (boundary lists); null: identity
+  bool local_io = false;             // state I/O over the owned rows (per-rank setup)
+};
+
+static int build_from_plan(ef_solver* h, ef::Plan& P, Src& S, const ef_boundary* bc);
+
 static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, const ef_dist* dist) {
-  const int D = h->dim, NV = h->nvar;
   const int64_t n = mat->n;
   if (!dist || !dist->cm_perm) return fail(EF_ERR_ARG, "ef_dist.cm_perm is required");
   ef::Plan P;
   if (!ef::build_plan(n, mat->indptr, mat->indices, dist->cm_perm, h->rank, h->nranks, dist->ranges, P))
     return fail(EF_ERR_ARG, P.error);
+  Src S;
+  S.m = mat->m;
+  S.c = mat->c;
+  S.cm_perm = dist->cm_perm;
+  const int64_t n_local = P.n_local;
+  S.orig.resize(n_local);
+  S.m_lumped.resize(n_local);
+  S.inv_m.resize(n_local);
+  S.cardf.resize(n_local);
+  ef::parallel_for(n_local, [&](int64_t a, int64_t b, int) {
+    for (int64_t i = a; i < b; ++i) {
+      const int64_t o = P.cm_inv[P.gid[i]];
+      S.orig[i] = o;
+      S.m_lumped[i] = mat->m_lumped[o];
+      S.inv_m[i] = mat->inv_m[o];
+      S.cardf[i] = (uint8_t)(mat->indptr[o + 1] - mat->indptr[o]);
+    }
+  });
+  return build_from_plan(h, P, S, bc);
+}
+
+// per-rank setup: the rank's rows only (ef_create_local)
+static int build_local(ef_solver* h, const ef_local_matrices* lm, const ef_boundary* bc, const ef_dist* dist) {
+  ef::Plan P;
+  if (!ef::build_plan_local(lm->n_global, lm->n_owned, lm->n_ghost, lm->ghost_gid, lm->rowptr, lm->col_gid,
+                            lm->pad_width, lm->standard_card, h->rank, h->nranks, dist ? dist->ranges : nullptr, P))
+    return fail(EF_ERR_ARG, P.error);
+  if (!lm->m || !lm->c || !lm->m_lumped || !lm->inv_m || !lm->full_card)
+    return fail(EF_ERR_ARG, "ef_local_matrices values are required");
+  Src S;
+  S.m = lm->m;
+  S.c = lm->c;
+  S.local_io = true;
+  const int64_t n_local = P.n_local;
+  S.orig.assign(P.gid.begin(), P.gid.end());
+  S.m_lumped.assign(lm->m_lumped, lm->m_lumped + n_local);
+  S.inv_m.assign(lm->inv_m, lm->inv_m + n_local);
+  S.cardf.resize(n_local);
+  for (int64_t i = 0; i < n_local; ++i) {
+    if (lm->full_card[i] < 1 || lm->full_card[i] > P.L) return fail(EF_ERR_ARG, "full_card out of range");
+    S.cardf[i] = (uint8_t)lm->full_card[i];
+  }
+  return build_from_plan(h, P, S, bc);
+}
+
+static int build_from_plan(ef_solver* h, ef::Plan& P, Src& S, const ef_boundary* bc) {
+  const int D = h->dim, NV = h->nvar;
+  const int64_t n = P.n;
   const int L = P.L;
   const int64_t n_owned = P.n_owned, n_local = P.n_local;
   h->L = L;
@@ -254,10 +318,8 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
   if (NPL >= (int64_t)1 << 31 || (int64_t)NV * NP >= (int64_t)1 << 31)
     return fail(EF_ERR_ARG, "local rows/slots exceed 32-bit indexing (use more ranks)");
   h->gid_host = P.gid;
-  h->orig_host.resize(n_local);
-  ef::parallel_for(n_local, [&](int64_t a, int64_t b, int) {
-    for (int64_t i = a; i < b; ++i) h->orig_host[i] = P.cm_inv[P.gid[i]];
-  });
+  h->orig_host = std::move(S.orig);
+  h->local_io = S.local_io;
   auto local_of = [&](int64_t g) -> int64_t {
     if (g >= P.s_lo && g < P.s_hi) return g - P.s_lo;
     auto it = std::lower_bound(P.gid.begin() + n_owned, P.gid.end(), g);
@@ -287,22 +349,25 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
         for (int d = 0; d < D; ++d) c[(size_t)d * NPL + p] = 0.0;
       }
       if (i >= n_local) continue;
-      const int64_t o = h->orig_host[i];
       card[i] = (uint8_t)cnt;
       if (i < n_owned) nnz_part += cnt;
       int dg = -1;
       for (int64_t s = 0; s < cnt; ++s) {
-        const int64_t cg = P.rcm[P.rptr[i] + s];
+        const int64_t cg = P.cols[P.rptr[i] + s];
         const int64_t j = local_of(cg);
-        const int64_t q = P.rsrc[P.rptr[i] + s];
+        const int64_t q = P.src(P.rptr[i] + s);
         const int64_t p = ef::sidx(i, (int)s, L);
         col[p] = (int32_t)j;
         if (j == i) dg = (int)s;
-        mij[p] = mat->m[q];
-        for (int d = 0; d < D; ++d) c[(size_t)d * NPL + p] = mat->c[q * D + d];
+        mij[p] = S.m[q];
+        for (int d = 0; d < D; ++d) c[(size_t)d * NPL + p] = S.c[q * D + d];
         // transpose slot: position of this row's CM id in row j (both rows local)
-        const int64_t* rb = P.rcm.data() + P.rptr[j];
-        const int64_t* re = P.rcm.data() + P.rptr[j + 1];
+        if (j < 0) {
+          bad.store(1);
+          continue;
+        }
+        const int64_t* rb = P.cols + P.rptr[j];
+        const int64_t* re = P.cols + P.rptr[j + 1];
         const int64_t* it = std::lower_bound(rb, re, P.gid[i]);
         if (it == re || *it != P.gid[i]) {
           bad.store(1);
@@ -316,9 +381,9 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
         dg = 0;
       }
       diag[i] = (uint8_t)dg;
-      cardf[i] = (uint8_t)(mat->indptr[o + 1] - mat->indptr[o]);
-      m_i[i] = mat->m_lumped[o];
-      inv_m[i] = mat->inv_m[o];
+      cardf[i] = S.cardf[i];
+      m_i[i] = S.m_lumped[i];
+      inv_m[i] = S.inv_m[i];
       const int64_t den = std::max<int64_t>(cnt - 1, 1);
       lam[i] = 1.0 / (double)den;  // stepper.py:214-215
       gid[i] = P.gid[i];
@@ -382,7 +447,7 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
     for (int64_t q = 0; q < bc->n_slip; ++q) {
       const int64_t o = bc->slip[q];
       if (o < 0 || o >= n) return fail(EF_ERR_ARG, "slip node id out of range");
-      const int64_t g = dist->cm_perm[o];
+      const int64_t g = S.cm_perm ? S.cm_perm[o] : o;
       if (g < P.s_lo || g >= P.s_hi) continue;
       const int64_t i = g - P.s_lo;
       bc_kind[i] |= 1;
@@ -391,7 +456,7 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
     for (int64_t q = 0; q < bc->n_inflow; ++q) {
       const int64_t o = bc->inflow[q];
       if (o < 0 || o >= n) return fail(EF_ERR_ARG, "inflow node id out of range");
-      const int64_t g = dist->cm_perm[o];
+      const int64_t g = S.cm_perm ? S.cm_perm[o] : o;
       if (g < P.s_lo || g >= P.s_hi) continue;
       bc_kind[g - P.s_lo] |= 2;
     }
@@ -404,26 +469,16 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
   const int R = h->nranks;
   h->xs_rows.assign(R, 0);
   h->xr_rows.assign(R, 0);
-  h->xs_slots.assign(R, 0);
-  h->xr_slots.assign(R, 0);
   h->os_rows.assign(R + 1, 0);
   h->or_rows.assign(R + 1, 0);
-  h->os_slots.assign(R + 1, 0);
-  h->or_slots.assign(R + 1, 0);
-  std::vector<int32_t> srows, rrows, spos, rpos;
+  std::vector<int32_t> srows, rrows;
   for (int q = 0; q < R; ++q) {
     for (int64_t i : P.send_rows[q]) srows.push_back((int32_t)i);
     for (int64_t i : P.recv_rows[q]) rrows.push_back((int32_t)i);
-    for (int64_t e : P.send_slots[q]) spos.push_back((int32_t)ef::sidx(e / 256, (int)(e % 256), L));
-    for (int64_t e : P.recv_slots[q]) rpos.push_back((int32_t)ef::sidx(e / 256, (int)(e % 256), L));
     h->xs_rows[q] = (int64_t)P.send_rows[q].size();
     h->xr_rows[q] = (int64_t)P.recv_rows[q].size();
-    h->xs_slots[q] = (int64_t)P.send_slots[q].size();
-    h->xr_slots[q] = (int64_t)P.recv_slots[q].size();
     h->os_rows[q + 1] = h->os_rows[q] + h->xs_rows[q];
     h->or_rows[q + 1] = h->or_rows[q] + h->xr_rows[q];
-    h->os_slots[q + 1] = h->os_slots[q] + h->xs_slots[q];
-    h->or_slots[q + 1] = h->or_slots[q] + h->xr_slots[q];
   }
   h->n_send_rows = (int64_t)srows.size();
   h->n_recv_rows = (int64_t)rrows.size();
@@ -466,8 +521,6 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
     h->rs_B = B;
     h->rs_I = I;
   }
-  h->n_send_pos = (int64_t)spos.size();
-  h->n_recv_pos = (int64_t)rpos.size();
 
   // ---- device images
   Layout& m = h->lay;
@@ -521,11 +574,9 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
   if (R > 1) {
     EF_TRY(upload(h, &h->send_rows, srows));
     EF_TRY(upload(h, &h->recv_rows, rrows));
-    EF_TRY(upload(h, &h->send_pos, spos));
-    EF_TRY(upload(h, &h->recv_pos, rpos));
     // the widest message row: R, U^L and bounds after the low-order update
-    const int64_t sb = std::max(h->n_send_rows * (2 * NV + 3), h->n_send_pos);
-    const int64_t rbn = std::max(h->n_recv_rows * (2 * NV + 3), h->n_recv_pos);
+    const int64_t sb = h->n_send_rows * (2 * NV + 3);
+    const int64_t rbn = h->n_recv_rows * (2 * NV + 3);
     EF_TRY(h->alloc(&h->sendbuf, sb));
     EF_TRY(h->alloc(&h->recvbuf, rbn));
   }
@@ -580,8 +631,15 @@ static int build(ef_solver* h, const ef_matrices* mat, const ef_boundary* bc, co
     EF_TRY(h->alloc(&h->Ubuf[k], (size_t)NV * NP));
     EF_CUDA(cudaMemset(h->Ubuf[k], 0, sizeof(double) * NV * NP));
   }
-  EF_TRY(h->alloc(&h->aos_dev, (size_t)n * NV));
-  EF_TRY(upload(h, &h->orig_dev, h->orig_host));
+  if (h->local_io) {  // owned rows only: no rank holds an n_global-sized array
+    EF_TRY(h->alloc(&h->aos_dev, (size_t)n_owned * NV));
+    std::vector<int64_t> iota(n_owned);
+    for (int64_t i = 0; i < n_owned; ++i) iota[i] = i;
+    EF_TRY(upload(h, &h->orig_dev, iota));
+  } else {
+    EF_TRY(h->alloc(&h->aos_dev, (size_t)n * NV));
+    EF_TRY(upload(h, &h->orig_dev, h->orig_host));
+  }
   EF_CUDA(cudaMallocHost((void**)&h->rb, sizeof(ef_solver::Readback)));
   return EF_OK;
 }
@@ -845,6 +903,19 @@ static int rk3_async(Driver& d, int32_t has_tau, int* out_buf) {
 // the timers off replays a CUDA graph of the step's launches, captured on first
 // use per (kind, U buffer, tau arguments); anything else launches directly.  A
 // capture that fails turns graphs off for the handle and runs the step directly.
+// One step (forward Euler or SSP-RK3) queued on the stream.  With the timers
+// off, the step's launches (all ranks of a same-device group, or one NCCL rank
+// with its send/recv and allreduce calls and the comm-stream halo overlap) are
+// captured once per key into a CUDA graph and replayed with one
+// cudaGraphLaunch; the step counters and halo statistics the capture recorded
+// are re-added per replay.  A capture that fails turns graphs off for the
+// handle and runs the step directly.  EF_GRAPHS_NCCL=0 keeps NCCL ranks on
+// direct launches.
+static bool graphs_nccl() {
+  const char* e = std::getenv("EF_GRAPHS_NCCL");
+  return !(e && e[0] == '0');
+}
+
 static int step_async(Driver& d, bool rk3, int32_t has_tau, double tau, double tau_max, int* out_buf) {
   ef_solver* h = d.h0();
   // the step's tau arguments: a pageable-source copy is staged at the call, so the
@@ -855,18 +926,25 @@ static int step_async(Driver& d, bool rk3, int32_t has_tau, double tau, double t
   auto body = [&]() {
     return rk3 ? rk3_async(d, has_tau, out_buf) : euler_async(d, has_tau, out_buf);
   };
-  if (!h->use_graphs || h->timing || d.group || h->nranks > 1) return body();
-  const ef_solver::GraphKey key{rk3 ? 1 : 0, h->cur, has_tau ? 1 : 0, h->uni_on ? 1 : 0};
+  if (!h->use_graphs || h->timing || (h->use_nccl && !graphs_nccl())) return body();
+  int uni_mask = 0;  // every rank picks its identical-state mode on its own
+  for (size_t r = 0; r < d.hs.size(); ++r) uni_mask |= (d.hs[r]->uni_on ? 1 : 0) << (r & 31);
+  const ef_solver::GraphKey key{rk3 ? 1 : 0, h->cur, has_tau ? 1 : 0, uni_mask};
   for (auto& g : h->graphs)
     if (g.key == key) {
       g.used = ++h->graph_clock;
       EF_CUDA(cudaGraphLaunch(g.exec, h->st));
       ef::add_kernel_launches(g.launches);
       *out_buf = (h->cur + 1) % 3;  // euler: in + 1; rk3: u0 + 1
-      h->n_euler += rk3 ? 3 : 1;
+      for (size_t r = 0; r < d.hs.size(); ++r) {
+        d.hs[r]->n_euler += rk3 ? 3 : 1;
+        d.hs[r]->sync_count += g.syncs[r].first;
+        d.hs[r]->sync_volume += g.syncs[r].second;
+      }
       return EF_OK;
     }
-  const int64_t n0 = h->n_euler;
+  std::vector<std::array<int64_t, 3>> before;
+  for (ef_solver* r : d.hs) before.push_back({r->n_euler, r->sync_count, r->sync_volume});
   const long long l0 = ef::kernel_launches();
   cudaError_t e = cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal);
   int rc = e == cudaSuccess ? body() : EF_ERR_CUDA;
@@ -879,7 +957,11 @@ static int step_async(Driver& d, bool rk3, int32_t has_tau, double tau, double t
     if (exec) cudaGraphExecDestroy(exec);
     cudaGetLastError();
     h->use_graphs = false;
-    h->n_euler = n0;
+    for (size_t r = 0; r < d.hs.size(); ++r) {
+      d.hs[r]->n_euler = before[r][0];
+      d.hs[r]->sync_count = before[r][1];
+      d.hs[r]->sync_volume = before[r][2];
+    }
     return body();
   }
   if (h->graphs.size() >= 8) {
@@ -888,8 +970,11 @@ static int step_async(Driver& d, bool rk3, int32_t has_tau, double tau, double t
     cudaGraphExecDestroy(old->exec);
     h->graphs.erase(old);
   }
-  h->graphs.push_back({key, exec, ++h->graph_clock, ef::kernel_launches() - l0});
-  EF_CUDA(cudaGraphLaunch(exec, h->st));  // n_euler was advanced by the captured body
+  std::vector<std::pair<int64_t, int64_t>> syncs;
+  for (size_t r = 0; r < d.hs.size(); ++r)
+    syncs.push_back({d.hs[r]->sync_count - before[r][1], d.hs[r]->sync_volume - before[r][2]});
+  h->graphs.push_back({key, exec, ++h->graph_clock, ef::kernel_launches() - l0, syncs});
+  EF_CUDA(cudaGraphLaunch(exec, h->st));  // the counters were advanced by the captured body
   return EF_OK;
 }
 
@@ -977,17 +1062,34 @@ static int finish(Driver& d, int out_buf, double* tau_used) {
   return EF_OK;
 }
 
-static int set_state_all(Driver& d, const double* U) {
+// Us[r]: rank r's input -- the whole state in original node order (global
+// setup), or the rank's owned rows (per-rank setup; ghost rows then come from
+// their owners through one halo exchange).  Every rank reaches the same verdict
+// (NCCL max of the flags), so a rejected state leaves every rank unchanged.
+static int set_state_all(Driver& d, const double* const* Us) {
   int bad = 0;
-  for (ef_solver* h : d.hs) {
+  for (size_t r = 0; r < d.hs.size(); ++r) {
+    ef_solver* h = d.hs[r];
     if (h->pending_out >= 0) {  // a new state replaces an unchecked async result
       EF_CUDA(cudaStreamSynchronize(h->st));
       h->pending_out = -1;
     }
     const int spare = (h->cur + 1) % 3;
     EF_TRY(clear_err(h));
-    EF_CUDA(cudaMemcpyAsync(h->aos_dev, U, sizeof(double) * h->nvar * h->n_global, cudaMemcpyHostToDevice, h->st));
-    ef::launch_gather_state(h->dim, h->lay, h->aos_dev, h->orig_dev, h->Ubuf[spare], h->w.err, h->st);
+    const int64_t rows = h->local_io ? h->n_owned : h->n_global;
+    EF_CUDA(cudaMemcpyAsync(h->aos_dev, Us[r], sizeof(double) * h->nvar * rows, cudaMemcpyHostToDevice, h->st));
+    ef::launch_gather_state(h->dim, h->lay, h->local_io ? h->n_owned : h->n_local, h->aos_dev, h->orig_dev,
+                            h->Ubuf[spare], h->w.err, h->st);
+  }
+  if (d.multi() && d.hs[0]->local_io) {
+    const int NV = d.hs[0]->nvar;
+    EF_TRY(exchange(d, {Fld{[&d](size_t r) { return d.hs[r]->Ubuf[(d.hs[r]->cur + 1) % 3]; }, NV}}, d.hs[0]->st));
+  }
+  if (d.multi() && !d.group) {
+    ef_solver* h0 = d.h0();
+    EF_NCCL(nccl().AllReduce(h0->w.err, h0->w.err, 1, ncclInt32, ncclMax, h0->comm, h0->st));
+  }
+  for (ef_solver* h : d.hs) {
     EF_TRY(readback(h));
     bad |= h->rb->err;
   }
@@ -1004,6 +1106,12 @@ static int set_state_all(Driver& d, const double* U) {
 
 static int get_state_one(ef_solver* h, double* U) {
   const int NV = h->nvar;
+  if (h->local_io) {  // the owned rows, in order
+    ef::launch_scatter_state(h->dim, h->lay, h->Ubuf[h->cur], h->orig_dev, h->aos_dev, h->st);
+    EF_CUDA(cudaMemcpyAsync(U, h->aos_dev, sizeof(double) * NV * h->n_owned, cudaMemcpyDeviceToHost, h->st));
+    EF_CUDA(cudaStreamSynchronize(h->st));
+    return EF_OK;
+  }
   if (h->nranks == 1) {
     ef::launch_scatter_state(h->dim, h->lay, h->Ubuf[h->cur], h->orig_dev, h->aos_dev, h->st);
     EF_CUDA(cudaMemcpyAsync(U, h->aos_dev, sizeof(double) * NV * h->n_global, cudaMemcpyDeviceToHost, h->st));
@@ -1040,37 +1148,19 @@ struct DevBufs {
   }
 };
 
-extern "C" {
-int ef_sync(ef_solver* h, double* tau_used);
-
-const char* ef_last_error(void) { return g_err.c_str(); }
-
-int64_t ef_kernel_launches(void) { return (int64_t)ef::kernel_launches(); }
-
-int ef_nccl_unique_id(void* out128) {
-  if (!out128) return fail(EF_ERR_ARG, "null argument");
-  if (!nccl().ok) return fail(EF_ERR_NCCL, "libnccl.so.2 could not be loaded");
-  ncclUniqueId id;
-  EF_NCCL(nccl().GetUniqueId(&id));
-  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
-  std::memcpy(out128, &id, sizeof id);
-  return EF_OK;
-}
-
-int ef_create(const ef_matrices* mat, const ef_params* prm, const ef_boundary* bc, const ef_dist* dist,
-              ef_solver** out) {
-  if (!mat || !prm || !out) return fail(EF_ERR_ARG, "null argument");
+// common part of ef_create / ef_create_local: `build` fills the layout
+template <class Build>
+static int create_handle(int dim, const ef_params* prm, const ef_dist* dist, ef_solver** out, Build build) {
   *out = nullptr;
   if (!(prm->c_cfl > 0.0 && prm->c_cfl <= 1.0)) return fail(EF_ERR_ARG, "c_cfl must lie in (0, 1]");
   if (prm->limiter_passes < 0) return fail(EF_ERR_ARG, "limiter_passes must be >= 0");
   if (prm->newton_steps < 0) return fail(EF_ERR_ARG, "newton_steps must be >= 0");
-  if (mat->dim != 2 && mat->dim != 3) return fail(EF_ERR_ARG, "dim must be 2 or 3");
-  if (mat->n <= 0) return fail(EF_ERR_ARG, "empty mesh");
+  if (dim != 2 && dim != 3) return fail(EF_ERR_ARG, "dim must be 2 or 3");
   if (dist && (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks))
     return fail(EF_ERR_ARG, "bad rank/nranks");
   ef_solver* h = new ef_solver();
-  h->dim = mat->dim;
-  h->nvar = mat->dim + 2;
+  h->dim = dim;
+  h->nvar = dim + 2;
   h->passes = prm->limiter_passes;
   h->newton = prm->newton_steps;
   h->c_cfl = prm->c_cfl;
@@ -1101,7 +1191,7 @@ int ef_create(const ef_matrices* mat, const ef_params* prm, const ef_boundary* b
     if (ue && (ue[0] == '0' || ue[0] == '1')) h->uni_force = ue[0] - '0';
     h->uni_on = h->uni_force != 0;
   }
-  int rc = build(h, mat, bc, dist);
+  int rc = build(h);
   if (rc != EF_OK) return bail(rc);
   if (h->nranks > 1) {
     e = cudaStreamCreateWithFlags(&h->cst, cudaStreamNonBlocking);
@@ -1119,6 +1209,49 @@ int ef_create(const ef_matrices* mat, const ef_params* prm, const ef_boundary* b
   }
   *out = h;
   return EF_OK;
+}
+
+extern "C" {
+int ef_sync(ef_solver* h, double* tau_used);
+
+// A synchronous call after ef_ssp_rk3_step_async first settles the pending
+// chain (ef_sync: its latched errors are reported by this call).
+static int settle(ef_solver* h) {
+  if (h->pending_out < 0) return EF_OK;
+  return ef_sync(h, nullptr);
+}
+
+
+const char* ef_last_error(void) { return g_err.c_str(); }
+
+int64_t ef_kernel_launches(void) { return (int64_t)ef::kernel_launches(); }
+
+int ef_nccl_unique_id(void* out128) {
+  if (!out128) return fail(EF_ERR_ARG, "null argument");
+  if (!nccl().ok) return fail(EF_ERR_NCCL, "libnccl.so.2 could not be loaded");
+  ncclUniqueId id;
+  EF_NCCL(nccl().GetUniqueId(&id));
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  std::memcpy(out128, &id, sizeof id);
+  return EF_OK;
+}
+
+int ef_create(const ef_matrices* mat, const ef_params* prm, const ef_boundary* bc, const ef_dist* dist,
+              ef_solver** out) {
+  if (!mat || !prm || !out) return fail(EF_ERR_ARG, "null argument");
+  *out = nullptr;
+  if (mat->n <= 0) return fail(EF_ERR_ARG, "empty mesh");
+  return create_handle(mat->dim, prm, dist, out, [&](ef_solver* h) { return build(h, mat, bc, dist); });
+}
+
+int ef_create_local(const ef_local_matrices* lm, const ef_params* prm, const ef_boundary* bc, const ef_dist* dist,
+                    ef_solver** out) {
+  if (!lm || !prm || !out) return fail(EF_ERR_ARG, "null argument");
+  *out = nullptr;
+  if (lm->n_global <= 0 || lm->n_owned < 0 || lm->n_ghost < 0 || !lm->rowptr || !lm->col_gid ||
+      (lm->n_ghost > 0 && !lm->ghost_gid))
+    return fail(EF_ERR_ARG, "bad ef_local_matrices");
+  return create_handle(lm->dim, prm, dist, out, [&](ef_solver* h) { return build_local(h, lm, bc, dist); });
 }
 
 int ef_destroy(ef_solver* h) {
@@ -1143,17 +1276,13 @@ static int single_driver(ef_solver* h, Driver& d) {
 
 int ef_set_state(ef_solver* h, const double* U) {
   if (!h || !U) return fail(EF_ERR_ARG, "null argument");
+  if (h->local_io) return fail(EF_ERR_ARG, "a per-rank handle takes its owned rows: ef_set_state_owned");
   cudaSetDevice(h->device);
   Driver d;
   d.hs = {h};
-  return set_state_all(d, U);
-}
-
-// A synchronous call after ef_ssp_rk3_step_async first settles the pending
-// chain (ef_sync: its latched errors are reported by this call).
-static int settle(ef_solver* h) {
-  if (h->pending_out < 0) return EF_OK;
-  return ef_sync(h, nullptr);
+  d.group = h->nranks > 1 && !h->use_nccl;
+  const double* Us[1] = {U};
+  return set_state_all(d, Us);
 }
 
 int ef_get_state(ef_solver* h, double* U) {
@@ -1179,6 +1308,23 @@ int ef_ssp_rk3_step(ef_solver* h, int32_t has_tau, double tau, double tau_max, d
   int out;
   EF_TRY(step_async(d, true, has_tau, tau, tau_max, &out));
   return finish(d, out, tau_used);
+}
+
+int ef_set_state_owned(ef_solver* h, const double* U) {
+  if (!h || !U) return fail(EF_ERR_ARG, "null argument");
+  if (!h->local_io) return fail(EF_ERR_ARG, "ef_set_state_owned needs a handle from ef_create_local");
+  Driver d;
+  EF_TRY(single_driver(h, d));
+  const double* Us[1] = {U};
+  return set_state_all(d, Us);
+}
+
+int ef_get_state_owned(ef_solver* h, double* U) {
+  if (!h || !U) return fail(EF_ERR_ARG, "null argument");
+  if (!h->local_io) return fail(EF_ERR_ARG, "ef_get_state_owned needs a handle from ef_create_local");
+  cudaSetDevice(h->device);
+  EF_TRY(settle(h));
+  return get_state_one(h, U);
 }
 
 int ef_ssp_rk3_step_async(ef_solver* h, int32_t has_tau, double tau, double tau_max) {
@@ -1426,8 +1572,29 @@ static Driver group_driver(ef_group* g) {
 
 int ef_group_set_state(ef_group* g, const double* U) {
   if (!g || !U) return fail(EF_ERR_ARG, "null argument");
+  if (g->hs[0]->local_io) return fail(EF_ERR_ARG, "per-rank handles take their owned rows: ef_group_set_state_owned");
+  Driver d = group_driver(g);
+  std::vector<const double*> Us(d.hs.size(), U);
+  return set_state_all(d, Us.data());
+}
+
+int ef_group_set_state_owned(ef_group* g, const double* const* U) {
+  if (!g || !U) return fail(EF_ERR_ARG, "null argument");
+  if (!g->hs[0]->local_io) return fail(EF_ERR_ARG, "ef_group_set_state_owned needs handles from ef_create_local");
+  for (size_t r = 0; r < g->hs.size(); ++r)
+    if (!U[r]) return fail(EF_ERR_ARG, "null argument");
   Driver d = group_driver(g);
   return set_state_all(d, U);
+}
+
+int ef_group_get_state_owned(ef_group* g, double* const* U) {
+  if (!g || !U) return fail(EF_ERR_ARG, "null argument");
+  if (!g->hs[0]->local_io) return fail(EF_ERR_ARG, "ef_group_get_state_owned needs handles from ef_create_local");
+  for (size_t r = 0; r < g->hs.size(); ++r) {
+    if (!U[r]) return fail(EF_ERR_ARG, "null argument");
+    EF_TRY(get_state_one(g->hs[r], U[r]));
+  }
+  return EF_OK;
 }
 
 int ef_group_get_state(ef_group* g, double* U) {
@@ -1466,6 +1633,20 @@ int ef_plan_build(const ef_matrices* mat, const ef_dist* dist, ef_plan** out) {
   return EF_OK;
 }
 
+int ef_plan_build_local(const ef_local_matrices* lm, const ef_dist* dist, ef_plan** out) {
+  if (!lm || !dist || !out || !lm->rowptr || !lm->col_gid) return fail(EF_ERR_ARG, "null argument");
+  if (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks) return fail(EF_ERR_ARG, "bad rank/nranks");
+  ef_plan* p = new ef_plan();
+  if (!ef::build_plan_local(lm->n_global, lm->n_owned, lm->n_ghost, lm->ghost_gid, lm->rowptr, lm->col_gid,
+                            lm->pad_width, lm->standard_card, dist->rank, dist->nranks, dist->ranges, p->p)) {
+    std::string msg = p->p.error;
+    delete p;
+    return fail(EF_ERR_ARG, msg);
+  }
+  *out = p;
+  return EF_OK;
+}
+
 int ef_plan_destroy(ef_plan* p) {
   delete p;
   return EF_OK;
@@ -1485,18 +1666,6 @@ int64_t ef_plan_rows(const ef_plan* p, int32_t peer, int32_t recv, int64_t* out_
   const auto& v = recv ? p->p.recv_rows[peer] : p->p.send_rows[peer];
   if (out_gids)
     for (int64_t k = 0; k < (int64_t)v.size() && k < cap; ++k) out_gids[k] = p->p.gid[v[k]];
-  return (int64_t)v.size();
-}
-
-int64_t ef_plan_slots(const ef_plan* p, int32_t peer, int32_t recv, int64_t* out_pairs, int64_t cap) {
-  if (!p || peer < 0 || peer >= p->p.nranks) return -1;
-  const auto& v = recv ? p->p.recv_slots[peer] : p->p.send_slots[peer];
-  if (out_pairs)
-    for (int64_t k = 0; k < (int64_t)v.size() && k < cap; ++k) {
-      const int64_t i = v[k] / 256, t = v[k] % 256;
-      out_pairs[2 * k] = p->p.gid[i];
-      out_pairs[2 * k + 1] = p->p.rcm[p->p.rptr[i] + t];
-    }
   return (int64_t)v.size();
 }
 

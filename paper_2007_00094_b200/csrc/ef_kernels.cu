@@ -206,11 +206,11 @@ __device__ __forceinline__ void pf_l2(const void* p) { asm volatile("prefetch.gl
 
 // ---------------------------------------------------------------- state I/O
 template <int D>
-__global__ void k_gather_state(Layout m, const double* __restrict__ Uaos,
+__global__ void k_gather_state(Layout m, int64_t count, const double* __restrict__ Uaos,
                                const int64_t* __restrict__ orig, double* __restrict__ U, int* err) {
   constexpr int NV = D + 2;
   const int64_t i = blockIdx.x * (int64_t)TPB + threadIdx.x;
-  if (i >= m.n_local) return;
+  if (i >= count) return;
   const int64_t o = orig[i];
   double x[NV];
 #pragma unroll
@@ -1140,16 +1140,6 @@ __global__ void k_unpack_rows(double* __restrict__ field, int ncomp, int64_t NP,
   const int k = (int)(q - r * ncomp);
   field[k * NP + idx[r]] = buf[r * stride + coff + k];
 }
-__global__ void k_pack_pos(const double* __restrict__ arr, const int32_t* __restrict__ pos, int64_t count,
-                           double* __restrict__ buf) {
-  const int64_t q = blockIdx.x * (int64_t)TPB + threadIdx.x;
-  if (q < count) buf[q] = arr[pos[q]];
-}
-__global__ void k_unpack_pos(double* __restrict__ arr, const int32_t* __restrict__ pos, int64_t count,
-                             const double* __restrict__ buf) {
-  const int64_t q = blockIdx.x * (int64_t)TPB + threadIdx.x;
-  if (q < count) arr[pos[q]] = buf[q];
-}
 // min of the CFL bounds of every rank of a same-device group, written back to all
 __global__ void k_group_min(unsigned long long* const* bits, int n) {
   unsigned long long v = ~0ull;
@@ -1187,10 +1177,10 @@ static inline unsigned grid_d(int dim, int64_t n) {
     else KERNEL<3><<<grid_d(3, (N)), EF_TPB3, 0, st>>>(__VA_ARGS__);                                \
   } while (0)
 
-void launch_gather_state(int dim, const Layout& m, const double* U_aos, const int64_t* orig,
+void launch_gather_state(int dim, const Layout& m, int64_t count, const double* U_aos, const int64_t* orig,
                          double* U, int* err, cudaStream_t st) {
-  if (m.n_local == 0) return;
-  EF_DISPATCH(dim, k_gather_state, grid_for(m.n_local), m, U_aos, orig, U, err);
+  if (count == 0) return;
+  EF_DISPATCH(dim, k_gather_state, grid_for(count), m, count, U_aos, orig, U, err);
 }
 void launch_scatter_state(int dim, const Layout& m, const double* U, const int64_t* orig,
                           double* U_aos, cudaStream_t st) {
@@ -1266,12 +1256,6 @@ void launch_unpack_rows(double* field, int ncomp, int64_t NP, const int32_t* idx
                         const double* buf, int stride, int coff, cudaStream_t st) {
   if (count > 0 && EF_COUNT() >= 0)
     k_unpack_rows<<<grid_for(count * ncomp), TPB, 0, st>>>(field, ncomp, NP, idx, count, buf, stride, coff);
-}
-void launch_pack_pos(const double* arr, const int32_t* pos, int64_t count, double* buf, cudaStream_t st) {
-  if (count > 0) k_pack_pos<<<grid_for(count), TPB, 0, st>>>(arr, pos, count, buf);
-}
-void launch_unpack_pos(double* arr, const int32_t* pos, int64_t count, const double* buf, cudaStream_t st) {
-  if (count > 0) k_unpack_pos<<<grid_for(count), TPB, 0, st>>>(arr, pos, count, buf);
 }
 void launch_group_min(unsigned long long* const* bits_dev, int n, cudaStream_t st) {
   EF_COUNT();

@@ -141,7 +141,7 @@ inline RowSet all_rows(int64_t n_owned) {
 }
 
 // launch wrappers (ef_kernels.cu); all asynchronous on `st`
-void launch_gather_state(int dim, const Layout& m, const double* U_aos, const int64_t* orig_of_local,
+void launch_gather_state(int dim, const Layout& m, int64_t count, const double* U_aos, const int64_t* orig_of_local,
                          double* U, int* err, cudaStream_t st);
 void launch_scatter_state(int dim, const Layout& m, const double* U, const int64_t* orig_of_local,
                           double* U_aos, cudaStream_t st);
@@ -176,8 +176,6 @@ void launch_pack_rows(const double* field, int ncomp, int64_t NP, const int32_t*
                       double* buf, int stride, int coff, cudaStream_t st);
 void launch_unpack_rows(double* field, int ncomp, int64_t NP, const int32_t* idx, int64_t count,
                         const double* buf, int stride, int coff, cudaStream_t st);
-void launch_pack_pos(const double* arr, const int32_t* pos, int64_t count, double* buf, cudaStream_t st);
-void launch_unpack_pos(double* arr, const int32_t* pos, int64_t count, const double* buf, cudaStream_t st);
 void launch_group_min(unsigned long long* const* bits_dev, int n, cudaStream_t st);
 // function-level checks: d_ij and the limiter on independent AoS batches
 void launch_eval_dij(int dim, const Gas& g, int64_t n, const double* Ui, const double* Uj, const double* cij,

@@ -1,20 +1,24 @@
 // ef_plan.h — host-side partition, local numbering and halo-exchange plans.
 //
 // Restates the reference's distribution scheme natively
-// (/root/reference/pkg/src/eulerflow/exchange.py:393-445, stepper.py:163-315):
+// (/root/reference/pkg/src/eulerflow/exchange.py:52-104, stepper.py:163-315):
 //   * rank r owns a contiguous range of the global Cuthill-McKee order
-//     (even split as exchange.py:405-411 unless explicit ranges are given);
-//   * its ghost layer = off-range columns of its owned rows (exchange.py:419-422);
+//     (even split as exchange.py:64-70 unless explicit ranges are given);
+//   * its ghost layer = off-range columns of its owned rows (exchange.py:78-81);
 //   * local rows = owned rows (CM order) then ghosts (ascending CM id); a
 //     ghost row carries its stencil truncated to local columns
 //     (stepper.py:175-181); slots of every row are sorted by CM id;
 //   * row messages (alpha, R, U) go owner -> ghost copies
-//     (_build_row_sends, stepper.py:270-285), limiter-factor messages send the
-//     owner's l restricted to the ghost row's truncated stencil
-//     (_build_l_sends, stepper.py:287-315).
-// Every rank derives every plan from the same global CSR + permutation, so
-// send and receive sides agree without any negotiation.  No CUDA here: the
-// CPU tests exercise these plans across gloo ranks.
+//     (_build_row_sends, stepper.py:270-285).  The reference's limiter-factor
+//     messages (_build_l_sends, stepper.py:287-315) have no counterpart: the
+//     edge kernel recomputes a ghost row's factors from halo'd rows (U^L, R,
+//     bounds), so every message is per row.
+// build_plan derives every rank's plan from the same global CSR + permutation;
+// build_plan_local (per-rank setup) from the rank's own rows only: with a
+// structurally symmetric pattern, owned row g is a ghost on rank q exactly when
+// one of g's columns is owned by q, so send and receive sides agree without any
+// negotiation either way.  No CUDA here: the CPU tests exercise these plans
+// across gloo ranks.
 #pragma once
 #include <algorithm>
 #include <atomic>
@@ -34,12 +38,140 @@ struct Plan {
   std::vector<int64_t> cm_inv;        // CM id -> original id
   std::vector<int64_t> gid;           // local row -> CM id
   std::vector<int64_t> rptr;          // local stencils: row pointers,
-  hvec<int64_t> rcm, rsrc;            // CM column ids, source nnz index
+  hvec<int64_t> rcm, rsrc;            // CM column ids, source nnz index (empty: identity)
+  const int64_t* cols = nullptr;      // = rcm.data(), or the caller's local columns
   // halo plans, one entry per peer rank (index = peer rank, empty when none)
   std::vector<std::vector<int64_t>> send_rows, recv_rows;  // local row ids
-  std::vector<std::vector<int64_t>> send_slots, recv_slots;  // local row * 256 + slot
   std::string error;
+  int64_t src(int64_t k) const { return rsrc.empty() ? k : rsrc[k]; }
 };
+
+// ranges given, or the even split of exchange.py:64-70
+inline bool plan_ranges(int64_t n, int nranks, const int64_t* ranges_in, Plan& P) {
+  P.ranges.resize(nranks + 1);
+  if (ranges_in) {
+    for (int q = 0; q <= nranks; ++q) P.ranges[q] = ranges_in[q];
+    if (P.ranges[0] != 0 || P.ranges[nranks] != n) {
+      P.error = "ranges must start at 0 and end at n";
+      return false;
+    }
+    for (int q = 0; q < nranks; ++q)
+      if (P.ranges[q + 1] < P.ranges[q]) {
+        P.error = "ranges must be non-decreasing";
+        return false;
+      }
+  } else {
+    const int64_t base = n / nranks, extra = n % nranks;
+    int64_t start = 0;
+    for (int q = 0; q < nranks; ++q) {
+      P.ranges[q] = start;
+      start += base + (q < extra ? 1 : 0);
+    }
+    P.ranges[nranks] = n;
+  }
+  return true;
+}
+
+inline int plan_owner(const Plan& P, int64_t g) {
+  return (int)(std::upper_bound(P.ranges.begin(), P.ranges.end(), g) - P.ranges.begin()) - 1;
+}
+
+// Per-rank plan from the rank's own rows: owned rows
+// [ranges[rank], ranges[rank+1]) with full stencils, then the ghost rows
+// (ascending global id) with stencils truncated to local columns; columns are
+// global ids, ascending per row.  Nothing global is read or allocated.
+inline bool build_plan_local(int64_t n, int64_t n_owned, int64_t n_ghost, const int64_t* ghost_gid,
+                             const int64_t* rowptr, const int64_t* col_gid, int L, int standard_card, int rank,
+                             int nranks, const int64_t* ranges_in, Plan& P) {
+  P.rank = rank;
+  P.nranks = nranks;
+  P.n = n;
+  if (!ranges_in && nranks > 1) {
+    P.error = "per-rank setup needs the ranges of every rank";
+    return false;
+  }
+  if (!plan_ranges(n, nranks, ranges_in, P)) return false;
+  P.s_lo = P.ranges[rank];
+  P.s_hi = P.ranges[rank + 1];
+  P.n_owned = P.s_hi - P.s_lo;
+  if (P.n_owned != n_owned) {
+    P.error = "n_owned does not match ranges[rank + 1] - ranges[rank]";
+    return false;
+  }
+  if (L < 1 || L > 255) {
+    P.error = "pad width must lie in [1, 255]";
+    return false;
+  }
+  P.L = L;
+  P.standard_card = standard_card;
+  P.n_local = n_owned + n_ghost;
+  P.gid.resize(P.n_local);
+  for (int64_t i = 0; i < n_owned; ++i) P.gid[i] = P.s_lo + i;
+  for (int64_t k = 0; k < n_ghost; ++k) {
+    const int64_t g = ghost_gid[k];
+    if (g < 0 || g >= n || (g >= P.s_lo && g < P.s_hi) || (k > 0 && g <= ghost_gid[k - 1])) {
+      P.error = "ghost ids must be ascending, in range and not owned";
+      return false;
+    }
+    P.gid[n_owned + k] = g;
+  }
+  P.rptr.assign(rowptr, rowptr + P.n_local + 1);
+  P.cols = col_gid;
+  // validation (parallel): row sizes, ascending local columns, owned rows reach
+  // only local rows (their stencils are complete)
+  std::atomic<int> bad{0};
+  auto is_local = [&](int64_t c) -> bool {
+    if (c >= P.s_lo && c < P.s_hi) return true;
+    return std::binary_search(ghost_gid, ghost_gid + n_ghost, c);
+  };
+  parallel_for(P.n_local, [&](int64_t a, int64_t b, int) {
+    for (int64_t i = a; i < b; ++i) {
+      const int64_t lo = rowptr[i], hi = rowptr[i + 1];
+      if (hi < lo || hi - lo > L) {
+        bad.store(1);
+        return;
+      }
+      for (int64_t k = lo; k < hi; ++k)
+        if ((k > lo && col_gid[k] <= col_gid[k - 1]) || !is_local(col_gid[k])) {
+          bad.store(2);
+          return;
+        }
+    }
+  });
+  if (bad.load() == 1) {
+    P.error = "row longer than the pad width (or rowptr not ascending)";
+    return false;
+  }
+  if (bad.load() == 2) {
+    P.error = "columns must be ascending local ids (owned rows need every column in the ghost layer)";
+    return false;
+  }
+  // halo plans: receive my ghosts from their owners; send an owned row to every
+  // rank owning one of its columns (pattern symmetry: then it is a ghost there)
+  P.send_rows.assign(nranks, {});
+  P.recv_rows.assign(nranks, {});
+  for (int64_t k = 0; k < n_ghost; ++k) P.recv_rows[plan_owner(P, ghost_gid[k])].push_back(n_owned + k);
+  if (nranks > 1) {
+    std::vector<std::vector<std::vector<int64_t>>> part(par_threads(), std::vector<std::vector<int64_t>>(nranks));
+    const int nch = parallel_for(n_owned, [&](int64_t a, int64_t b, int t) {
+      auto& out = part[t];
+      std::vector<int> seen;
+      for (int64_t i = a; i < b; ++i) {
+        seen.clear();
+        for (int64_t k = rowptr[i]; k < rowptr[i + 1]; ++k) {
+          const int64_t c = col_gid[k];
+          if (c >= P.s_lo && c < P.s_hi) continue;
+          const int q = plan_owner(P, c);
+          if (std::find(seen.begin(), seen.end(), q) == seen.end()) seen.push_back(q);
+        }
+        for (int q : seen) out[q].push_back(i);
+      }
+    });
+    for (int t = 0; t < nch; ++t)  // chunks are ascending row ranges in thread order
+      for (int q = 0; q < nranks; ++q) P.send_rows[q].insert(P.send_rows[q].end(), part[t][q].begin(), part[t][q].end());
+  }
+  return true;
+}
 
 inline bool build_plan(int64_t n, const int64_t* indptr, const int64_t* indices, const int64_t* cm_perm,
                        int rank, int nranks, const int64_t* ranges_in, Plan& P) {
@@ -55,25 +187,8 @@ inline bool build_plan(int64_t n, const int64_t* indptr, const int64_t* indices,
     }
     P.cm_inv[g] = o;
   }
-  P.ranges.resize(nranks + 1);
-  if (ranges_in) {
-    for (int q = 0; q <= nranks; ++q) P.ranges[q] = ranges_in[q];
-    if (P.ranges[0] != 0 || P.ranges[nranks] != n) {
-      P.error = "ranges must start at 0 and end at n";
-      return false;
-    }
-  } else {  // exchange.py:405-411
-    const int64_t base = n / nranks, extra = n % nranks;
-    int64_t start = 0;
-    for (int q = 0; q < nranks; ++q) {
-      P.ranges[q] = start;
-      start += base + (q < extra ? 1 : 0);
-    }
-    P.ranges[nranks] = n;
-  }
-  auto owner = [&](int64_t g) -> int {
-    return (int)(std::upper_bound(P.ranges.begin(), P.ranges.end(), g) - P.ranges.begin()) - 1;
-  };
+  if (!plan_ranges(n, nranks, ranges_in, P)) return false;  // exchange.py:64-70
+  auto owner = [&](int64_t g) -> int { return plan_owner(P, g); };
   // global pad width and most frequent cardinality (stepper.py:128-131)
   int64_t L = 0;
   std::vector<int64_t> hist(1, 0);
@@ -89,7 +204,7 @@ inline bool build_plan(int64_t n, const int64_t* indptr, const int64_t* indices,
   }
   P.L = (int)L;
   P.standard_card = (int)(std::max_element(hist.begin(), hist.end()) - hist.begin());
-  // ghost layer of every rank (exchange.py:419-422); none with one rank
+  // ghost layer of every rank (exchange.py:78-81); none with one rank
   std::vector<std::vector<int64_t>> ghosts(nranks);
   for (int q = 0; q < nranks && nranks > 1; ++q) {
     const int64_t lo = P.ranges[q], hi = P.ranges[q + 1];
@@ -158,29 +273,18 @@ inline bool build_plan(int64_t n, const int64_t* indptr, const int64_t* indices,
       }
     }
   });
-  // halo plans
+  P.cols = P.rcm.data();
+  // halo plans (row messages only: every exchanged quantity is per row)
   P.send_rows.assign(nranks, {});
   P.recv_rows.assign(nranks, {});
-  P.send_slots.assign(nranks, {});
-  P.recv_slots.assign(nranks, {});
-  for (size_t k = 0; k < mine.size(); ++k) {  // receives: my ghosts by owner, ascending CM id
-    const int64_t g = mine[k];
-    const int q = owner(g);
-    const int64_t j = P.n_owned + (int64_t)k;
-    P.recv_rows[q].push_back(j);
-    for (int64_t t = 0; t < P.rptr[j + 1] - P.rptr[j]; ++t) P.recv_slots[q].push_back(j * 256 + t);
-  }
+  for (size_t k = 0; k < mine.size(); ++k)  // receives: my ghosts by owner, ascending CM id
+    P.recv_rows[owner(mine[k])].push_back(P.n_owned + (int64_t)k);
   for (int q = 0; q < nranks; ++q) {  // sends: my owned rows that are ghosts on q
     if (q == rank) continue;
     const auto& gq = ghosts[q];
     auto lo = std::lower_bound(gq.begin(), gq.end(), P.s_lo);
     auto hi = std::lower_bound(gq.begin(), gq.end(), P.s_hi);
-    for (auto it = lo; it != hi; ++it) {
-      const int64_t i = *it - P.s_lo;
-      P.send_rows[q].push_back(i);
-      for (int64_t t = 0; t < P.rptr[i + 1] - P.rptr[i]; ++t)
-        if (is_local(q, P.rcm[P.rptr[i] + t])) P.send_slots[q].push_back(i * 256 + t);
-    }
+    for (auto it = lo; it != hi; ++it) P.send_rows[q].push_back(*it - P.s_lo);
   }
   return true;
 }

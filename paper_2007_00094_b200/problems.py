@@ -591,13 +591,9 @@ def mach3_cylinder(ny: int = 255, nz: int = 255, seed: int = 2007, gas: GasConst
     return ProblemSetup("c4-mach3-cylinder", mat, U0, bc, c_cfl=0.9, steps=steps, mesh=mesh)
 
 
-def periodic_box_matrices(n: int) -> PrecomputedMatrices:
-    """Q1 matrices of the uniform periodic n^3 hex mesh of the unit cube, built
-    from its translation invariance (every node has the same 27-point stencil
-    values) instead of a per-cell assembly -- O(n^3) memory and time, so the
-    262M-node C5 instance is feasible.  The values are those of `assemble_q1`
-    (same quadrature; the per-offset sums are taken over the 8 cells around a
-    node in a fixed order and m is symmetrised exactly)."""
+def _periodic_stencil(n: int):
+    """The translation-invariant 27-point Q1 stencil of the periodic n^3 box:
+    offsets, m per offset (symmetrised exactly), c per offset, lumped mass."""
     if n < 3:
         raise ValueError("periodic box needs n >= 3")
     h = 1.0 / n
@@ -624,15 +620,23 @@ def periodic_box_matrices(n: int) -> PrecomputedMatrices:
     m_i = m_sym[0]
     for k in range(1, 27):
         m_i = m_i + m_sym[k]
-    N = n ** 3
-    # Away from the periodic seams every row's columns are i + flat(o), already
-    # sorted by the offsets' flat order; only the seam rows need a per-row sort.
+    return offs, m_sym, c_off, m_i
+
+
+def _periodic_rows(n: int, ids: np.ndarray, offs, m_sym, c_off, values: bool = True):
+    """Stencils of the rows `ids` (node id = (ix n + iy) n + iz) of the periodic
+    box: columns ascending, with the matching m and c.  Away from the periodic
+    seams every row's columns are i + flat(o), already sorted by the offsets'
+    flat order; only the seam rows need a per-row sort."""
+    ids = np.asarray(ids, dtype=np.int64)
     flat = (offs[:, 0] * n + offs[:, 1]) * n + offs[:, 2]
     base_order = np.argsort(flat, kind="stable")
-    cols = np.arange(N, dtype=np.int64)[:, None] + flat[base_order][None, :]
-    m = np.broadcast_to(m_sym[base_order], (N, 27)).copy()
-    c = np.broadcast_to(c_off[base_order], (N, 27, 3)).copy()
-    ix, iy, iz = np.unravel_index(np.arange(N, dtype=np.int64), (n, n, n))
+    cols = ids[:, None] + flat[base_order][None, :]
+    m = c = None
+    if values:
+        m = np.broadcast_to(m_sym[base_order], (len(ids), 27)).copy()
+        c = np.broadcast_to(c_off[base_order], (len(ids), 27, 3)).copy()
+    ix, iy, iz = np.unravel_index(ids, (n, n, n))
     seam = np.flatnonzero((ix == 0) | (ix == n - 1) | (iy == 0) | (iy == n - 1) | (iz == 0) | (iz == n - 1))
     sx, sy, sz = ix[seam], iy[seam], iz[seam]
     del ix, iy, iz
@@ -641,9 +645,22 @@ def periodic_box_matrices(n: int) -> PrecomputedMatrices:
         sc[:, k] = (((sx + o[0]) % n) * n + (sy + o[1]) % n) * n + (sz + o[2]) % n
     order = np.argsort(sc, axis=1, kind="stable")
     cols[seam] = np.take_along_axis(sc, order, axis=1)
-    m[seam] = m_sym[order]
-    c[seam] = c_off[order]
-    del sc, order, sx, sy, sz, seam
+    if values:
+        m[seam] = m_sym[order]
+        c[seam] = c_off[order]
+    return cols, m, c
+
+
+def periodic_box_matrices(n: int) -> PrecomputedMatrices:
+    """Q1 matrices of the uniform periodic n^3 hex mesh of the unit cube, built
+    from its translation invariance (every node has the same 27-point stencil
+    values) instead of a per-cell assembly -- O(n^3) memory and time, so the
+    262M-node C5 instance is feasible.  The values are those of `assemble_q1`
+    (same quadrature; the per-offset sums are taken over the 8 cells around a
+    node in a fixed order and m is symmetrised exactly)."""
+    offs, m_sym, c_off, m_i = _periodic_stencil(n)
+    N = n ** 3
+    cols, m, c = _periodic_rows(n, np.arange(N, dtype=np.int64), offs, m_sym, c_off)
     m = m.ravel()
     c = c.reshape(-1, 3)
     m_lumped = np.full(N, m_i)
@@ -652,15 +669,85 @@ def periodic_box_matrices(n: int) -> PrecomputedMatrices:
                                inv_m=1.0 / m_lumped)
 
 
-def periodic_fourier_box(n: int = 320, seed: int = 2007, gas: GasConstants = AIR,
-                         steps: int = 50, modes: int = 8) -> ProblemSetup:
-    """BASELINE C5: periodic n^3 hex mesh; rho, p in [0.5,1.5], |u| <= 1 from a
-    sum of `modes` random low-frequency Fourier modes per field."""
-    mat = periodic_box_matrices(n)
-    ix, iy, iz = np.unravel_index(np.arange(mat.n, dtype=np.int64), (n, n, n))
+@dataclass
+class LocalMatrices:
+    """One rank's rows of a PrecomputedMatrices (per-rank setup, ef_local_matrices in
+    include/ef_b200.h): owned rows [ranges[rank], ranges[rank+1]) with full stencils,
+    then the ghost rows (ascending global id) truncated to local columns; global
+    column ids ascending per row."""
+    n_global: int
+    dim: int
+    pad_width: int
+    standard_card: int
+    rank: int
+    nranks: int
+    ranges: np.ndarray
+    ghost_gid: np.ndarray
+    rowptr: np.ndarray
+    col_gid: np.ndarray
+    m: Optional[np.ndarray]
+    c: Optional[np.ndarray]
+    m_lumped: np.ndarray
+    inv_m: np.ndarray
+    full_card: np.ndarray
+
+    @property
+    def n_owned(self) -> int:
+        return int(self.ranges[self.rank + 1] - self.ranges[self.rank])
+
+    @property
+    def first(self) -> int:
+        return int(self.ranges[self.rank])
+
+
+def even_ranges(n: int, nranks: int) -> np.ndarray:
+    """exchange.partition's split (exchange.py:64-70)."""
+    base, extra = divmod(n, nranks)
+    sizes = [base + (1 if r < extra else 0) for r in range(nranks)]
+    return np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+
+
+def periodic_box_local(n: int, rank: int, nranks: int, values: bool = True) -> LocalMatrices:
+    """Rank `rank`'s rows of periodic_box_matrices(n) in the box's lexicographic
+    node order (x slowest: contiguous ranges are x-slabs), without building the
+    global matrix: O(n^3 / nranks) host memory and time.  Each row equals the
+    matching row of periodic_box_matrices(n) bit for bit (same stencil routine)."""
+    offs, m_sym, c_off, m_i = _periodic_stencil(n)
+    N = n ** 3
+    ranges = even_ranges(N, nranks)
+    a, b = int(ranges[rank]), int(ranges[rank + 1])
+    own_cols, own_m, own_c = _periodic_rows(n, np.arange(a, b, dtype=np.int64), offs, m_sym, c_off, values)
+    off = own_cols[(own_cols < a) | (own_cols >= b)]
+    ghosts = np.unique(off)
+    del off
+    g_cols, g_m, g_c = _periodic_rows(n, ghosts, offs, m_sym, c_off, values)
+    keep = ((g_cols >= a) & (g_cols < b)) | np.isin(g_cols, ghosts)
+    g_card = keep.sum(axis=1)
+    n_own = b - a
+    rowptr = np.empty(n_own + len(ghosts) + 1, dtype=np.int64)
+    rowptr[0] = 0
+    rowptr[1:n_own + 1] = 27 * np.arange(1, n_own + 1, dtype=np.int64)
+    rowptr[n_own + 1:] = 27 * n_own + np.cumsum(g_card)
+    col_gid = np.concatenate([own_cols.ravel(), g_cols[keep]])
+    del own_cols
+    m = c = None
+    if values:
+        m = np.concatenate([own_m.ravel(), g_m[keep]])
+        c = np.concatenate([own_c.reshape(-1, 3), g_c[keep]])
+    n_loc = n_own + len(ghosts)
+    m_lumped = np.full(n_loc, m_i)
+    return LocalMatrices(n_global=N, dim=3, pad_width=27, standard_card=27, rank=rank, nranks=nranks,
+                         ranges=ranges, ghost_gid=ghosts.astype(np.int64), rowptr=rowptr, col_gid=col_gid,
+                         m=m, c=c, m_lumped=m_lumped, inv_m=1.0 / m_lumped,
+                         full_card=np.full(n_loc, 27, dtype=np.int32))
+
+
+def _fourier_state(n: int, ids: np.ndarray, seed: int, gas: GasConstants, modes: int = 8) -> np.ndarray:
+    """The C5 initial state at the nodes `ids` (elementwise in a fixed order:
+    independent of which rows are evaluated together)."""
+    ix, iy, iz = np.unravel_index(np.asarray(ids, dtype=np.int64), (n, n, n))
     rep = np.column_stack([ix, iy, iz]) / float(n)
     del ix, iy, iz
-    mesh = None
     rng = np.random.default_rng(seed)
     fields = []
     chunk = 1 << 20  # row chunks evaluated on all host threads (numpy releases the GIL)
@@ -677,7 +764,6 @@ def periodic_fourier_box(n: int = 320, seed: int = 2007, gas: GasConstants = AIR
             gsum = np.empty(len(rep))
 
             def part(lo, k=k, a=a, ph=ph, gsum=gsum):
-                # elementwise in a fixed order, so the values do not depend on the chunking
                 r = rep[lo:lo + chunk]
                 acc = np.zeros(len(r))
                 for q in range(modes):
@@ -690,8 +776,36 @@ def periodic_fourier_box(n: int = 320, seed: int = 2007, gas: GasConstants = AIR
     rho = 1.0 + 0.5 * fields[0]
     p = 1.0 + 0.5 * fields[1]
     vel = np.column_stack(fields[2:5]) / np.sqrt(3.0)
-    U0 = _conserved(rho, vel, p, gas)
-    return ProblemSetup("c5-periodic-box", mat, U0, None, c_cfl=0.9, steps=steps, mesh=mesh)
+    return _conserved(rho, vel, p, gas)
+
+
+@dataclass
+class LocalProblem:
+    """One rank's share of a problem (per-rank setup): its rows and its owned states."""
+    name: str
+    local: LocalMatrices
+    U0: np.ndarray          # (n_owned, nvar): owned rows, global-id order
+    c_cfl: float
+    steps: int
+
+
+def periodic_fourier_box_local(n: int, rank: int, nranks: int, seed: int = 2007, gas: GasConstants = AIR,
+                               steps: int = 50) -> LocalProblem:
+    """Rank `rank`'s share of periodic_fourier_box(n) (C5 weak scaling: 320^3 per
+    GPU, n = round(320 N^(1/3))).  Rows and states equal those of the global
+    generator for the same global ids."""
+    lm = periodic_box_local(n, rank, nranks)
+    U0 = _fourier_state(n, np.arange(lm.first, lm.first + lm.n_owned, dtype=np.int64), seed, gas)
+    return LocalProblem("c5-periodic-box", lm, U0, c_cfl=0.9, steps=steps)
+
+
+def periodic_fourier_box(n: int = 320, seed: int = 2007, gas: GasConstants = AIR,
+                         steps: int = 50, modes: int = 8) -> ProblemSetup:
+    """BASELINE C5: periodic n^3 hex mesh; rho, p in [0.5,1.5], |u| <= 1 from a
+    sum of `modes` random low-frequency Fourier modes per field."""
+    mat = periodic_box_matrices(n)
+    U0 = _fourier_state(n, np.arange(mat.n, dtype=np.int64), seed, gas, modes)
+    return ProblemSetup("c5-periodic-box", mat, U0, None, c_cfl=0.9, steps=steps, mesh=None)
 
 
 def random_state(rng, n: int, dim: int = 2) -> np.ndarray:

@@ -7,7 +7,7 @@ timers, n_euler_steps, standard_card, comm.sync_count/sync_volume) and the
 same exceptions (ValueError, AdmissibilityError, RuntimeError).  Every stage
 runs as hand-written sm_100a kernels inside libef_b200.so; this module only
 computes the global Cuthill-McKee order (scipy, exactly as
-exchange.partition does, exchange.py:397-403) and marshals arrays.
+exchange.partition does, exchange.py:58-62) and marshals arrays.
 
 `lanes`, `workers` and `chunk_size` are accepted for signature
 compatibility; the reference's results are bitwise independent of them
@@ -16,7 +16,7 @@ computes the exported rows first and moves their halo on a second stream
 while the interior rows are computed (exchange.py:168-222); results are
 identical either way.  `ranks` > 1 partitions the mesh
 into contiguous Cuthill-McKee ranges with ghost layers exactly like the
-reference's simulated ranks (exchange.py:393-445) and steps them in lockstep
+reference's simulated ranks (exchange.py:52-104) and steps them in lockstep
 on one device; one process per GPU with NCCL is
 paper_2007_00094_b200.distributed.DistributedSolver.
 """
@@ -50,7 +50,7 @@ def compute_tau(d_diag: np.ndarray, m_i: np.ndarray, c_cfl: float) -> float:
 
 
 def cm_permutation(matrices):
-    """Global Cuthill-McKee order of exchange.partition (exchange.py:397-403):
+    """Global Cuthill-McKee order of exchange.partition (exchange.py:58-62):
     returns (cm_perm: original -> CM id, cm_inv: CM id -> original)."""
     n = int(matrices.n)
     conn = sp.csr_matrix(

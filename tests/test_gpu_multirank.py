@@ -92,3 +92,86 @@ def test_ranks_identical_state_shortcuts_forced(mode, case, monkeypatch):
     t1, U1, _ = _run(ps.matrices, ps.U0, ps.boundary, 1, 4, c_cfl=ps.c_cfl)
     t3, U3, _ = _run(ps.matrices, ps.U0, ps.boundary, 3, 4, c_cfl=ps.c_cfl)
     assert t1 == t3 and np.array_equal(U1, U3)
+
+
+def test_eight_ranks_c5_64_with_overlap():
+    """The 8-GPU shape on one device: C5 at 64^3 split into 8 CM ranges,
+    overlap on, bitwise equal to one rank."""
+    ps = P.periodic_fourier_box(64)
+    t1, U1, _ = _run(ps.matrices, ps.U0, None, 1, 3)
+    t8, U8, s = _run(ps.matrices, ps.U0, None, 8, 3, overlap=True)
+    assert t1 == t8 and np.array_equal(U1, U8)
+
+
+# ---- per-rank setup (ShardedSolver / ef_create_local) -------------------------
+from paper_2007_00094_b200.distributed import ShardedSolver  # noqa: E402
+
+
+def _box_global(n, steps, **kw):
+    """One rank, the global periodic box matrices in their lexicographic order
+    (identity permutation: the order the per-rank generator uses)."""
+    ps = P.periodic_fourier_box(n)
+    s = Solver(ps.matrices, cm_perm=np.arange(ps.matrices.n), **kw)
+    s.set_state(ps.U0)
+    taus = [s.ssp_rk3_step() for _ in range(steps)]
+    return ps, taus, s.get_state()
+
+
+@pytest.mark.parametrize("ranks", [2, 3, 8])
+@pytest.mark.parametrize("overlap", [True, False])
+def test_sharded_ranks_equal_one_rank(ranks, overlap):
+    """Every rank built from its own rows (no global matrix): bitwise equal to
+    one rank built from the global matrices in the same node order."""
+    n, steps = 16, 4
+    ps, t1, U1 = _box_global(n, steps)
+    parts = [P.periodic_box_local(n, r, ranks) for r in range(ranks)]
+    s = ShardedSolver(parts, overlap=overlap)
+    s.set_state(ps.U0)
+    tR = [s.ssp_rk3_step() for _ in range(steps)]
+    assert t1 == tR
+    assert np.array_equal(U1, s.get_state())
+    assert s.comm.sync_count > 0
+
+
+def test_sharded_single_rank_and_oracle_in_box_order():
+    """R = 1 per-rank setup == global setup == the oracle with the same order."""
+    n, steps = 12, 3
+    ps, t1, U1 = _box_global(n, steps)
+    s = ShardedSolver([P.periodic_box_local(n, 0, 1)])
+    s.set_state(ps.U0)
+    assert [s.ssp_rk3_step() for _ in range(steps)] == t1
+    assert np.array_equal(s.get_state(), U1)
+    o = O.OracleSolver(ps.matrices, cm_perm=np.arange(ps.matrices.n))
+    o.set_state(ps.U0)
+    assert [o.ssp_rk3_step() for _ in range(steps)] == t1
+    assert np.array_equal(o.get_state(), U1)
+
+
+def test_sharded_rejects_inadmissible_state_on_every_rank():
+    n, R = 8, 3
+    ps = P.periodic_fourier_box(n)
+    s = ShardedSolver([P.periodic_box_local(n, r, R) for r in range(R)])
+    s.set_state(ps.U0)
+    bad = ps.U0.copy()
+    bad[n ** 3 - 5, 0] = -1.0  # owned by the last rank, a ghost of rank 0 (periodic wrap)
+    with pytest.raises(ValueError):
+        s.set_state(bad)
+    assert np.array_equal(s.get_state(), ps.U0)
+
+
+@pytest.mark.parametrize("overlap", [True, False])
+def test_group_graph_replay_is_bitwise_identical(overlap):
+    """Multi-rank steps (halo copies on the comm stream, tau min over the
+    ranks) captured into CUDA graphs and replayed equal direct launches; the
+    halo statistics are re-added per replay."""
+    ps = P.mach3_disc(30, seed=4)
+    runs = []
+    for graphs in (True, False):
+        s = Solver(ps.matrices, boundary=ps.boundary, ranks=3, overlap=overlap)
+        s.enable_graphs(graphs)
+        s.set_state(ps.U0)
+        taus = [s.ssp_rk3_step() for _ in range(4)] + [s.euler_step(tau=1e-4)]
+        runs.append((taus, s.get_state(), s.comm.sync_count, s.comm.sync_volume, s.n_euler_steps))
+    (ta, Ua, ca, va, na), (tb, Ub, cb, vb, nb) = runs
+    assert ta == tb and np.array_equal(Ua, Ub)
+    assert (ca, va, na) == (cb, vb, nb)

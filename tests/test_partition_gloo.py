@@ -1,10 +1,11 @@
 """Multi-rank halo protocol across real processes (gloo, CPU).
 
 Each rank builds its own plan (ef_plan_build: contiguous CM ranges, ghost
-layer, truncated ghost stencils -- exchange.py:393-445, stepper.py:163-315)
-from the global matrices alone, sends the global ids of every message it will
-send to the peer, and the peer checks them against what it expects to
-receive: rows for alpha/R/U, (row, column) pairs for the limiter factors."""
+layer, truncated ghost stencils -- exchange.py:52-104, stepper.py:163-315)
+from the global matrices alone -- or, per-rank setup (ef_plan_build_local),
+from its own rows only -- sends the global ids of every message it will send
+to the peer, and the peer checks them against what it expects to receive
+(rows for alpha, R + U^L + bounds, U^L and U; every message is per row)."""
 
 import os
 import socket
@@ -16,7 +17,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2007_00094_b200 import problems as P
-from paper_2007_00094_b200.distributed import partition_plan
+from paper_2007_00094_b200.distributed import partition_plan, partition_plan_local
 from paper_2007_00094_b200.stepper import cm_permutation
 
 
@@ -55,14 +56,19 @@ def _worker(rank, world, port, results):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    try:
+    def plans():
         for name, mat in _cases():
             cm_perm, _ = cm_permutation(mat)
-            plan = partition_plan(mat, rank, world, cm_perm=cm_perm)
+            yield name, mat.n, partition_plan(mat, rank, world, cm_perm=cm_perm)
+        for n in (7, 10):  # per-rank setup: no rank sees the global matrix
+            yield f"c5-local-{n}", n ** 3, partition_plan_local(P.periodic_box_local(n, rank, world, values=False))
+
+    try:
+        for name, n_global, plan in plans():
             # ownership covers every node exactly once
             owned = torch.tensor([plan["n_owned"]], dtype=torch.int64)
             dist.all_reduce(owned)
-            assert int(owned.item()) == mat.n, name
+            assert int(owned.item()) == n_global, name
             # every ghost row is received from exactly one owner
             recv_total = sum(len(r) for r in plan["recv_rows"])
             assert recv_total == plan["n_local"] - plan["n_owned"], name
@@ -74,12 +80,9 @@ def _worker(rank, world, port, results):
                 for peer_first in (rank < q, rank > q):
                     if peer_first:
                         _send_array(plan["send_rows"][q], q)
-                        _send_array(plan["send_slots"][q], q)
                     else:
                         rows = _recv_array(q)
-                        slots = _recv_array(q).reshape(-1, 2)
                         assert np.array_equal(rows, plan["recv_rows"][q]), (name, rank, q)
-                        assert np.array_equal(slots, plan["recv_slots"][q]), (name, rank, q)
             # the halo of each ghost row holds exactly its stencil columns that are local here
             dist.barrier()
         results[rank] = "ok"
@@ -100,7 +103,7 @@ def test_halo_plans_agree_across_gloo_ranks(world):
 
 
 def test_plan_ghost_layer_matches_the_reference_definition():
-    """Ghost rows = off-range columns of the owned rows (exchange.py:419-422)."""
+    """Ghost rows = off-range columns of the owned rows (exchange.py:78-81)."""
     mat = P.mach3_disc(20, seed=5).matrices
     cm_perm, _ = cm_permutation(mat)
     n, R = mat.n, 3
@@ -118,3 +121,36 @@ def test_plan_ghost_layer_matches_the_reference_definition():
         got = np.sort(np.concatenate(plan["recv_rows"]))
         assert np.array_equal(got, ghosts)
         assert plan["n_owned"] == e - s
+
+
+def _gather_worker(rank, world, port, results):
+    from paper_2007_00094_b200.distributed import gather_owned_rows
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n, nvar = 11, 4
+        rng = np.random.default_rng(5)
+        full = rng.normal(size=(n, nvar))
+        full[rng.random((n, nvar)) < 0.3] = -0.0   # negative zeros must survive
+        cm_inv = rng.permutation(n)
+        ranges = np.array([0, 4, 7, 11][: world + 1] if world == 3 else [0, 6, 11])
+        mine = full[cm_inv[ranges[rank]:ranges[rank + 1]]]
+        out = np.full((n, nvar), np.nan)
+        gather_owned_rows(mine, ranges, cm_inv, out)
+        ok = np.array_equal(out.view(np.int64), full.view(np.int64))
+        results[rank] = "ok" if ok else "mismatch"
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_distributed_get_state_gather_keeps_every_bit(world):
+    """DistributedSolver.get_state assembles owned rows by copy (no SUM
+    all_reduce, which turned -0.0 into +0.0)."""
+    ctx = mp.get_context("spawn")
+    results = ctx.Manager().dict()
+    mp.start_processes(_gather_worker, args=(world, _free_port(), results), nprocs=world, join=True,
+                       start_method="spawn")
+    assert dict(results) == {r: "ok" for r in range(world)}
