@@ -1437,6 +1437,14 @@ int ef_debug_fetch(ef_solver* h, int32_t which, int32_t which_pass, double* out)
     case 7: return node_field(h->Ubuf[h->cur], NV);
     case 8: return node_field(h->w.Unext, NV);
     case 9: return slot_field(h->w.ml);  // min(l_ij, l_ji) of the last non-final pass
+    case 10: {  // P_0 as stored: (n_local, L, nvar); the pass structure is applied by the caller
+      std::vector<double> tmp((size_t)NV * NPL);
+      EF_CUDA(cudaMemcpy(tmp.data(), h->w.P, sizeof(double) * NV * NPL, cudaMemcpyDeviceToHost));
+      for (int64_t i = 0; i < n; ++i)
+        for (int s = 0; s < L; ++s)
+          for (int k = 0; k < NV; ++k) out[(i * L + s) * NV + k] = tmp[(size_t)k * NPL + ef::sidx(i, s, (int)L)];
+      return EF_OK;
+    }
   }
   return fail(EF_ERR_ARG, "unknown field");
 }

@@ -259,100 +259,6 @@ __global__ void k_nodal(Layout m, Gas g, const double* __restrict__ U, Work w, i
 }
 
 // ---------------------------------------------------------------- step1a
-// d_ij in two phases per block (the general path, EF_VISC_Q): every thread
-// projects its edge's states and tries lambda_fast for both directions; the
-// edges it cannot decide (two-shock or pressure-dominated waves: about half on
-// a smooth 3D field) are queued in shared memory with their four projections
-// and then evaluated exactly (lambda_max2: the four pows) by the first threads
-// of the block.  The exact work runs on densely packed warps instead of on
-// whichever lanes happen to need it.  Results are the reference's bits either way.
-#ifndef EF_VISC_Q
-#define EF_VISC_Q 1
-#endif
-template <int D>
-__device__ __forceinline__ void edge_visc_queued(const Layout& m, const Gas& g, const double* __restrict__ U,
-                                                 const Work& w, int flags, int e) {
-  constexpr int NV = D + 2;
-  constexpr int NT = EF_TPB_D(D);
-  constexpr int QF = 18;  // 4 projections x (rho, u, p, c), |c_ij|, |c_ji|
-  __shared__ double qv[QF][NT];
-  __shared__ int qp[2][NT];
-  __shared__ int qn;
-  if (threadIdx.x == 0) qn = 0;
-  __syncthreads();
-  const int NP = (int)m.NP, NE = (int)m.n_edges;
-  bool bad = false;
-  if (e < NE) {
-    const int p = m.edges[e];
-    const int i = (int)fdiv((uint32_t)p, m.slab) * 32 + (p & 31);
-    const int j = m.edge_j[e];
-    const int pt = m.edge_pt[e];
-    double Ui[NV], Uj[NV], nij[D], nji[D];
-    load_node<NV>(U, NP, i, Ui);
-    load_node<NV>(U, NP, j, Uj);
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      nij[a] = m.egeo[(size_t)a * NE + e];
-      nji[a] = m.egeo[(size_t)(D + 1 + a) * NE + e];
-    }
-    const double norm_ij = m.egeo[(size_t)D * NE + e], norm_ji = m.egeo[(size_t)(2 * D + 1) * NE + e];
-    const Recip ri = recip(Ui[0]), rj = recip(Uj[0]);
-    // both directions (a zero |c| direction is projected on n = e_1 and then
-    // discarded with its status, as the reference discards it; d_ij_geo)
-    Proj La, Ra, Lb, Rb;
-    const bool ba = project<D>(Ui, ri, nij, g, La) | project<D>(Uj, rj, nij, g, Ra);
-    const bool bb = project<D>(Uj, rj, nji, g, Lb) | project<D>(Ui, ri, nji, g, Rb);
-    bad = (norm_ij > 0.0 && ba) || (norm_ji > 0.0 && bb);
-    double la = 0.0, lb = 0.0;
-    const bool da = !(norm_ij > 0.0) || (EF_LAM_FAST && lambda_fast(La, Ra, g, la));
-    const bool db = !(norm_ji > 0.0) || (EF_LAM_FAST && lambda_fast(Lb, Rb, g, lb));
-    if (da && db) {
-      const double v_ij = norm_ij > 0.0 ? la * norm_ij : 0.0;
-      const double v_ji = norm_ji > 0.0 ? lb * norm_ji : 0.0;
-      const double dv = npmax(v_ij, v_ji);
-      w.d[p] = dv;
-      w.d[pt] = dv;
-    } else {
-      const int k = atomicAdd(&qn, 1);
-      const Proj* pr[4] = {&La, &Ra, &Lb, &Rb};
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        qv[4 * q + 0][k] = pr[q]->rho;
-        qv[4 * q + 1][k] = pr[q]->u;
-        qv[4 * q + 2][k] = pr[q]->p;
-        qv[4 * q + 3][k] = pr[q]->c;
-      }
-      qv[16][k] = norm_ij;
-      qv[17][k] = norm_ji;
-      qp[0][k] = p;
-      qp[1][k] = pt;
-    }
-    // with the shortcuts off: sample (1 block in 8, first stage) how many would apply
-    if ((flags & 2) && (blockIdx.x & 7) == 0) count_hits(same_state<NV>(Ui, Uj), w.n_same);
-  }
-  if (bad) raise_err(w, ERR_PROJECT, flags >> 4, PH_VISC);
-  __syncthreads();
-  const int k = threadIdx.x;
-  if (k < qn) {
-    Proj P4[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      P4[q].rho = qv[4 * q + 0][k];
-      P4[q].u = qv[4 * q + 1][k];
-      P4[q].p = qv[4 * q + 2][k];
-      P4[q].c = qv[4 * q + 3][k];
-    }
-    const double norm_ij = qv[16][k], norm_ji = qv[17][k];
-    double la, lb;
-    lambda_max2(P4[0], P4[1], P4[2], P4[3], g, la, lb);
-    const double v_ij = norm_ij > 0.0 ? la * norm_ij : 0.0;
-    const double v_ji = norm_ji > 0.0 ? lb * norm_ji : 0.0;
-    const double dv = npmax(v_ij, v_ji);
-    w.d[qp[0][k]] = dv;
-    w.d[qp[1][k]] = dv;
-  }
-}
-
 // One thread per upper edge (global id of the column above the row's, i.e. a
 // slot after the diagonal; stepper.py:211, 415).  The edge list holds SELL
 // positions in ascending order, so a warp reads 32 consecutive positions of
@@ -364,10 +270,6 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_EDGE(D), D)) k_edge
   constexpr int NV = D + 2;
   const int e = blockIdx.x * EF_TPB_D(D) + threadIdx.x;
   if ((flags & 1) && e == 0) *w.tau_min_bits = 0x7ff0000000000000ULL;
-  if constexpr (EF_VISC_Q && D == 3 && !UNI) {
-    edge_visc_queued<D>(m, g, U, w, flags, e);
-    return;
-  }
   if (e >= m.n_edges) return;
   const int NP = (int)m.NP, NE = (int)m.n_edges;
   if (UNI && EF_PF_VISC_UNI > 0 && e + EF_PF_VISC_UNI < NE) {
@@ -1303,25 +1205,7 @@ __global__ void k_eval_dij(Gas g, int64_t n, const double* __restrict__ Ui, cons
     nji[k] = norm_ji > 0.0 ? cji[q * D + k] / norm_ji : (k == 0 ? 1.0 : 0.0);
   }
   bool bd = false;
-  if (EF_VISC_Q && D == 3) {  // the stage kernel's general path: lambda_fast, else exact
-    const Recip ri = recip(a[0]), rj = recip(b[0]);
-    Proj La, Ra, Lb, Rb;
-    const bool ba = project<D>(a, ri, nij, g, La) | project<D>(b, rj, nij, g, Ra);
-    const bool bb = project<D>(b, rj, nji, g, Lb) | project<D>(a, ri, nji, g, Rb);
-    bd = (norm_ij > 0.0 && ba) || (norm_ji > 0.0 && bb);
-    double la = 0.0, lb = 0.0, ea, eb;
-    const bool da = lambda_fast(La, Ra, g, la), db = lambda_fast(Lb, Rb, g, lb);
-    if (!da || !db) {
-      lambda_max2(La, Ra, Lb, Rb, g, ea, eb);
-      if (!da) la = ea;
-      if (!db) lb = eb;
-    }
-    const double v_ij = norm_ij > 0.0 ? la * norm_ij : 0.0;
-    const double v_ji = norm_ji > 0.0 ? lb * norm_ji : 0.0;
-    out[q] = npmax(v_ij, v_ji);
-  } else {
-    out[q] = d_ij_geo<D>(a, b, nij, norm_ij, nji, norm_ji, g, bd, same_state<NV>(a, b));
-  }
+  out[q] = d_ij_geo<D>(a, b, nij, norm_ij, nji, norm_ji, g, bd, same_state<NV>(a, b));
   bad[q] = bd ? 1 : 0;
 }
 

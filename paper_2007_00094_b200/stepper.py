@@ -297,16 +297,34 @@ class Solver:
         _lib.load().ef_phase_times(self._h, s.ctypes.data)
         return {name: float(v) for name, v in zip(STEP_NAMES, s)}
 
-    _FIELDS = {"d": 0, "alpha": 1, "R": 2, "bounds": 3, "l": 4, "eor": 5, "phi": 6, "U": 7, "U_next": 8, "l_prev": 9}
+    _FIELDS = {"d": 0, "alpha": 1, "R": 2, "bounds": 3, "l": 4, "eor": 5, "phi": 6, "U": 7, "U_next": 8,
+               "l_prev": 9, "P_stored": 10}
 
     def fetch(self, which: str, pass_index: int = 0) -> np.ndarray:
-        """Internal arrays (rows = local rows in global CM order; slots in stencil order).
-        "l" / "l_prev": min(l_ij, l_ji) of the last / the previous limiter pass; slots of
-        edges on the exact P = 0 fast path hold the tag -1 in "l_prev" (their factor multiplies a
-        zero P and is not stored by later passes: "l" keeps an earlier value there)."""
+        """Internal arrays of the last stage (rows = local rows in global CM order; slots
+        in stencil order), the reference's rk.* arrays (stepper.py:73-84, 456-491):
+        "d", "alpha", "R", "bounds" (rho_min, rho_max, phi_min), "U_next", "eor", "phi";
+        "P": rk.P after the stage, i.e. the correction fluxes the last limiter pass
+        used: P_0 (1 - min l_0) ... (1 - min l_{q-1}) (stepper.py:468, 485);
+        "l" / "l_prev": min(l_ij, l_ji) of the last / the previous pass.  The last pass
+        runs only on the edges whose previous factor was below 1 (elsewhere its P is
+        +-0 and the factor does not enter the result): "l" holds its value there and an
+        earlier value elsewhere.  Slots of edges on the exact P = 0 fast path
+        (identical-state mode) hold the tag -1 in "l_prev"; their "P" is a zero whose
+        sign is not tracked."""
         n, L, nv = self.n_local, self.pad_width, self.nvar
+        if which == "P":
+            if self.limiter_passes == 0:
+                return np.zeros((n, L, nv))
+            P = self.fetch("P_stored")
+            if self.limiter_passes == 1:
+                return P
+            ml = self.fetch("l_prev")
+            fac = np.where(ml < 0.0, 0.0, 1.0 - ml)
+            return P * fac[..., None]
         shapes = {"d": (n, L), "alpha": (n,), "R": (n, nv), "bounds": (n, 3), "l": (n, L),
-                  "eor": (n,), "phi": (n,), "U": (n, nv), "U_next": (n, nv), "l_prev": (n, L)}
+                  "eor": (n,), "phi": (n,), "U": (n, nv), "U_next": (n, nv), "l_prev": (n, L),
+                  "P_stored": (n, L, nv)}
         out = np.empty(shapes[which])
         _raise(_lib.load().ef_debug_fetch(self._h, self._FIELDS[which], int(pass_index), out.ctypes.data))
         return out

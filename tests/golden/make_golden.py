@@ -76,6 +76,9 @@ def internals_cm(solver: RefSolver):
         a = np.empty((solver.n, rk.width))
         a[cm] = getattr(rk, name)[:n_lo]
         out["int_" + name] = a
+    a = np.empty((solver.n, rk.width, solver.nvar))
+    a[cm] = rk.P[:n_lo]
+    out["int_P"] = a
     a = np.empty(solver.n)
     a[cm] = rk.alpha[:n_lo]
     out["int_alpha"] = a

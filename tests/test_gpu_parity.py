@@ -24,10 +24,10 @@ def test_gpu_matches_reference_golden(name):
     assert np.array_equal(U, g.U_final)
 
 
-def _internals_cm(s):
+def _internals_cm(s, keys=("d", "alpha", "R", "bounds")):
     gids = s.local_gids()
     out = {}
-    for key in ("d", "alpha", "R", "bounds"):
+    for key in keys:
         a = s.fetch(key)
         b = np.empty_like(a)
         b[gids] = a
@@ -47,6 +47,50 @@ def test_gpu_first_stage_internals(name):
     assert np.array_equal(got["alpha"], g.internal("alpha"))
     assert np.array_equal(got["R"], g.internal("R"))
     assert np.array_equal(got["bounds"], g.internal("bounds"))
+
+
+def _transpose_slots(mat):
+    """(row, slot) -> (row, slot) of the transposed entry, rows and slots in the
+    global CM order the reference uses (stepper.py:195-236)."""
+    cm_perm, _ = O.cm_permutation(mat)
+    n = mat.n
+    rows = [[] for _ in range(n)]
+    for o in range(n):
+        rows[cm_perm[o]] = sorted(int(cm_perm[c]) for c in mat.indices[mat.indptr[o]:mat.indptr[o + 1]])
+    pos = [{c: t for t, c in enumerate(r)} for r in rows]
+    return rows, pos
+
+
+@pytest.mark.parametrize("name", [n for n in names() if n.endswith("euler") or "_euler_" in n])
+def test_gpu_first_stage_P_and_limiter_factors(name):
+    """The reference's rk.P after the first stage (the correction fluxes of its last
+    limiter pass) bit for bit, and -- on the edges the last pass limits (previous
+    factor below 1) -- min(l_ij, l_ji) of the reference's last-pass factors rk.l.
+    General path (identical-state shortcuts off: their zero-P tags do not keep
+    the sign of a zero P)."""
+    g = Golden(name)
+    s = Solver(g.matrices, **g.solver_kwargs())
+    s.set_uniform_shortcuts(0)
+    s.set_state(g.U0)
+    s.euler_step(g.params.get("tau"))
+    got = _internals_cm(s, ("P", "l", "l_prev"))
+    if g.params["passes"] == 0:
+        return
+    refP = g.internal("P")
+    bad = np.argwhere(got["P"].view(np.int64) != refP.view(np.int64))
+    assert len(bad) == 0, (len(bad), [(tuple(b), got["P"][tuple(b)], refP[tuple(b)],
+                                       got["l_prev"][tuple(b[:2])]) for b in bad[:6]])
+    if g.params["passes"] != 2:
+        return
+    rows, pos = _transpose_slots(g.matrices)
+    ref_l = g.internal("l")
+    for i, cols in enumerate(rows):
+        for sl, j in enumerate(cols):
+            if j <= i or not (0.0 <= got["l_prev"][i, sl] < 1.0):
+                continue  # the last pass limits only edges whose previous factor was below 1
+            t = pos[j][i]
+            want = min(ref_l[i, sl], ref_l[j, t])
+            assert got["l"][i, sl] == want and got["l"][j, t] == want, (i, sl)
 
 
 def _compare(ps_matrices, U0, bc, steps, c_cfl=0.9, passes=2, newton=2, threads=8):

@@ -24,7 +24,8 @@ def test_oracle_matches_reference_golden(name):
     assert np.array_equal(taus, g.taus)
     assert np.array_equal(U, g.U_final)
     if g.params["mode"] == "euler":
-        for key, field in (("d", "d"), ("alpha", "alpha"), ("R", "R"), ("bounds", "bounds"), ("l", "l")):
+        for key, field in (("d", "d"), ("alpha", "alpha"), ("R", "R"), ("bounds", "bounds"), ("l", "l"),
+                           ("P", "P")):
             ref = g.internal(key)
             if ref is None:
                 continue
