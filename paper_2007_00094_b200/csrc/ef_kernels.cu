@@ -103,16 +103,6 @@ constexpr int TPB = EF_TPB;  // state I/O, halo and pow kernels
 #define EF_MINB_FINAL3 8  // 3D k_final at 8 resident blocks: -11% (from 6)
 #endif
 #define EF_MINB_FINAL(D) ((D) == 3 ? EF_MINB_FINAL3 : EF_MINB)
-// unroll factors of the per-row slot loops (lets ptxas hoist later slots' loads)
-#define EF_STR(x) #x
-#define EF_PRAGMA(x) _Pragma(EF_STR(x))
-#ifndef EF_UNROLL_N
-#define EF_UNROLL_N 1
-#endif
-#define EF_UNROLL_ROW EF_PRAGMA(unroll(D == 2 ? 2 : 1))
-#define EF_UNROLL_LOW EF_PRAGMA(unroll EF_UNROLL_N)
-#define EF_UNROLL_PASS1 EF_PRAGMA(unroll EF_UNROLL_N)
-#define EF_UNROLL_FINAL EF_PRAGMA(unroll EF_UNROLL_N)
 
 static inline unsigned grid_for(int64_t n) { return (unsigned)((n + TPB - 1) / TPB); }
 
@@ -132,13 +122,10 @@ __device__ __forceinline__ void load_node(const double* __restrict__ U, int64_t 
 }
 
 // L2 prefetch of the streamed per-edge index arrays about one wave of resident
-// threads ahead (k_edge_lim: EF_PF_LIM edges; k_edge_visc: EF_PF_DIST, 0 = off):
+// threads ahead (k_edge_lim: EF_PF_LIM edges):
 // those loads miss L2 (read once per launch), and their DRAM latency otherwise
 // heads every edge's dependent load chain.  Measured: limiter passes -2% (2D)
 // / -3% (3D); k_edge_visc +3% in 3D (issue-bound), so off there.
-#ifndef EF_PF_DIST
-#define EF_PF_DIST 0
-#endif
 // Rows whose whole stencil holds the row's own state (bitwise; w.nonuni == 0)
 // take exact closed forms in k_row_visc (alpha = 0), k_low_order (no neighbour
 // loads) and k_edge_lim's first pass (P = 0) -- EF_UNIFORM_ROWS, default on.
@@ -284,14 +271,6 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_EDGE(D), D)) k_edge
     const int i0 = (int)fdiv((uint32_t)p0, m.slab) * 32 + (p0 & 31);
     if (!w.chg[i0] && !w.chg[m.edge_j[e]]) return;
   }
-  if (EF_PF_DIST > 0 && e + EF_PF_DIST < NE) {
-    const int f = e + EF_PF_DIST;
-    pf_l2(m.edges + f);
-    pf_l2(m.edge_j + f);
-    pf_l2(m.edge_pt + f);
-#pragma unroll
-    for (int a = 0; a < 2 * (D + 1); ++a) pf_l2(m.egeo + (size_t)a * NE + f);
-  }
   const int p = m.edges[e];
   const int i = (int)fdiv((uint32_t)p, m.slab) * 32 + (p & 31);
   const int j = m.edge_j[e];
@@ -370,22 +349,11 @@ __device__ __forceinline__ void row_pipe(const int* __restrict__ col, int base, 
 }
 // k_low_order: the prefetch pays once the kernel may keep more registers
 // (2D 5 blocks/SM: -21%; 3D 4 blocks/SM: -23%); k_row_visc: -3% in 2D.
-#ifndef EF_PIPE_LOW
-#define EF_PIPE_LOW 1
-#endif
-#define EF_PIPE(D) (EF_PIPE_LOW != 0)
-#define EF_PIPE_ROW(D) true
 // the row kernels form neighbour fluxes from v, p cached by step0 (measured:
 // 2D k_row_visc -5%, k_low_order -10%, 3D k_low_order -19%; 3D k_row_visc
 // +4%, so it keeps computing them)
-#ifndef EF_VP
-#define EF_VP 1
-#endif
-#ifndef EF_VP_ROW3
-#define EF_VP_ROW3 0
-#endif
-#define EF_VP_ROW(D) (EF_VP && ((D) == 2 || EF_VP_ROW3))
-#define EF_VP_LOW(D) (EF_VP != 0)
+#define EF_VP_ROW(D) ((D) == 2)
+#define EF_VP_LOW(D) true
 template <int D, bool USE>
 __device__ __forceinline__ void node_flux(const double* Ui, const Work& w, int NP, int i, const Gas& g,
                                           double (*f)[D]) {
@@ -454,7 +422,7 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ROW(D), D)) k_row_v
         B[k] = B[k] + t;
       }
     };
-    if constexpr (EF_PIPE_ROW(D)) {
+    {
       constexpr int NQ = EF_VP_ROW(D) ? D + 1 : 0;  // v_j, p_j
       constexpr int F = NV + 1 + D + NQ;     // U_j, eor_j, c, (v_j, p_j)
       __shared__ double buf[2][F][EF_TPB_D(D)];
@@ -480,19 +448,6 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ROW(D), D)) k_row_v
         slot(Uj, cc, buf[st][NV][t], vpj);
       };
       if (!uni) row_pipe(m.col, base, card, dg, issue, body);
-    } else if (!uni) {
-      EF_UNROLL_ROW
-      for (int s = 0; s < card; ++s) {  // indicator: sequential over slots
-        if (s == dg) continue;
-        const int p = base + s * 32;
-        const int j = m.col[p];
-        double Uj[NV], cc[D], vpj[D + 1];
-        load_node<NV>(U, NP, j, Uj);
-#pragma unroll
-        for (int a = 0; a < D; ++a) cc[a] = m.c[(size_t)a * NPL + p];
-        if (EF_VP_ROW(D)) load_node<D + 1>(w.vp, NP, j, vpj);
-        slot(Uj, cc, w.eor[j], vpj);
-      }
     }
     // d row sum over the L padded slots (lower slots were filled by k_edge_visc)
     double* __restrict__ d = w.d;
@@ -648,7 +603,7 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_LOW(D), D)) k_low_o
     rmax = npmax(rmax, ubar);
     pmin = npmin(pmin, phij);
   };
-  if constexpr (EF_PIPE(D)) {
+  {
     // fields per slot: U_j (NV), alpha_j, phi_j, c (D), d
     constexpr int NQ = EF_VP_LOW(D) ? D + 1 : 0;  // v_j, p_j
     constexpr int F = NV + 2 + D + 1 + NQ;
@@ -678,20 +633,6 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_LOW(D), D)) k_low_o
       slot(Uj, cc, buf[st][NV + 2 + D][t], buf[st][NV][t], buf[st][NV + 1][t], vpj);
     };
     if (!uni) row_pipe(m.col, base, card, dg, issue, body);
-  } else if (!uni) {
-    EF_UNROLL_LOW
-    for (int s = 0; s < card; ++s) {
-      if (s == dg) continue;
-      const int p = base + s * 32;
-      const int j = m.col[p];
-      double Uj[NV], cc[D];
-      load_node<NV>(U, NP, j, Uj);
-#pragma unroll
-      for (int a = 0; a < D; ++a) cc[a] = m.c[(size_t)a * NPL + p];
-      double vpj[D + 1];
-      if (EF_VP_LOW(D)) load_node<D + 1>(w.vp, NP, j, vpj);
-      slot(Uj, cc, w.d[p], w.alpha[j], w.phi[j], vpj);
-    }
   }
   const double fac = tau * m.inv_m[i];
 #pragma unroll
@@ -894,7 +835,7 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_PASS(D), D)) k_row_
   // outside the mask has min(l) == 1 exactly, and 1.0 * P == P, so its factor
   // is not loaded
   const unsigned long long mk = use_mask ? w.lmask[i] : 0ull;
-  EF_UNROLL_PASS1
+#pragma unroll 1
   for (int s = 0; s < nslots; ++s) {
     if (s == dg) continue;
     const int p = base + s * 32;
@@ -961,7 +902,7 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_FINAL(D), D)) k_fin
         upd[k] = upd[k] + ml * Pk;
       }
     };
-    EF_UNROLL_FINAL
+#pragma unroll 1
     for (int s = 0; s < nslots; ++s)
       if (s != dg) term(s);
     while (mk) {
