@@ -439,6 +439,25 @@ static int build_from_plan(ef_solver* h, ef::Plan& P, Src& S, const ef_boundary*
       }
     }
   });
+  // EF_CHECKS=1: every real slot (row < n_local, s != diag, s < card) is written
+  // by exactly one edge thread -- at p (upper) or pt (lower) -- so the edge
+  // kernels' plain stores of d, P and min(l) never collide
+  if (const char* ck = std::getenv("EF_CHECKS"); ck && ck[0] == '1') {
+    std::vector<uint8_t> hits(NPL, 0);
+    for (int64_t e = 0; e < NE; ++e) {
+      hits[edges[e]]++;
+      hits[edge_pt[e]]++;
+    }
+    for (int64_t i = 0; i < n_local; ++i)
+      for (int s = 0; s < card[i]; ++s) {
+        const int64_t p = ef::sidx(i, s, L);
+        const bool owned_edge = i < n_owned || col[p] < n_owned;  // edges with an owned end
+        const int want = (s == diag[i] || !owned_edge) ? 0 : 1;
+        if (hits[p] != want)
+          return fail(EF_ERR_ARG, "EF_CHECKS: slot (" + std::to_string(i) + ", " + std::to_string(s) +
+                                      ") is written by " + std::to_string(hits[p]) + " edges");
+      }
+  }
   // boundary data (stepper.py:258-267): owned rows only
   std::vector<int8_t> bc_kind(NP, 0);
   std::vector<double> bc_n((size_t)D * NP, 0.0);

@@ -33,10 +33,30 @@
 // (the *<..., UNI> variants, chosen per step from a sampled count); in 3D the
 // limiter accepts t_R from an fp32 bound of the pow when the margin is clear.
 #include <atomic>
+#include <cstdio>
 
 #include "ef_kernels.cuh"
 
 namespace ef {
+
+// Bounds checks of every computed index (-DEF_CHECKS debug build, used in place
+// of compute-sanitizer, which the GPU pool does not allow): a violated check
+// prints its location and traps.
+#ifdef EF_CHECKS
+#define EF_ASSERT(c)                                                               \
+  do {                                                                             \
+    if (!(c)) {                                                                    \
+      printf("EF_ASSERT failed %s:%d: %s\n", __FILE__, __LINE__, #c);              \
+      __trap();                                                                    \
+    }                                                                              \
+  } while (0)
+#else
+#define EF_ASSERT(c) \
+  do {               \
+  } while (0)
+#endif
+#define EF_IN(x, n) EF_ASSERT((int64_t)(x) >= 0 && (int64_t)(x) < (int64_t)(n))
+
 
 #ifndef EF_TPB
 #define EF_TPB 128
@@ -141,6 +161,7 @@ __device__ __forceinline__ void wl_append(bool need, int e, int* __restrict__ wl
   int base = 0;
   if (lane == leader) base = atomicAdd(n, __popc(bal));
   base = __shfl_sync(act, base, leader);
+  EF_ASSERT(base >= 0);
   if (need) wl[base + __popc(bal & ((1u << lane) - 1u))] = e;
 }
 // warp-aggregated count into one of kSameSlots counters (spread: no hot address)
@@ -275,6 +296,10 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_EDGE(D), D)) k_edge
   const int i = (int)fdiv((uint32_t)p, m.slab) * 32 + (p & 31);
   const int j = m.edge_j[e];
   const int pt = m.edge_pt[e];
+  EF_IN(p, m.NP * m.L);
+  EF_IN(pt, m.NP * m.L);
+  EF_IN(i, m.n_local);
+  EF_IN(j, m.n_local);
   double Ui[NV], Uj[NV], nij[D], nji[D];
   load_node<NV>(U, NP, i, Ui);
   load_node<NV>(U, NP, j, Uj);
@@ -429,6 +454,8 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ROW(D), D)) k_row_v
       const int t = threadIdx.x;
       auto issue = [&](int s, int j, int st) {
         const int p = base + s * 32;
+        EF_IN(j, m.n_local);
+        EF_IN(p, NPL);
 #pragma unroll
         for (int k = 0; k < NV; ++k) cp_async8(&buf[st][k][t], U + k * NP + j);
         cp_async8(&buf[st][NV][t], w.eor + j);
@@ -611,6 +638,8 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_LOW(D), D)) k_low_o
     const int t = threadIdx.x;
     auto issue = [&](int s, int j, int st) {
       const int p = base + s * 32;
+      EF_IN(j, m.n_local);
+      EF_IN(p, NPL);
 #pragma unroll
       for (int k = 0; k < NV; ++k) cp_async8(&buf[st][k][t], U + k * NP + j);
       cp_async8(&buf[st][NV][t], w.alpha + j);
@@ -671,6 +700,10 @@ __device__ __forceinline__ void edge_lim_one(const Layout& m, const Gas& g, cons
   const int i = (int)fdiv((uint32_t)p, m.slab) * 32 + (p & 31);
   const int NP = (int)m.NP;
   const size_t NPL = (size_t)NP * m.L;
+  EF_IN(p, NPL);
+  EF_IN(pt, NPL);
+  EF_IN(i, m.n_local);
+  EF_IN(j, m.n_local);
   double Pi[NV], Pj[NV];
   if (FIRST && UNI && EF_UNIFORM_ROWS) {
     // both rows took k_low_order's uniform shortcut (ust >= 1; owned rows):
@@ -767,6 +800,8 @@ __device__ __forceinline__ void edge_lim_one(const Layout& m, const Gas& g, cons
     wl_append(mlv != 1.0, e, w.wl, w.wl_n);
     if (mlv != 1.0 && m.L <= 64) {  // the slots of this edge in rows i and j
       const int sL = 32 * m.L;
+      EF_IN((p - (i >> 5) * sL) >> 5, m.L);
+      EF_IN((pt - (j >> 5) * sL) >> 5, m.L);
       atomicOr(w.lmask + i, 1ull << ((p - (i >> 5) * sL) >> 5));
       atomicOr(w.lmask + j, 1ull << ((pt - (j >> 5) * sL) >> 5));
     }
@@ -804,8 +839,10 @@ template <int D>
 __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ELIM(D, false), D))
     k_edge_lim_last(Layout m, Gas g, const double* __restrict__ U, Work w, StageParams sp, int q) {
   const int n = *w.wl_n;
+  EF_ASSERT(n <= m.n_edges);
   for (int t = blockIdx.x * EF_TPB_D(D) + threadIdx.x; t < n; t += gridDim.x * EF_TPB_D(D)) {
     const int e = w.wl[t];
+    EF_IN(e, m.n_edges);
     edge_lim_one<D, false, false>(m, g, U, w, sp, q, m.edges[e], m.edge_j[e], m.edge_pt[e], e);
   }
 }
@@ -839,6 +876,7 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_PASS(D), D)) k_row_
   for (int s = 0; s < nslots; ++s) {
     if (s == dg) continue;
     const int p = base + s * 32;
+    EF_IN(p, NPL);
     const double ml = (use_mask && !((mk >> s) & 1ull)) ? 1.0 : w.ml[p];
     if (ml < 0.0) continue;  // kZeroP: the term is ml * (+-0)
 #pragma unroll
@@ -888,6 +926,8 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_FINAL(D), D)) k_fin
     const int nslots = (zrow || lr) ? 0 : card;
     auto term = [&](int s) {
       const int p = base + s * 32;
+      EF_IN(p, NPL);
+      EF_ASSERT(s < card);
       const double mlp = rescale ? w.ml[p] : 0.0;
       const double gp = rescale ? 1.0 - mlp : 1.0;
       // gp == 0: the term is ml2 * (P * 0) = +-0 (P finite), and adding +-0 to a
@@ -972,6 +1012,7 @@ __global__ void k_pack_rows(const double* __restrict__ field, int ncomp, int64_t
   if (q >= count * ncomp) return;
   const int64_t r = q / ncomp;
   const int k = (int)(q - r * ncomp);
+  EF_IN(idx[r], NP);
   buf[r * stride + coff + k] = field[k * NP + idx[r]];
 }
 __global__ void k_unpack_rows(double* __restrict__ field, int ncomp, int64_t NP,
@@ -981,6 +1022,7 @@ __global__ void k_unpack_rows(double* __restrict__ field, int ncomp, int64_t NP,
   if (q >= count * ncomp) return;
   const int64_t r = q / ncomp;
   const int k = (int)(q - r * ncomp);
+  EF_IN(idx[r], NP);
   field[k * NP + idx[r]] = buf[r * stride + coff + k];
 }
 // min of the CFL bounds of every rank of a same-device group, written back to all
