@@ -118,9 +118,13 @@ constexpr int TPB = EF_TPB;  // state I/O, halo and pow kernels
 #ifndef EF_MINB_UPD
 #define EF_MINB_UPD 10
 #endif
-#define EF_MINB_PASS(D) EF_MINB_UPD
+// 3D k_row_upd at 8 resident blocks: -15% (from 10; 160^3 box)
+#ifndef EF_MINB_UPD3
+#define EF_MINB_UPD3 8
+#endif
+#define EF_MINB_PASS(D) ((D) == 3 ? EF_MINB_UPD3 : EF_MINB_UPD)
 #ifndef EF_MINB_FINAL3
-#define EF_MINB_FINAL3 8  // 3D k_final at 8 resident blocks: -11% (from 6)
+#define EF_MINB_FINAL3 12  // 3D k_final: -11% from 6 to 8, -4% from 8 to 10, -3% from 10 to 12 resident blocks
 #endif
 #define EF_MINB_FINAL(D) ((D) == 3 ? EF_MINB_FINAL3 : EF_MINB)
 
