@@ -51,7 +51,7 @@ CONFIG_NAMES = {
     "c1": "C1 2D isentropic vortex 129x129, CFL 0.5",
     "c2": "C2 2D Mach-3 flow past a disc, ~1.24M Q1 nodes, shuffled ids + RCM",
     "c3": "C3 3D Sod box 512x128x128 (jittered)",
-    "c4": "C4 3D Mach-3 flow past a cylinder, extruded O-grid, ~67M nodes (8 GPUs)",
+    "c4": "C4 3D Mach-3 flow past a cylinder, extruded O-grid 255x255 layers, 67M nodes (per-rank z-slabs; 8 GPUs)",
     "c4m": "C4-shaped 3D Mach-3 cylinder, extruded O-grid 100x50 (~2.1M nodes)",
     "c5": "C5 3D periodic Fourier box 320^3 (32.8M nodes)",
     "c3m": "C3-shaped 3D Sod box 256x64x64 (jittered, 1.05M nodes)",
@@ -127,6 +127,8 @@ class ClockSampler:
 # above this size the CPU oracle (and the reference arm) time the same generator's
 # mid-size instance: the port's per-rank arrays need ~3 KB/node of host memory
 CPU_MAX_NODES = 5_000_000
+# configs whose ranks are built from their own rows (no rank holds the global matrix)
+PER_RANK = ("c5w", "c4")
 CPU_SAMPLE_OF = {"c3": "c3m", "c4": "c4m", "c5": "c5m"}
 
 
@@ -241,15 +243,19 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
-    if args.config == "c5w":
-        # per-rank setup: each rank generates only its rows (x-slab of the box in its
-        # lexicographic order) and its ghost layer; NCCL halos for N > 1
+    if args.config in PER_RANK:
+        # per-rank setup: each rank generates only its rows (an x-slab of the box in
+        # its lexicographic order / a z-slab of the extruded O-grid) and its ghost
+        # layer; NCCL halos for N > 1
         from paper_2007_00094_b200 import problems as P
         from paper_2007_00094_b200.distributed import ShardedSolver
 
-        ps = P.periodic_fourier_box_local(weak_side(world), rank, world)
-        solver = ShardedSolver(ps.local, c_cfl=ps.c_cfl, device=local_rank, stream=stream.cuda_stream,
-                               nccl=dist)
+        if args.config == "c5w":
+            ps = P.periodic_fourier_box_local(weak_side(world), rank, world)
+        else:
+            ps = P.mach3_cylinder_local(255, 255, rank, world)
+        solver = ShardedSolver(ps.local, c_cfl=ps.c_cfl, boundary=ps.boundary, device=local_rank,
+                               stream=stream.cuda_stream, nccl=dist)
         n_nodes, dim = ps.local.n_global, ps.local.dim
         mat = None
     else:
@@ -383,7 +389,7 @@ def run_ours(args, rank, world, local_rank):
 
     # e2e through the public API with pinned host buffers
     nv = dim + 2
-    io_rows = ps.local.n_owned if args.config == "c5w" else n_nodes  # a rank's state I/O
+    io_rows = ps.local.n_owned if args.config in PER_RANK else n_nodes  # a rank's state I/O
     host = torch.empty((io_rows, nv), dtype=torch.float64).pin_memory()
     Uh = host.numpy()
     solver.set_state(ps.U0)
@@ -418,7 +424,7 @@ def run_ours(args, rank, world, local_rank):
         "config": {"workload": CONFIG_NAMES[args.config], "nodes": int(n_nodes), "nnz_rank0": int(nnz),
                    "dim": dim, "pad_width": solver.pad_width, "standard_card": card,
                    "c_cfl": ps.c_cfl, "limiter_passes": passes, "newton_steps": solver.newton_steps,
-                   "parallelism": (f"{'x-slab (per-rank setup)' if args.config == 'c5w' else 'cm-range'} "
+                   "parallelism": (f"{'slab (per-rank setup)' if args.config in PER_RANK else 'cm-range'} "
                                    f"partition x{world}, NCCL halo" if world > 1 else "single"),
                    "ghost_fraction_rank0": (solver.n_local - solver.n_owned) / max(solver.n_owned, 1),
                    "halo_bytes_per_stage_rank0": halo_bytes,

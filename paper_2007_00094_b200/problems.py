@@ -787,6 +787,7 @@ class LocalProblem:
     U0: np.ndarray          # (n_owned, nvar): owned rows, global-id order
     c_cfl: float
     steps: int
+    boundary: Optional[BoundaryConditions] = None  # global ids, owned rows only
 
 
 def periodic_fourier_box_local(n: int, rank: int, nranks: int, seed: int = 2007, gas: GasConstants = AIR,
@@ -806,6 +807,101 @@ def periodic_fourier_box(n: int = 320, seed: int = 2007, gas: GasConstants = AIR
     mat = periodic_box_matrices(n)
     U0 = _fourier_state(n, np.arange(mat.n, dtype=np.int64), seed, gas, modes)
     return ProblemSetup("c5-periodic-box", mat, U0, None, c_cfl=0.9, steps=steps, mesh=None)
+
+
+def _q1_cardinality(mesh: Mesh) -> np.ndarray:
+    """Stencil cardinality of every node of a Q1 mesh (the nodes sharing a cell)."""
+    k = mesh.cells.shape[1]
+    rows = np.repeat(mesh.cells, k, axis=1).ravel()
+    cols = np.tile(mesh.cells, (1, k)).ravel()
+    n = len(mesh.points)
+    conn = sp.csr_matrix((np.ones(len(rows), dtype=np.int8), (rows, cols)), shape=(n, n))
+    conn.sum_duplicates()
+    return np.diff(conn.indptr)
+
+
+def mach3_cylinder_local(ny: int = 255, nz: int = 255, rank: int = 0, nranks: int = 1,
+                         gas: GasConstants = AIR, steps: int = 50) -> LocalProblem:
+    """Rank `rank`'s share of mach3_cylinder(ny, nz, shuffle=False) (BASELINE C4),
+    built without the global mesh: node ids are layer-major (extrude order), so
+    a contiguous range of them is a z-slab.  The rank assembles only the cell
+    layers around its slab (its owned and ghost rows need every cell they touch:
+    node layers la-2 .. lb+2 for owned layers la .. lb), with the global node
+    ids and cell order restricted, so every row value, lumped mass and boundary
+    normal of its owned rows (and the row values of its ghost rows) equals the
+    global generator's bit for bit (tests/test_partition_local.py).  Host memory
+    ~1/nranks of the global assembly: the 67M-node C4 at 8 GPUs is 8.4M rows a
+    rank.  Boundary lists are in global ids, owned rows only."""
+    m2 = disc_channel_mesh(ny)
+    n2 = len(m2.points)
+    zs = np.linspace(0.0, 1.0, nz + 1)  # extrude's z values
+    N = (nz + 1) * n2
+    ranges = even_ranges(N, nranks)
+    a, b = int(ranges[rank]), int(ranges[rank + 1])
+    la, lb = a // n2, (b - 1) // n2
+    c0, c1 = max(la - 2, 0), min(lb + 1, nz - 1)  # cell layers
+    n0, n1 = c0, c1 + 1                           # node layers of the sub-mesh
+    pts = np.empty(((n1 - n0 + 1) * n2, 3))
+    pts[:, :2] = np.tile(m2.points, (n1 - n0 + 1, 1))
+    pts[:, 2] = np.repeat(zs[n0:n1 + 1], n2)
+    q = m2.cells
+    kk = np.arange(c1 - c0 + 1, dtype=np.int64)[:, None, None] * n2
+    cells = np.concatenate([q[None] + kk, q[None] + kk + n2], axis=2).reshape(-1, 8)
+    sub = Mesh(points=pts, cells=cells.astype(np.int64), dim=3)
+    off = n0 * n2                                 # sub-mesh id + off = global id
+    nc = len(sub.cells)  # large slabs: row ranges of ~0.5M cells (bit-identical, assemble_q1_rows)
+    mat = assemble_q1(sub) if nc <= (1 << 21) else assemble_q1_rows(sub, slabs=-(-nc // (1 << 19)))
+    ff = _conserved(np.array([1.4]), np.array([[3.0, 0.0, 0.0]]), np.array([1.0]), gas)[0]
+    bc = _slip_inflow_bc(sub, lambda X: X[..., 0] < 1e-9, lambda X: X[..., 0] > 4.0 - 1e-9, ff)
+    ip, ix = mat.indptr, mat.indices
+
+    def entries(rows):  # CSR positions of the given sub-mesh rows, row by row
+        cnt = ip[rows + 1] - ip[rows]
+        first = np.repeat(ip[rows] - np.concatenate([[0], np.cumsum(cnt)[:-1]]), cnt)
+        return first + np.arange(int(cnt.sum()), dtype=np.int64), cnt
+
+    own = np.arange(a - off, b - off, dtype=np.int64)
+    sel, own_cnt = entries(own)
+    cols_own = ix[sel] + off
+    ghosts = np.unique(cols_own[(cols_own < a) | (cols_own >= b)])
+    gl = ghosts - off
+    gsel, g_cnt = entries(gl)
+    gcols = ix[gsel] + off
+    keep = ((gcols >= a) & (gcols < b)) | np.isin(gcols, ghosts)
+    g_rows = np.repeat(np.arange(len(gl)), g_cnt)
+    g_card = np.bincount(g_rows[keep], minlength=len(gl))
+    rowptr = np.concatenate([[0], np.cumsum(np.concatenate([own_cnt, g_card]))]).astype(np.int64)
+    loc = np.concatenate([own, gl])
+    # global pad width and most frequent cardinality (stepper.py:128-131) of the
+    # extruded pattern: a node's 3D card is its 2D card times 3 (2 at z = 0, 1)
+    card2 = _q1_cardinality(m2)
+    hist = np.zeros(3 * int(card2.max()) + 1, dtype=np.int64)
+    np.add.at(hist, 3 * card2, max(nz - 1, 0))
+    np.add.at(hist, 2 * card2, 2)
+    lm = LocalMatrices(n_global=N, dim=3, pad_width=int(np.flatnonzero(hist).max()),
+                       standard_card=int(np.argmax(hist)), rank=rank, nranks=nranks, ranges=ranges,
+                       ghost_gid=ghosts.astype(np.int64), rowptr=rowptr,
+                       col_gid=np.concatenate([cols_own, gcols[keep]]).astype(np.int64),
+                       m=np.concatenate([mat.m[sel], mat.m[gsel][keep]]),
+                       c=np.concatenate([mat.c[sel], mat.c[gsel][keep]]),
+                       m_lumped=mat.m_lumped[loc], inv_m=mat.inv_m[loc],
+                       full_card=(ip[loc + 1] - ip[loc]).astype(np.int32))
+
+    def owned(ids):
+        g = np.asarray(ids, dtype=np.int64) + off
+        return (g >= a) & (g < b), g
+
+    inflow = slip = normals = None
+    if bc.inflow_nodes is not None:
+        k_in, g = owned(bc.inflow_nodes)
+        inflow = g[k_in] if k_in.any() else None
+    if bc.slip_nodes is not None:
+        k_s, g = owned(bc.slip_nodes)
+        if k_s.any():
+            slip, normals = g[k_s], bc.slip_normals[k_s]
+    bcl = BoundaryConditions(inflow_nodes=inflow, farfield=ff, slip_nodes=slip, slip_normals=normals)
+    return LocalProblem("c4-mach3-cylinder", lm, np.tile(ff, (b - a, 1)), c_cfl=0.9, steps=steps,
+                        boundary=bcl)
 
 
 def random_state(rng, n: int, dim: int = 2) -> np.ndarray:
