@@ -380,11 +380,8 @@ __device__ __forceinline__ void row_pipe(const int* __restrict__ col, int base, 
 // (2D 5 blocks/SM: -21%; 3D 4 blocks/SM: -23%); k_row_visc: -3% in 2D.
 // the row kernels form neighbour fluxes from v, p cached by step0 (measured:
 // 2D k_row_visc -5%, k_low_order -10%, 3D k_low_order -19%; 3D k_row_visc
-// +4%, so it keeps computing them)
-#ifndef EF_VP_ROW3
-#define EF_VP_ROW3 0
-#endif
-#define EF_VP_ROW(D) ((D) == 2 || EF_VP_ROW3)
+// neutral on the 160^3 box, -18% on the Sod box)
+#define EF_VP_ROW(D) true
 #define EF_VP_LOW(D) true
 template <int D, bool USE>
 __device__ __forceinline__ void node_flux(const double* Ui, const Work& w, int NP, int i, const Gas& g,
