@@ -621,9 +621,6 @@ static int build_from_plan(ef_solver* h, ef::Plan& P, Src& S, const ef_boundary*
   EF_CUDA(cudaMemset(w.pnz, 1, NP));
   EF_TRY(h->alloc(&w.wl, std::max<int64_t>(h->lay.n_edges, 1)));
   EF_TRY(h->alloc(&w.wl_n, 1));
-  EF_TRY(h->alloc(&w.nl, std::max<int64_t>(h->lay.n_edges, 1)));
-  EF_TRY(h->alloc(&w.nl_n, 1));
-  EF_CUDA(cudaMemset(w.nl_n, 0, sizeof(int)));
   EF_TRY(h->alloc(&w.lmask, NP));
   EF_CUDA(cudaMemset(w.lmask, 0, sizeof(unsigned long long) * NP));
   EF_CUDA(cudaMemset(w.wl_n, 0, sizeof(int)));

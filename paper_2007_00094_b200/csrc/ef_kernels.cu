@@ -696,10 +696,6 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_LOW(D), D)) k_low_o
 // kernels then only stream their own slots.  Every operation is the
 // reference's, in its order; each side uses its own m_ij / m_ji, alpha sum and
 // factor, so nothing assumes symmetry that the inputs might not have.
-// 3D first limiter pass: Newton iterations deferred to k_edge_newton (EF_DEFER_NEWTON)
-#ifndef EF_DEFER_NEWTON
-#define EF_DEFER_NEWTON 1
-#endif
 template <int D>
 __device__ __forceinline__ void edge_lim_store(const Layout& m, const Work& w, const StageParams& sp, int q, int p,
                                                int j, int pt, int e, int i, double li, double lj);
@@ -799,24 +795,10 @@ __device__ __forceinline__ void edge_lim_one(const Layout& m, const Gas& g, cons
     }
   }
   double Un[NV];
-  double li, lj;
-  if constexpr (D == 3 && FIRST && !UNI && EF_DEFER_NEWTON) {
-    // the limiters as far as the fast accept settles them; an edge with a side
-    // that needs the Newton iteration goes to the list k_edge_newton finishes
-    // (from the stored P), which keeps the iteration's registers out of this
-    // memory-bound kernel
-    load_node<NV>(w.Unext, NP, i, Un);
-    const bool di = limiter_try<D>(Un, Pi, w.bounds[i], w.bounds[NP + i], w.bounds[2 * NP + i], sp.newton, g, li);
-    load_node<NV>(w.Unext, NP, j, Un);
-    const bool dj = limiter_try<D>(Un, Pj, w.bounds[j], w.bounds[NP + j], w.bounds[2 * NP + j], sp.newton, g, lj);
-    wl_append(!(di && dj), e, w.nl, w.nl_n);
-    if (!(di && dj)) return;
-  } else {
-    load_node<NV>(w.Unext, NP, i, Un);
-    li = limiter<D>(Un, Pi, w.bounds[i], w.bounds[NP + i], w.bounds[2 * NP + i], sp.newton, g);
-    load_node<NV>(w.Unext, NP, j, Un);
-    lj = limiter<D>(Un, Pj, w.bounds[j], w.bounds[NP + j], w.bounds[2 * NP + j], sp.newton, g);
-  }
+  load_node<NV>(w.Unext, NP, i, Un);
+  const double li = limiter<D>(Un, Pi, w.bounds[i], w.bounds[NP + i], w.bounds[2 * NP + i], sp.newton, g);
+  load_node<NV>(w.Unext, NP, j, Un);
+  const double lj = limiter<D>(Un, Pj, w.bounds[j], w.bounds[NP + j], w.bounds[2 * NP + j], sp.newton, g);
   edge_lim_store<D>(m, w, sp, q, p, j, pt, e, i, li, lj);
 }
 
@@ -879,35 +861,6 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ELIM(D, false), D))
     const int e = w.wl[t];
     EF_IN(e, m.n_edges);
     edge_lim_one<D, false, false>(m, g, U, w, sp, q, m.edges[e], m.edge_j[e], m.edge_pt[e], e);
-  }
-}
-
-// The limiters of the first pass's deferred edges (3D): both sides from scratch
-// with the stored P (the fast-accepted side gives the same t_R again), then the
-// same stores as the first pass.  Grid-stride over the device-side count.
-template <int D>
-__global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ELIM(D, false), D))
-    k_edge_newton(Layout m, Gas g, Work w, StageParams sp) {
-  constexpr int NV = D + 2;
-  const int n = *w.nl_n;
-  EF_ASSERT(n <= m.n_edges);
-  const int NP = (int)m.NP;
-  const size_t NPL = (size_t)NP * m.L;
-  for (int t = blockIdx.x * EF_TPB_D(D) + threadIdx.x; t < n; t += gridDim.x * EF_TPB_D(D)) {
-    const int e = w.nl[t];
-    EF_IN(e, m.n_edges);
-    const int p = m.edges[e], j = m.edge_j[e], pt = m.edge_pt[e];
-    const int i = (int)fdiv((uint32_t)p, m.slab) * 32 + (p & 31);
-    double P[NV], Un[NV];
-#pragma unroll
-    for (int k = 0; k < NV; ++k) P[k] = w.P[(size_t)k * NPL + p];
-    load_node<NV>(w.Unext, NP, i, Un);
-    const double li = limiter<D>(Un, P, w.bounds[i], w.bounds[NP + i], w.bounds[2 * NP + i], sp.newton, g);
-#pragma unroll
-    for (int k = 0; k < NV; ++k) P[k] = w.P[(size_t)k * NPL + pt];
-    load_node<NV>(w.Unext, NP, j, Un);
-    const double lj = limiter<D>(Un, P, w.bounds[j], w.bounds[NP + j], w.bounds[2 * NP + j], sp.newton, g);
-    edge_lim_store<D>(m, w, sp, 0, p, j, pt, e, i, li, lj);
   }
 }
 
@@ -1174,14 +1127,7 @@ static void edge_lim_launch(const Layout& m, const Gas& g, const double* U, Work
     k_edge_lim_last<D><<<grid < EF_WL_GRID ? grid : EF_WL_GRID, tb, 0, st>>>(m, g, U, w, sp, q);
   else if (q > 0) k_edge_lim<D, false, false><<<grid, tb, 0, st>>>(m, g, U, w, sp, q);
   else if (sp.uni) k_edge_lim<D, true, true><<<grid, tb, 0, st>>>(m, g, U, w, sp, q);
-  else {
-    if (D == 3 && EF_DEFER_NEWTON) cudaMemsetAsync(w.nl_n, 0, sizeof(int), st);
-    k_edge_lim<D, true, false><<<grid, tb, 0, st>>>(m, g, U, w, sp, q);
-    if (D == 3 && EF_DEFER_NEWTON) {
-      EF_COUNT();
-      k_edge_newton<D><<<grid < EF_WL_GRID ? grid : EF_WL_GRID, tb, 0, st>>>(m, g, w, sp);
-    }
-  }
+  else k_edge_lim<D, true, false><<<grid, tb, 0, st>>>(m, g, U, w, sp, q);
 }
 
 void launch_edge_lim(int dim, const Layout& m, const Gas& g, const double* U, Work w,

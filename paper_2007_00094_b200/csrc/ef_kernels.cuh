@@ -88,8 +88,6 @@ struct Work {
                      // 0: every edge of the row took the first pass's P = 0 shortcut
   int* wl;           // [n_edges] worklist of the last limiter pass: the edges whose min(l)
   int* wl_n;         // came out below 1 in the pass before it (count in wl_n)
-  int* nl;           // [n_edges] 3D first limiter pass: edges whose limiters need the Newton
-  int* nl_n;         // iteration (the fast accept did not settle them), finished by k_edge_newton
   unsigned long long* lmask;  // [NP] bit s: slot s of the row belongs to a worklist edge (its
                               // k_final rescaled term can be nonzero); cleared by k_final
   uint8_t* ust;      // [NP] k_low_order's row status for the first limiter pass: 0 general,
