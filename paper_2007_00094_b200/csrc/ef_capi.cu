@@ -1026,6 +1026,7 @@ static int finish(Driver& d, int out_buf, double* tau_used) {
     first = std::min(first, h->rb->err_first);
     bad = std::min(bad, h->rb->bad);
   }
+  bad &= (1ull << 56) - 1;  // drop the stage tag
   if (err) {  // the state rolls back: nothing computed for the failed stages may be reused --
               // step0 of the current state again (it also clears the memo marks)
     for (ef_solver* h : d.hs) {

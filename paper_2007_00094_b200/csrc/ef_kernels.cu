@@ -989,7 +989,9 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_FINAL(D), D)) k_fin
   // _finish_step admissibility, stepper.py:612-621
   if (!((Un[0] > 0.0) && (internal_energy<D>(Un) > 0.0))) {
     raise_err(w, ERR_BAD_STATE, sp.stage, PH_STATE);
-    atomicMin(w.bad_gid, (unsigned long long)m.gid[i]);
+    // the earliest failing stage first (the reference stops there), then the
+    // smallest CM id of that stage
+    atomicMin(w.bad_gid, ((unsigned long long)sp.stage << 56) | (unsigned long long)m.gid[i]);
   }
   double Uo[NV];
   if (sp.rk_a >= 0.0) {  // ssp_rk3_step incremental combination, stepper.py:632,635

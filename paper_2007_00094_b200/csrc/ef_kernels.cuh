@@ -100,7 +100,7 @@ struct Work {
                      // a synchronous step / set_state): errors latch across async steps
   int* err_first;    // min over the errors of (stage * 8 + phase): the one the reference
                      // would have raised first (stepper.py:508-622 order of the checks)
-  unsigned long long* bad_gid;       // min global CM id of an inadmissible row
+  unsigned long long* bad_gid;       // min of (stage << 56 | global CM id) of an inadmissible row
   unsigned long long* n_same;        // [kSameSlots] spread counters since the last reset:
                                      // identical-state edges (shortcuts off) or uniform rows (on)
 };

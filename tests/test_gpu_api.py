@@ -303,3 +303,24 @@ def test_advance_with_changing_tau_max_replays_one_graph():
         out.append((t, s.get_state()))
     assert out[0][0] == out[1][0]
     assert np.array_equal(out[0][1], out[1][1])
+
+
+def test_inadmissible_rk_step_reports_the_first_failing_stage_like_the_reference():
+    """A step far beyond the CFL bound: the reference raises after the first stage
+    whose result is inadmissible (stepper.py:612-622), naming its first bad
+    node; the later stages (computed anyway on the device) must not change the
+    reported error or node."""
+    ps = P.make_config("c2", scale="small")
+    s = Solver(ps.matrices, c_cfl=ps.c_cfl, boundary=ps.boundary)
+    o = O.OracleSolver(ps.matrices, c_cfl=ps.c_cfl, boundary=ps.boundary)
+    s.set_state(ps.U0)
+    o.set_state(ps.U0)
+    for _ in range(3):
+        assert s.ssp_rk3_step() == o.ssp_rk3_step()
+    for tau in (5.0, 0.5):
+        with pytest.raises(ValueError) as eg:
+            s.ssp_rk3_step(tau=tau)
+        with pytest.raises(ValueError) as eo:
+            o.ssp_rk3_step(tau)
+        assert str(eg.value) == str(eo.value), tau
+        o.set_state(s.get_state())
