@@ -129,11 +129,17 @@ int ef_counters(ef_solver* h, int64_t* out3);
  * [4]=standard card (most frequent), [5]=dim */
 int ef_info(ef_solver* h, int64_t* out6);
 
-/* Per-phase parity hook (the reference exposes these as solver.ranks[r].*):
- * which = 0 d (n_local*L), 1 alpha (n_local), 2 R (n_local*nvar), 3 bounds
- * (n_local*3), 4 l of pass p (n_local*L; p = which_pass), 5 eor, 6 phi,
- * 7 U (n_local*nvar), 8 U_next.  Rows in local order (owned rows = global CM
- * ids rank_start.., then ghosts ascending), slots in stencil order. */
+/* Per-phase parity hook (the reference exposes these as solver.ranks[r].*,
+ * stepper.py:73-84), the last stage's arrays: which = 0 d (n_local*L),
+ * 1 alpha (n_local), 2 R (n_local*nvar), 3 bounds (n_local*3), 4 min(l_ij,
+ * l_ji) of the last limiter pass (n_local*L; written on the edges that pass
+ * limits: those whose previous factor was below 1), 5 eor, 6 phi,
+ * 7 U (n_local*nvar), 8 U_next, 9 min(l) of the pass before the last (-1 tags
+ * a slot whose P is zero from then on), 10 P as stored by the first limiter
+ * pass (n_local*L*nvar; the reference's rk.P is P_0 (1 - min l_0) ... for
+ * two or more passes: Solver.fetch("P") forms it).  which_pass is reserved.
+ * Rows in local order (owned rows = global CM ids rank_start.., then ghosts
+ * ascending), slots in stencil order. */
 int ef_debug_fetch(ef_solver* h, int32_t which, int32_t which_pass, double* out);
 /* local row -> global CM id, (n_local) */
 int ef_local_gids(ef_solver* h, int64_t* out);
