@@ -1,13 +1,17 @@
 """Benchmark: fp64 Q1 node-updates per second per SSP-RK3 stage (BASELINE.json).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5|c5w|c1|c2|c3|c3m|c4m|c5m] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5w|c5|c1|c2|c3|c3m|c4|c4m|c5m] [--impl ours|reference]
 
-Workload (config.workload): at N = 1 the largest single-GPU configuration of
-BASELINE.json, configs[4] at its 1-GPU point: the 3D periodic Q1 hex box 320^3
-(32.8M nodes, 885M stencil entries, 27-point stencil), seeded smooth random
-state from 8 Fourier modes, synthetic (generated mesh; no dataset exists).
-At N > 1 the default is the same config's weak-scaling series (`c5w`,
-n = round(320 N^(1/3)) per side: 403^3 / 508^3 / 640^3 at N = 2 / 4 / 8).
+Workload (config.workload): BASELINE.json configs[4], the largest
+single-GPU configuration, as its weak-scaling series `c5w`: the 3D periodic Q1
+hex box n^3 with n = round(320 N^(1/3)) (320^3 = 32.8M nodes and 885M stencil
+entries at N = 1; 403^3 / 508^3 / 640^3 at N = 2 / 4 / 8), seeded smooth
+random state from 8 Fourier modes, synthetic (generated mesh; no dataset
+exists).  Every N runs the same code path: per-rank setup (each rank builds
+its x-slab of the box in the box's lexicographic node order, ShardedSolver).
+`--config c5` runs the same 320^3 problem through the global-setup Solver in
+the reference's Cuthill-McKee order (bit-identical to the reference's own
+output at 64^3 x 50 steps, tests/test_gpu_stated.py).
 A step is one SSP-RK3 step (3 forward-Euler stages) over the whole mesh.
 
 value     device-resident throughput: N_nodes * 3 * K / (CUDA-event time of K
@@ -466,7 +470,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default=None, choices=sorted(CONFIG_NAMES),
-                    help="default: c5 (320^3) at N = 1, c5w (weak scaling) at N > 1")
+                    help="default: c5w (C5 weak scaling, 320^3 per GPU)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
@@ -477,7 +481,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.config is None:
-        args.config = "c5" if world == 1 else "c5w"
+        args.config = "c5w"
     if args.impl == "reference":
         run_reference(args, rank, world)
         return

@@ -53,3 +53,22 @@ def test_gpu_c2_full_200_steps_equals_oracle():
     for k in range(200):
         assert s.ssp_rk3_step() == o.ssp_rk3_step(), k
     assert np.array_equal(s.get_state(), o.get_state())
+
+
+def test_gpu_benchmark_order_equals_oracle_at_stated_steps():
+    """The benchmark's code path (bench.py c5w: per-rank setup, the box's
+    lexicographic node order) on C5 at 64^3 over the stated 50 steps: tau of
+    every step and the final state equal the oracle run in the same node order
+    (the oracle equals the reference in its Cuthill-McKee order, above)."""
+    from paper_2007_00094_b200.distributed import ShardedSolver
+
+    n, steps = 64, 50
+    lp = P.periodic_fourier_box_local(n, 0, 1)
+    s = ShardedSolver([lp.local])
+    s.set_state(lp.U0)
+    ps = P.periodic_fourier_box(n)
+    o = O.OracleSolver(ps.matrices, cm_perm=np.arange(ps.matrices.n), threads=os.cpu_count() or 1)
+    o.set_state(ps.U0)
+    for k in range(steps):
+        assert s.ssp_rk3_step() == o.ssp_rk3_step(), k
+    assert np.array_equal(s.get_state(), o.get_state())
