@@ -157,6 +157,12 @@ int ef_eval_dij(const ef_params* prm, int32_t dim, int64_t n, const double* Ui, 
                 const double* cij, const double* cji, double* out, int32_t* bad);
 int ef_eval_limiter(const ef_params* prm, int32_t dim, int64_t n, const double* U, const double* P,
                     const double* bounds, double* out);
+/* The straight-line division / reciprocal / square root of the d_ij kernel
+ * (csrc/ef_math.cuh: rcp_sl, div_sl, sqrt_sl, qdiv_sl) against the IEEE
+ * operations they restate (the reference's numpy /, sqrt: riemann.py:56-109):
+ * mismatches[0..3] = operands (a[q], b[q]) inside the safe exponent range with
+ * 1/b, a/b, sqrt|a| or the shared-reciprocal a/b differing in any bit. */
+int ef_eval_arith(int64_t n, const double* a, const double* b, uint64_t* mismatches);
 
 void ef_pow_host(const double* x, double y, double* out, int64_t n);
 int ef_pow_device(const double* x, double y, double* out, int64_t n);

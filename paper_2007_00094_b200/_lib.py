@@ -55,6 +55,7 @@ SIGNATURES = {
     "ef_destroy": (_i32, [_p]),
     "ef_eval_dij": (_i32, [ctypes.POINTER(EfParams), _i32, _i64, _p, _p, _p, _p, _p, _p]),
     "ef_eval_limiter": (_i32, [ctypes.POINTER(EfParams), _i32, _i64, _p, _p, _p, _p]),
+    "ef_eval_arith": (_i32, [_i64, _p, _p, _p]),
     "ef_set_state": (_i32, [_p, _p]),
     "ef_get_state": (_i32, [_p, _p]),
     "ef_euler_step": (_i32, [_p, _i32, _d, _d, ctypes.POINTER(_d)]),

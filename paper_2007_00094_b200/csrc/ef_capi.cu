@@ -232,6 +232,8 @@ static Gas make_gas(const ef_params* p) {
   g.sqrt2 = std::sqrt(2.0);
   const char* fa = std::getenv("EF_FAST_ACCEPT");  // results are identical either way
   g.fast_accept = (fa && fa[0] == '0') ? 0 : 1;
+  const char* sl = std::getenv("EF_SL");  // straight-line d_ij path (ef_math.cuh); results are identical either way
+  g.sl = (sl && sl[0] == '0') ? 0 : 1;
   return g;
 }
 
@@ -1497,6 +1499,24 @@ int ef_pow_bound_device(const double* x, double y, double* out, int64_t n) {
   ef::launch_pow_ub(dx, y, dy, n, 0);
   EF_CUDA(cudaGetLastError());
   EF_CUDA(cudaMemcpy(out, dy, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  return EF_OK;
+}
+
+int ef_eval_arith(int64_t n, const double* a, const double* b, uint64_t* mismatches) {
+  if (n < 0 || !mismatches) return fail(EF_ERR_ARG, "bad arguments");
+  for (int k = 0; k < 4; ++k) mismatches[k] = 0;
+  if (n == 0) return EF_OK;
+  if (!a || !b) return fail(EF_ERR_ARG, "null argument");
+  DevBufs bufs;
+  double *da, *db;
+  unsigned long long* dm;
+  EF_TRY(bufs.get(&da, (size_t)n, a));
+  EF_TRY(bufs.get(&db, (size_t)n, b));
+  EF_TRY(bufs.get(&dm, (size_t)4));
+  EF_CUDA(cudaMemset(dm, 0, 4 * sizeof(unsigned long long)));
+  ef::launch_eval_arith(n, da, db, dm, 0);
+  EF_CUDA(cudaGetLastError());
+  EF_CUDA(cudaMemcpy(mismatches, dm, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
   return EF_OK;
 }
 

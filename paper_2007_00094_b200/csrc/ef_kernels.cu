@@ -275,6 +275,17 @@ __global__ void k_nodal(Layout m, Gas g, const double* __restrict__ U, Work w, i
 // slot after the diagonal; stepper.py:211, 415).  The edge list holds SELL
 // positions in ascending order, so a warp reads 32 consecutive positions of
 // one slot row (coalesced) and the row / slot are recovered from the position.
+template <int D>
+__device__ __forceinline__ void load_edge(const Layout& m, const double* __restrict__ U, int NP, int NE, int e, int i,
+                                          int j, double* Ui, double* Uj, double* nij, double* nji) {
+  load_node<D + 2>(U, NP, i, Ui);
+  load_node<D + 2>(U, NP, j, Uj);
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    nij[a] = m.egeo[(size_t)a * NE + e];
+    nji[a] = m.egeo[(size_t)(D + 1 + a) * NE + e];
+  }
+}
 template <int D, bool UNI>
 __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_EDGE(D), D)) k_edge_visc(Layout m, Gas g, const double* __restrict__ U,
                                                    Work w, int flags) {  // 1: reset the CFL bound, 2: count,
@@ -304,22 +315,29 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_EDGE(D), D)) k_edge
   EF_IN(pt, m.NP * m.L);
   EF_IN(i, m.n_local);
   EF_IN(j, m.n_local);
-  double Ui[NV], Uj[NV], nij[D], nji[D];
-  load_node<NV>(U, NP, i, Ui);
-  load_node<NV>(U, NP, j, Uj);
-#pragma unroll
-  for (int a = 0; a < D; ++a) {
-    nij[a] = m.egeo[(size_t)a * NE + e];
-    nji[a] = m.egeo[(size_t)(D + 1 + a) * NE + e];
+  bool bad = false, same = false, done = false;
+  double dv;
+  {
+    double Ui[NV], Uj[NV], nij[D], nji[D];
+    load_edge<D>(m, U, NP, NE, e, i, j, Ui, Uj, nij, nji);
+    const double norm_ij = m.egeo[(size_t)D * NE + e], norm_ji = m.egeo[(size_t)(2 * D + 1) * NE + e];
+    if (UNI || ((flags & 2) && (blockIdx.x & 7) == 0)) same = same_state<NV>(Ui, Uj);
+    if (UNI && !same) {
+      w.nonuni[i] = 1;
+      w.nonuni[j] = 1;
+    }
+    // the straight-line evaluation (ef_math.cuh); identical states keep their closed form
+    if (!(UNI && same)) done = d_ij_sl<D>(Ui, Uj, nij, norm_ij, nji, norm_ji, g, dv);
   }
-  const double norm_ij = m.egeo[(size_t)D * NE + e], norm_ji = m.egeo[(size_t)(2 * D + 1) * NE + e];
-  bool bad = false;
-  const bool same = same_state<NV>(Ui, Uj);
-  if (UNI && !same) {
-    w.nonuni[i] = 1;
-    w.nonuni[j] = 1;
+  if (!done) {
+    // zero or extreme operands, an inadmissible state, vacuum, identical states: the
+    // general code on operands loaded again (nothing of the rare path stays live above)
+    asm volatile("" ::: "memory");
+    double Ui[NV], Uj[NV], nij[D], nji[D];
+    load_edge<D>(m, U, NP, NE, e, i, j, Ui, Uj, nij, nji);
+    const double norm_ij = m.egeo[(size_t)D * NE + e], norm_ji = m.egeo[(size_t)(2 * D + 1) * NE + e];
+    dv = d_ij_geo<D>(Ui, Uj, nij, norm_ij, nji, norm_ji, g, bad, UNI && same);
   }
-  const double dv = d_ij_geo<D>(Ui, Uj, nij, norm_ij, nji, norm_ji, g, bad, UNI && same);
   // d is symmetric by construction (riemann.py:139-142): the value is also
   // the lower-triangle entry of row j, written straight to its slot (the
   // reference's mirror, stepper.py:427-434, without a gather)
@@ -1207,7 +1225,11 @@ __global__ void k_eval_dij(Gas g, int64_t n, const double* __restrict__ Ui, cons
     nji[k] = norm_ji > 0.0 ? cji[q * D + k] / norm_ji : (k == 0 ? 1.0 : 0.0);
   }
   bool bd = false;
-  out[q] = d_ij_geo<D>(a, b, nij, norm_ij, nji, norm_ji, g, bd, same_state<NV>(a, b));
+  double dv;
+  // as k_edge_visc<D, true>: identical states by their closed form, then the straight-line path, else the general code
+  const bool same = same_state<NV>(a, b);
+  if (same || !d_ij_sl<D>(a, b, nij, norm_ij, nji, norm_ji, g, dv)) dv = d_ij_geo<D>(a, b, nij, norm_ij, nji, norm_ji, g, bd, same);
+  out[q] = dv;
   bad[q] = bd ? 1 : 0;
 }
 
@@ -1224,6 +1246,25 @@ __global__ void k_eval_limiter(Gas g, int64_t n, const double* __restrict__ U, c
     pp[k] = P[q * NV + k];
   }
   out[q] = limiter<D>(u, pp, bounds[3 * q], bounds[3 * q + 1], bounds[3 * q + 2], newton, g);
+}
+
+// the straight-line primitives against the compiler's own 1/b, a/b, sqrt (test hook):
+// mism[0..2] count operands in the safe range whose results differ
+__global__ void k_eval_arith(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
+                             unsigned long long* __restrict__ mism) {
+  const int64_t q = blockIdx.x * (int64_t)TPB + threadIdx.x;
+  if (q >= n) return;
+  const double x = a[q], y = b[q];
+  if (!(exp_within<450>(x) && exp_within<450>(y))) return;
+  if (__double_as_longlong(rcp_sl(y)) != __double_as_longlong(1.0 / y)) atomicAdd(mism + 0, 1ULL);
+  if (__double_as_longlong(div_sl(x, y)) != __double_as_longlong(x / y)) atomicAdd(mism + 1, 1ULL);
+  const double ax = fabs(x);
+  if (__double_as_longlong(sqrt_sl(ax)) != __double_as_longlong(sqrt(ax))) atomicAdd(mism + 2, 1ULL);
+  const double yr = 1.0 / y;
+  if (__double_as_longlong(qdiv_sl(x, y, yr)) != __double_as_longlong(x / y)) atomicAdd(mism + 3, 1ULL);
+}
+void launch_eval_arith(int64_t n, const double* a, const double* b, unsigned long long* mism, cudaStream_t st) {
+  if (n > 0) k_eval_arith<<<grid_for(n), TPB, 0, st>>>(n, a, b, mism);
 }
 
 void launch_eval_dij(int dim, const Gas& g, int64_t n, const double* Ui, const double* Uj, const double* cij,

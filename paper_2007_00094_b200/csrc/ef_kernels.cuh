@@ -178,6 +178,7 @@ void launch_unpack_rows(double* field, int ncomp, int64_t NP, const int32_t* idx
                         const double* buf, int stride, int coff, cudaStream_t st);
 void launch_group_min(unsigned long long* const* bits_dev, int n, cudaStream_t st);
 // function-level checks: d_ij and the limiter on independent AoS batches
+void launch_eval_arith(int64_t n, const double* a, const double* b, unsigned long long* mism, cudaStream_t st);
 void launch_eval_dij(int dim, const Gas& g, int64_t n, const double* Ui, const double* Uj, const double* cij,
                      const double* cji, double* out, int* bad, cudaStream_t st);
 void launch_eval_limiter(int dim, const Gas& g, int64_t n, const double* U, const double* P,

@@ -36,7 +36,7 @@ from .physics import AIR, AdmissibilityError, GasConstants, is_admissible
 from .problems import BoundaryConditions
 
 __all__ = ["Solver", "BoundaryConditions", "compute_tau", "cm_permutation", "STEP_NAMES", "eval_dij",
-           "eval_limiter"]
+           "eval_limiter", "eval_arith"]
 
 STEP_NAMES = ["step0", "step1", "step2", "step3", "step4", "step5", "step6"]
 
@@ -385,4 +385,16 @@ def eval_limiter(U, P, bounds, newton_steps=2, gas=None):
     prm = _params(gas, newton_steps)
     _raise(_lib.load().ef_eval_limiter(ctypes.byref(prm), nv - 2, n, U.ctypes.data, P.ctypes.data,
                                        bounds.ctypes.data, out.ctypes.data))
+    return out
+
+
+def eval_arith(a, b):
+    """Mismatch counts of the d_ij kernel's straight-line 1/b, a/b, sqrt|a| and shared-reciprocal
+    a/b (csrc/ef_math.cuh) against the IEEE operations, over the operands inside the safe range."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    if a.shape != b.shape or a.ndim != 1:
+        raise ValueError("a and b must be 1-D arrays of one length")
+    out = np.zeros(4, dtype=np.uint64)
+    _raise(_lib.load().ef_eval_arith(a.size, a.ctypes.data, b.ctypes.data, out.ctypes.data))
     return out

@@ -19,7 +19,7 @@ import pytest
 import oracle as O
 from goldens import GOLDEN_DIR
 from paper_2007_00094_b200.physics import AIR
-from paper_2007_00094_b200.stepper import eval_dij, eval_limiter
+from paper_2007_00094_b200.stepper import eval_arith, eval_dij, eval_limiter
 
 pytestmark = pytest.mark.gpu
 
@@ -157,3 +157,75 @@ def test_limiter_fast_accept_bound_is_an_upper_bound():
     xs = np.array([2.0 ** -21, 2.0 ** 21, 0.0, np.nan])
     _lib.load().ef_pow_bound_device(xs.ctypes.data, 2.4, out.ctypes.data, 4)
     assert np.all(np.isinf(out))
+
+
+def _bit_patterns(rng, n):
+    """Doubles with exponents in the safe range and adversarial significands: random bits,
+    all ones / all zeros tails, neighbours of powers of two and of squares."""
+    sig = rng.integers(0, 1 << 52, n, dtype=np.uint64)
+    kind = rng.integers(0, 8, n)
+    tail = rng.integers(1, 52, n).astype(np.uint64)
+    ones = (np.uint64(1) << tail) - np.uint64(1)
+    sig = np.where(kind == 0, sig | ones, sig)                       # trailing ones
+    sig = np.where(kind == 1, sig & ~ones, sig)                      # trailing zeros
+    sig = np.where(kind == 2, ones, sig)                             # just above a power of two
+    sig = np.where(kind == 3, np.uint64((1 << 52) - 1) ^ ones, sig)  # just below the next one
+    e = rng.integers(1023 - 450, 1023 + 450, n).astype(np.uint64)
+    sign = rng.integers(0, 2, n).astype(np.uint64)
+    return ((sign << np.uint64(63)) | (e << np.uint64(52)) | sig).view(np.float64)
+
+
+def test_straight_line_division_and_root_are_ieee():
+    """rcp_sl / div_sl / sqrt_sl / qdiv_sl (ef_math.cuh) restate nvcc's fast paths of 1/b, a/b,
+    sqrt: no operand in the safe range may differ in a bit (the reference divides and takes
+    roots with numpy's IEEE operations, riemann.py:56-109)."""
+    rng = np.random.default_rng(20070094)
+    total = np.zeros(4, dtype=np.uint64)
+    for _ in range(4):
+        n = 1 << 24
+        a, b = _bit_patterns(rng, n), _bit_patterns(rng, n)
+        # quotients near 1 and exact squares / products stress the final rounding
+        k = n // 4
+        b[:k] = a[:k] * (1.0 + rng.integers(-4, 5, k) * 2.0 ** -52)
+        r = np.abs(_bit_patterns(rng, k))
+        a[k:2 * k] = np.where(np.isfinite(r * r) & (r * r > 0), r * r, a[k:2 * k])
+        total += eval_arith(a, b)
+    assert not total.any(), total
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_device_dij_corner_cases_equal_oracle(dim):
+    """Pairs that leave the straight-line path (or sit on its selects): zero momenta and
+    momenta along / across the normal, equal pressures, strong shocks and expansions up to
+    vacuum, extreme magnitudes, inadmissible states."""
+    rng = np.random.default_rng(77 + dim)
+    n = 60000
+    Ui, Uj = _states(rng, n, dim), _states(rng, n, dim)
+    cij = rng.normal(0.0, 1.0, (n, dim))
+    cji = -cij * (1 + 1e-3 * rng.normal(size=(n, 1)))
+    k = n // 12
+    s = [slice(q * k, (q + 1) * k) for q in range(12)]
+    Ui[s[0], 1:-1] = 0.0                                        # i at rest
+    Ui[s[1], 1:-1] = 0.0
+    Uj[s[1], 1:-1] = 0.0                                        # both at rest
+    cij[s[2], 1:] = 0.0                                         # axis-aligned normals
+    cji[s[2], 1:] = 0.0
+    Ui[s[2], 2:-1] = 0.0                                        # momentum along the normal: tt = 0
+    Uj[s[3]] = Ui[s[3]]                                         # equal pressures, opposite velocities
+    Uj[s[3], 1:-1] = -Ui[s[3], 1:-1]
+    Uj[s[4], 1:-1] += 30.0 * Uj[s[4], :1] * cij[s[4]] / np.linalg.norm(cij[s[4]], axis=1, keepdims=True)  # vacuum
+    Uj[s[5], 1:-1] -= 30.0 * Uj[s[5], :1] * cij[s[5]] / np.linalg.norm(cij[s[5]], axis=1, keepdims=True)  # two shocks
+    Uj[s[6], -1] *= 1e6                                         # pressure ratio 1e6
+    Ui[s[7]] *= 1e60                                            # large magnitudes
+    Uj[s[7]] *= 1e60
+    Ui[s[8]] *= 1e-70                                           # small magnitudes
+    Uj[s[8]] *= 1e-70
+    Uj[s[9], -1] = 0.5 * (Uj[s[9], 1:-1] ** 2).sum(axis=1) / Uj[s[9], 0] * (1 - 1e-3)  # p < 0
+    Uj[s[10], 0] = -Uj[s[10], 0]                                # rho < 0
+    cji[s[11]] = 0.0                                            # a zero-norm direction
+    with np.errstate(all="ignore"):
+        d, bad = eval_dij(Ui, Uj, cij, cji)
+        do, bo = O.eval_dij(Ui, Uj, cij, cji)
+    assert np.array_equal(bad, bo) and bo[s[9]].all() and bo[s[10]].all() and not bo[s[0]].any()
+    good = bo == 0  # a flagged pair raises; its value is not used
+    assert np.array_equal(d[good].view(np.int64), do[good].view(np.int64))
