@@ -17,11 +17,20 @@ passes = int(kw.get("passes", 2))
 newton = int(kw.get("newton", 2))
 steps = int(kw.get("steps", 20))
 warm = int(kw.get("warm", 20))
-ps = P.make_config(cfg)
 st = torch.cuda.Stream()
-s = Solver(ps.matrices, c_cfl=ps.c_cfl, boundary=ps.boundary, limiter_passes=passes, newton_steps=newton,
-           stream=st.cuda_stream)
-s.set_state(ps.U0)
+if cfg.startswith("c5w"):  # bench.py's default path: per-rank setup in lexicographic order, one rank (c5w160 = 160^3)
+    from paper_2007_00094_b200.distributed import ShardedSolver
+
+    lp = P.periodic_fourier_box_local(int(cfg[3:] or 320), 0, 1)
+    s = ShardedSolver([lp.local], limiter_passes=passes, newton_steps=newton, stream=st.cuda_stream)
+    s.set_state(lp.U0)
+    n_nodes = s.n
+else:
+    ps = P.make_config(cfg)
+    s = Solver(ps.matrices, c_cfl=ps.c_cfl, boundary=ps.boundary, limiter_passes=passes, newton_steps=newton,
+               stream=st.cuda_stream)
+    s.set_state(ps.U0)
+    n_nodes = ps.matrices.n
 for _ in range(warm):
     s.ssp_rk3_step_async()
 s.sync()
@@ -34,4 +43,4 @@ t1 = s.timers
 per = {k: (t1[k] - t0[k]) / (3 * steps) * 1e3 for k in t0}
 tot = sum(per.values())
 print(cfg, f"passes={passes} newton={newton}", " ".join(f"{k}={v:.3f}" for k, v in per.items()),
-      f"total={tot:.3f} ms/stage -> {ps.matrices.n / (tot * 1e-3):.3e} node-upd/s")
+      f"total={tot:.3f} ms/stage -> {n_nodes / (tot * 1e-3):.3e} node-upd/s")
