@@ -234,7 +234,6 @@ static Gas make_gas(const ef_params* p) {
   g.fast_accept = (fa && fa[0] == '0') ? 0 : 1;
   const char* sl = std::getenv("EF_SL");  // straight-line d_ij path (ef_math.cuh); results are identical either way
   g.sl = (sl && sl[0] == '0') ? 0 : 1;
-  g.y7 = std::fabs(p->two_g_over_gm1 - 7.0) < 1e-13 ? 1 : 0;
   return g;
 }
 

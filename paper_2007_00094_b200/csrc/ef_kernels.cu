@@ -206,14 +206,6 @@ constexpr double kZeroP = -1.0;
 #ifndef EF_ZSKIP
 #define EF_ZSKIP 1
 #endif
-// L2 prefetch distance (slots) of c / d in the row loops of k_row_visc / k_low_order (0: off)
-#ifndef EF_PF_ROW3
-#define EF_PF_ROW3 0
-#endif
-#ifndef EF_PF_ROW2
-#define EF_PF_ROW2 0
-#endif
-#define EF_PF_ROW(D) ((D) == 3 ? EF_PF_ROW3 : EF_PF_ROW2)
 #ifndef EF_PF_LIM
 #define EF_PF_LIM 131072
 #endif
@@ -493,10 +485,6 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ROW(D), D)) k_row_v
         for (int a = 0; a < D; ++a) cp_async8(&buf[st][NV + 1 + a][t], m.c + (size_t)a * NPL + p);
 #pragma unroll
         for (int a = 0; a < NQ; ++a) cp_async8(&buf[st][NV + 1 + D + a][t], w.vp + a * NP + j);
-        if (EF_PF_ROW(D) > 0 && s + EF_PF_ROW(D) < card) {  // the streamed slot arrays, a few slots ahead, into L2
-#pragma unroll
-          for (int a = 0; a < D; ++a) pf_l2(m.c + (size_t)a * NPL + p + 32 * EF_PF_ROW(D));
-        }
       };
       auto body = [&](int, int st) {
         double Uj[NV], cc[D], vpj[D + 1];
@@ -683,11 +671,6 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_LOW(D), D)) k_low_o
       cp_async8(&buf[st][NV + 2 + D][t], w.d + p);
 #pragma unroll
       for (int a = 0; a < NQ; ++a) cp_async8(&buf[st][NV + 3 + D + a][t], w.vp + a * NP + j);
-      if (EF_PF_ROW(D) > 0 && s + EF_PF_ROW(D) < card) {  // the streamed slot arrays, a few slots ahead, into L2
-#pragma unroll
-        for (int a = 0; a < D; ++a) pf_l2(m.c + (size_t)a * NPL + p + 32 * EF_PF_ROW(D));
-        pf_l2(w.d + p + 32 * EF_PF_ROW(D));
-      }
     };
     auto body = [&](int, int st) {
       double Uj[NV], cc[D];
