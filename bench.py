@@ -133,6 +133,7 @@ class ClockSampler:
 CPU_MAX_NODES = 5_000_000
 # configs whose ranks are built from their own rows (no rank holds the global matrix)
 PER_RANK = ("c5w", "c4")
+FORCE_NCCL = os.environ.get("EF_BENCH_NCCL") == "1"
 CPU_SAMPLE_OF = {"c3": "c3m", "c4": "c4m", "c5": "c5m"}
 
 
@@ -243,7 +244,7 @@ def run_ours(args, rank, world, local_rank):
     from paper_2007_00094_b200 import Solver
     from paper_2007_00094_b200.perf import KERNEL_OF_PHASE, PHASES, predict_traffic, stage_doubles_per_nnz
 
-    dist = world > 1
+    dist = world > 1 or FORCE_NCCL  # (EF_BENCH_NCCL=1: the N > 1 code path with a one-rank communicator)
     torch.cuda.set_device(local_rank)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
@@ -485,7 +486,7 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
-    if world > 1:
+    if world > 1 or FORCE_NCCL:
         import torch
 
         torch.cuda.set_device(local_rank)
@@ -493,7 +494,7 @@ def main():
     try:
         run_ours(args, rank, world, local_rank)
     finally:
-        if world > 1:
+        if world > 1 or FORCE_NCCL:
             import torch
 
             torch.distributed.destroy_process_group()
