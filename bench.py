@@ -372,7 +372,9 @@ def run_ours(args, rank, world, local_rank):
     prof = {}
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-            prof = json.load(fh).get(args.config, {}).get(KERNEL_OF_PHASE[dom], {})
+            allprof = json.load(fh)
+            prof = (allprof.get(args.config) or allprof.get("c5" if args.config == "c5w" else args.config, {})
+                    ).get(KERNEL_OF_PHASE[dom], {})
         traffic = prof.get("traffic_bytes")
     except Exception:
         traffic = None

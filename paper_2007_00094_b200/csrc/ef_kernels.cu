@@ -326,8 +326,8 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_EDGE(D), D)) k_edge
       w.nonuni[i] = 1;
       w.nonuni[j] = 1;
     }
-    // the straight-line evaluation (ef_math.cuh); identical states keep their closed form
-    if (!(UNI && same)) done = d_ij_sl<D>(Ui, Uj, nij, norm_ij, nji, norm_ji, g, dv);
+    // the straight-line evaluation (ef_math.cuh); identical states by their closed form
+    done = d_ij_sl<D>(Ui, Uj, nij, norm_ij, nji, norm_ji, g, dv, UNI && same);
   }
   if (!done) {
     // zero or extreme operands, an inadmissible state, vacuum, identical states: the
@@ -1228,7 +1228,7 @@ __global__ void k_eval_dij(Gas g, int64_t n, const double* __restrict__ Ui, cons
   double dv;
   // as k_edge_visc<D, true>: identical states by their closed form, then the straight-line path, else the general code
   const bool same = same_state<NV>(a, b);
-  if (same || !d_ij_sl<D>(a, b, nij, norm_ij, nji, norm_ji, g, dv)) dv = d_ij_geo<D>(a, b, nij, norm_ij, nji, norm_ji, g, bd, same);
+  if (!d_ij_sl<D>(a, b, nij, norm_ij, nji, norm_ji, g, dv, same)) dv = d_ij_geo<D>(a, b, nij, norm_ij, nji, norm_ji, g, bd, same);
   out[q] = dv;
   bad[q] = bd ? 1 : 0;
 }

@@ -17,6 +17,7 @@ passes = int(kw.get("passes", 2))
 newton = int(kw.get("newton", 2))
 steps = int(kw.get("steps", 20))
 warm = int(kw.get("warm", 20))
+uni = int(kw.get("uni", -1))  # 0: identical-state shortcuts forced off (bench.py's general path)
 st = torch.cuda.Stream()
 if cfg.startswith("c5w"):  # bench.py's default path: per-rank setup in lexicographic order, one rank (c5w160 = 160^3)
     from paper_2007_00094_b200.distributed import ShardedSolver
@@ -31,6 +32,8 @@ else:
                stream=st.cuda_stream)
     s.set_state(ps.U0)
     n_nodes = ps.matrices.n
+if uni >= 0:
+    s.set_uniform_shortcuts(uni)
 for _ in range(warm):
     s.ssp_rk3_step_async()
 s.sync()
@@ -42,5 +45,5 @@ s.sync()
 t1 = s.timers
 per = {k: (t1[k] - t0[k]) / (3 * steps) * 1e3 for k in t0}
 tot = sum(per.values())
-print(cfg, f"passes={passes} newton={newton}", " ".join(f"{k}={v:.3f}" for k, v in per.items()),
+print(cfg, f"passes={passes} newton={newton} uni={uni}", " ".join(f"{k}={v:.3f}" for k, v in per.items()),
       f"total={tot:.3f} ms/stage -> {n_nodes / (tot * 1e-3):.3e} node-upd/s")
