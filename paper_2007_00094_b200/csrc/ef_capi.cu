@@ -416,7 +416,8 @@ static int build_from_plan(ef_solver* h, ef::Plan& P, Src& S, const ef_boundary*
   // the edge position (one coalesced load each) instead of through col/tslot
   std::vector<int32_t> edge_j(std::max<int64_t>(NE, 1), 0), edge_pt(std::max<int64_t>(NE, 1), 0);
   // static edge geometry (riemann.py:131-136): n = c / |c|, |c| = sqrt(R1(c*c)),
-  // for c_ij and c_ji, evaluated with the reference's operation order
+  // for c_ij and c_ji, evaluated with the reference's operation order; one record of
+  // 2 (D + 1) doubles per edge (the edge kernel reads it as 16-byte pairs)
   ef::hvec<double> egeo((size_t)2 * (D + 1) * std::max<int64_t>(NE, 1));
   if (NE == 0)
     for (auto& v : egeo) v = 0.0;
@@ -436,8 +437,8 @@ static int build_from_plan(ef_solver* h, ef::Plan& P, Src& S, const ef_boundary*
         const double nrm = std::sqrt((double)ss);
         const int base = dir * (D + 1);
         for (int d = 0; d < D; ++d)
-          egeo[(size_t)(base + d) * NE + e] = nrm > 0.0 ? c[(size_t)d * NPL + q] / nrm : (d == 0 ? 1.0 : 0.0);
-        egeo[(size_t)(base + D) * NE + e] = nrm;
+          egeo[(size_t)e * (2 * (D + 1)) + base + d] = nrm > 0.0 ? c[(size_t)d * NPL + q] / nrm : (d == 0 ? 1.0 : 0.0);
+        egeo[(size_t)e * (2 * (D + 1)) + base + D] = nrm;
       }
     }
   });

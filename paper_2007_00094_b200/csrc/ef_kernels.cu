@@ -275,16 +275,28 @@ __global__ void k_nodal(Layout m, Gas g, const double* __restrict__ U, Work w, i
 // slot after the diagonal; stepper.py:211, 415).  The edge list holds SELL
 // positions in ascending order, so a warp reads 32 consecutive positions of
 // one slot row (coalesced) and the row / slot are recovered from the position.
+// the two states and the geometry record (n_ij, |c_ij|, n_ji, |c_ji|) of an edge
 template <int D>
-__device__ __forceinline__ void load_edge(const Layout& m, const double* __restrict__ U, int NP, int NE, int e, int i,
-                                          int j, double* Ui, double* Uj, double* nij, double* nji) {
+__device__ __forceinline__ void load_edge(const Layout& m, const double* __restrict__ U, int NP, int e, int i, int j,
+                                          double* Ui, double* Uj, double* nij, double& norm_ij, double* nji,
+                                          double& norm_ji) {
   load_node<D + 2>(U, NP, i, Ui);
   load_node<D + 2>(U, NP, j, Uj);
+  double g[2 * (D + 1)];
+  const double2* __restrict__ rec = reinterpret_cast<const double2*>(m.egeo) + (size_t)e * (D + 1);
+#pragma unroll
+  for (int k = 0; k < D + 1; ++k) {
+    const double2 v = rec[k];
+    g[2 * k] = v.x;
+    g[2 * k + 1] = v.y;
+  }
 #pragma unroll
   for (int a = 0; a < D; ++a) {
-    nij[a] = m.egeo[(size_t)a * NE + e];
-    nji[a] = m.egeo[(size_t)(D + 1 + a) * NE + e];
+    nij[a] = g[a];
+    nji[a] = g[D + 1 + a];
   }
+  norm_ij = g[D];
+  norm_ji = g[2 * D + 1];
 }
 template <int D, bool UNI>
 __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_EDGE(D), D)) k_edge_visc(Layout m, Gas g, const double* __restrict__ U,
@@ -318,9 +330,8 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_EDGE(D), D)) k_edge
   bool bad = false, same = false, done = false;
   double dv;
   {
-    double Ui[NV], Uj[NV], nij[D], nji[D];
-    load_edge<D>(m, U, NP, NE, e, i, j, Ui, Uj, nij, nji);
-    const double norm_ij = m.egeo[(size_t)D * NE + e], norm_ji = m.egeo[(size_t)(2 * D + 1) * NE + e];
+    double Ui[NV], Uj[NV], nij[D], nji[D], norm_ij, norm_ji;
+    load_edge<D>(m, U, NP, e, i, j, Ui, Uj, nij, norm_ij, nji, norm_ji);
     if (UNI || ((flags & 2) && (blockIdx.x & 7) == 0)) same = same_state<NV>(Ui, Uj);
     if (UNI && !same) {
       w.nonuni[i] = 1;
@@ -333,9 +344,8 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_EDGE(D), D)) k_edge
     // zero or extreme operands, an inadmissible state, vacuum, identical states: the
     // general code on operands loaded again (nothing of the rare path stays live above)
     asm volatile("" ::: "memory");
-    double Ui[NV], Uj[NV], nij[D], nji[D];
-    load_edge<D>(m, U, NP, NE, e, i, j, Ui, Uj, nij, nji);
-    const double norm_ij = m.egeo[(size_t)D * NE + e], norm_ji = m.egeo[(size_t)(2 * D + 1) * NE + e];
+    double Ui[NV], Uj[NV], nij[D], nji[D], norm_ij, norm_ji;
+    load_edge<D>(m, U, NP, e, i, j, Ui, Uj, nij, norm_ij, nji, norm_ji);
     dv = d_ij_geo<D>(Ui, Uj, nij, norm_ij, nji, norm_ji, g, bad, UNI && same);
   }
   // d is symmetric by construction (riemann.py:139-142): the value is also

@@ -52,7 +52,7 @@ struct Layout {
   const uint8_t* cardf;  // [NP] full stencil cardinality (ghost rows: the owner's)
   const uint8_t* diag;   // [NP] slot of the diagonal
   const double* c;       // [D][NP*L]  c_ij
-  const double* egeo;    // [2(D+1)][n_edges]  n_ij, |c_ij|, n_ji, |c_ji| per upper edge
+  const double* egeo;    // [n_edges][2(D+1)]  n_ij, |c_ij|, n_ji, |c_ji| per upper edge (16-byte aligned records)
   const double* mij;     // [NP*L]     consistent mass m_ij
   const double* m_i;     // [NP] lumped mass
   const double* inv_m;   // [NP]
