@@ -234,6 +234,8 @@ static Gas make_gas(const ef_params* p) {
   g.fast_accept = (fa && fa[0] == '0') ? 0 : 1;
   const char* sl = std::getenv("EF_SL");  // straight-line d_ij path (ef_math.cuh); results are identical either way
   g.sl = (sl && sl[0] == '0') ? 0 : 1;
+  g.near7_a = ef_near7(g.neg_gm1_over_2g);
+  g.near7_b = ef_near7(g.two_g_over_gm1);
   return g;
 }
 

@@ -481,7 +481,8 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ROW(D), D)) k_row_v
     };
     {
       constexpr int NQ = EF_VP_ROW(D) ? D + 1 : 0;  // v_j, p_j
-      constexpr int F = NV + 1 + D + NQ;     // U_j, eor_j, c, (v_j, p_j)
+      constexpr int K0 = EF_VP_ROW(D) ? 1 : 0;      // rho_j is not used once v_j, p_j are cached
+      constexpr int F = (NV - K0) + 1 + D + NQ;     // U_j (from K0), eor_j, c, (v_j, p_j)
       __shared__ double buf[2][F][EF_TPB_D(D)];
       const int t = threadIdx.x;
       auto issue = [&](int s, int j, int st) {
@@ -489,22 +490,23 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ROW(D), D)) k_row_v
         EF_IN(j, m.n_local);
         EF_IN(p, NPL);
 #pragma unroll
-        for (int k = 0; k < NV; ++k) cp_async8(&buf[st][k][t], U + k * NP + j);
-        cp_async8(&buf[st][NV][t], w.eor + j);
+        for (int k = K0; k < NV; ++k) cp_async8(&buf[st][k - K0][t], U + k * NP + j);
+        cp_async8(&buf[st][NV - K0][t], w.eor + j);
 #pragma unroll
-        for (int a = 0; a < D; ++a) cp_async8(&buf[st][NV + 1 + a][t], m.c + (size_t)a * NPL + p);
+        for (int a = 0; a < D; ++a) cp_async8(&buf[st][NV - K0 + 1 + a][t], m.c + (size_t)a * NPL + p);
 #pragma unroll
-        for (int a = 0; a < NQ; ++a) cp_async8(&buf[st][NV + 1 + D + a][t], w.vp + a * NP + j);
+        for (int a = 0; a < NQ; ++a) cp_async8(&buf[st][NV - K0 + 1 + D + a][t], w.vp + a * NP + j);
       };
       auto body = [&](int, int st) {
         double Uj[NV], cc[D], vpj[D + 1];
+        Uj[0] = 0.0;  // (unused with the v, p cache)
 #pragma unroll
-        for (int k = 0; k < NV; ++k) Uj[k] = buf[st][k][t];
+        for (int k = K0; k < NV; ++k) Uj[k] = buf[st][k - K0][t];
 #pragma unroll
-        for (int a = 0; a < D; ++a) cc[a] = buf[st][NV + 1 + a][t];
+        for (int a = 0; a < D; ++a) cc[a] = buf[st][NV - K0 + 1 + a][t];
 #pragma unroll
-        for (int a = 0; a < NQ; ++a) vpj[a] = buf[st][NV + 1 + D + a][t];
-        slot(Uj, cc, buf[st][NV][t], vpj);
+        for (int a = 0; a < NQ; ++a) vpj[a] = buf[st][NV - K0 + 1 + D + a][t];
+        slot(Uj, cc, buf[st][NV - K0][t], vpj);
       };
       if (!uni) row_pipe(m.col, base, card, dg, issue, body);
     }
