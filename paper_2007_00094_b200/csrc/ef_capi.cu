@@ -236,6 +236,8 @@ static Gas make_gas(const ef_params* p) {
   g.sl = (sl && sl[0] == '0') ? 0 : 1;
   g.near7_a = ef_near7(g.neg_gm1_over_2g);
   g.near7_b = ef_near7(g.two_g_over_gm1);
+  g.near7_gp1 = ef_near7(g.gp1);
+  g.near7_gamma = ef_near7(g.gamma);
   return g;
 }
 
