@@ -234,10 +234,10 @@ static Gas make_gas(const ef_params* p) {
   g.fast_accept = (fa && fa[0] == '0') ? 0 : 1;
   const char* sl = std::getenv("EF_SL");  // straight-line d_ij path (ef_math.cuh); results are identical either way
   g.sl = (sl && sl[0] == '0') ? 0 : 1;
-  g.near7_a = ef_near7(g.neg_gm1_over_2g);
-  g.near7_b = ef_near7(g.two_g_over_gm1);
-  g.near7_gp1 = ef_near7(g.gp1);
-  g.near7_gamma = ef_near7(g.gamma);
+  g.kind_a = ef_pow_kind(g.neg_gm1_over_2g);
+  g.kind_b = ef_pow_kind(g.two_g_over_gm1);
+  g.kind_gp1 = ef_pow_kind(g.gp1);
+  g.kind_gamma = ef_pow_kind(g.gamma);
   return g;
 }
 

@@ -45,3 +45,38 @@ def test_pow_is_monotone_on_a_fine_grid():
         r = O.shared_pow(x, y)
         d = np.diff(r)
         assert (d >= 0).all() if y > 0 else (d <= 0).all()
+
+
+def _worst_ulp(x, y):
+    mp.mp.prec = 160
+    r = O.shared_pow(x, y)
+    worst = 0.0
+    for xi, ri in zip(x, r):
+        ex = mp.power(mp.mpf(float(xi)), mp.mpf(y))
+        worst = max(worst, float(abs(mp.mpf(float(ri)) - ex) / math.ulp(float(ex))))
+    return worst
+
+
+@pytest.mark.parametrize("name", ["two_g_over_gm1", "neg_gm1_over_2g"])
+def test_specialised_pows_of_gamma_seven_fifths(name):
+    """ef_pow7 / ef_powm17 (csrc/ef_pow.h): the two-rarefaction exponents of gamma = 7/5
+    (riemann.py:88-100) stay within 0.52 ulp over their whole argument range 2^-100 .. 2^100,
+    and the pow is continuous (to an ulp) where it hands over to the general algorithm."""
+    from paper_2007_00094_b200.physics import AIR
+
+    y = AIR.two_g_over_gm1 if name == "two_g_over_gm1" else -AIR.gm1_over_2g
+    assert abs(y - (7.0 if y > 0 else -1 / 7)) < 2.0 ** -44  # the specialised algorithms apply
+    rng = np.random.default_rng(5)
+    lim = 100.0 / 7.2 if y > 0 else 100.0  # keep x^7 finite
+    x = np.concatenate([np.exp2(rng.uniform(-lim, lim, 3000)), rng.uniform(0.25, 4.0, 3000),
+                        1.0 + rng.standard_normal(500) * 1e-6,
+                        np.exp2(rng.integers(-99, 100, 200).astype(np.float64)) * (1.0 + 2.0 ** -52)])
+    assert _worst_ulp(x, y) < 0.52
+    for edge in (2.0 ** -100, 2.0 ** 100):  # hand-over to the general algorithm
+        xs = np.array([np.nextafter(edge, 0.0), edge, np.nextafter(edge, np.inf)])
+        with np.errstate(all="ignore"):
+            r = O.shared_pow(xs, y)
+        if np.isfinite(r).all() and (r > 1e-300).all():
+            assert _worst_ulp(xs, y) < 0.52
+    # an exponent just outside the 2^-44 window takes the general algorithm: same accuracy class
+    assert _worst_ulp(x[:500], y + 2.0 ** -40) < 0.52
