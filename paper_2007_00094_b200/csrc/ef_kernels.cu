@@ -206,18 +206,6 @@ constexpr double kZeroP = -1.0;
 #ifndef EF_ZSKIP
 #define EF_ZSKIP 1
 #endif
-// stages of the row kernels' cp.async slot prefetch (3D; 2D keeps two)
-#ifndef EF_ROW_STAGES3
-#define EF_ROW_STAGES3 2
-#endif
-#ifndef EF_LOW_STAGES3
-#define EF_LOW_STAGES3 2
-#endif
-#define EF_ROW_STAGES(D) ((D) == 3 ? EF_ROW_STAGES3 : 2)
-#define EF_LOW_STAGES(D) ((D) == 3 ? EF_LOW_STAGES3 : 2)
-#ifndef EF_LIM_LOADS
-#define EF_LIM_LOADS 0
-#endif
 #ifndef EF_PF_LIM
 #define EF_PF_LIM 131072
 #endif
@@ -389,37 +377,31 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
-// Row loop over the real slots s != diag in ascending order with an S-stage
-// prefetch: the fields of the slot S-1 ahead are issued (issue(s, j, stage))
-// before slot s is consumed (body(s, stage)); the column of the slot after that
-// is loaded one iteration ahead so the issue never waits on it.
-template <int S, class Issue, class Body>
+// Row loop over the real slots s != diag in ascending order with a two-stage
+// prefetch: slot s+1's fields are issued (issue(s, j, stage)) before slot s is
+// consumed (body(s, stage)); the column of slot s+2 is loaded one iteration
+// ahead so the issue never waits on it.
+template <class Issue, class Body>
 __device__ __forceinline__ void row_pipe(const int* __restrict__ col, int base, int card, int dg, Issue issue,
                                          Body body) {
-  auto nxt = [dg](int s) { return s + 1 + (s + 1 == dg ? 1 : 0); };
-  int sA = (dg == 0) ? 1 : 0;  // next slot to consume
-  int sB = sA;                 // next slot to issue
-#pragma unroll
-  for (int k = 0; k < S - 1; ++k) {
-    if (sB < card) issue(sB, col[base + sB * 32], k);
-    cp_commit();
-    sB = nxt(sB);
-  }
+  int sA = (dg == 0) ? 1 : 0;
+  int sB = sA + 1 + (sA + 1 == dg ? 1 : 0);
+  if (sA < card) issue(sA, col[base + sA * 32], 0);
+  cp_commit();
   int jB = (sB < card) ? col[base + sB * 32] : 0;
-  int st = 0, sn = S - 1;  // stage of the slot consumed / issued in this iteration
-  while (sA < card) {
-    if (sB < card) issue(sB, jB, sn);
+  for (int it = 0; sA < card; ++it) {
+    const int st = it & 1;
+    if (sB < card) issue(sB, jB, st ^ 1);
     cp_commit();
-    sB = nxt(sB);
-    jB = (sB < card) ? col[base + sB * 32] : 0;
-    cp_wait<S - 1>();
+    const int sC = sB + 1 + (sB + 1 == dg ? 1 : 0);
+    const int jC = (sC < card) ? col[base + sC * 32] : 0;
+    cp_wait1();
     body(sA, st);
-    sA = nxt(sA);
-    st = (st + 1 == S) ? 0 : st + 1;
-    sn = (sn + 1 == S) ? 0 : sn + 1;
+    sA = sB;
+    sB = sC;
+    jB = jC;
   }
 }
 // k_low_order: the prefetch pays once the kernel may keep more registers
@@ -501,7 +483,7 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ROW(D), D)) k_row_v
       constexpr int NQ = EF_VP_ROW(D) ? D + 1 : 0;  // v_j, p_j
       constexpr int K0 = EF_VP_ROW(D) ? 1 : 0;      // rho_j is not used once v_j, p_j are cached
       constexpr int F = (NV - K0) + 1 + D + NQ;     // U_j (from K0), eor_j, c, (v_j, p_j)
-      __shared__ double buf[EF_ROW_STAGES(D)][F][EF_TPB_D(D)];
+      __shared__ double buf[2][F][EF_TPB_D(D)];
       const int t = threadIdx.x;
       auto issue = [&](int s, int j, int st) {
         const int p = base + s * 32;
@@ -526,7 +508,7 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_ROW(D), D)) k_row_v
         for (int a = 0; a < NQ; ++a) vpj[a] = buf[st][NV - K0 + 1 + D + a][t];
         slot(Uj, cc, buf[st][NV - K0][t], vpj);
       };
-      if (!uni) row_pipe<EF_ROW_STAGES(D)>(m.col, base, card, dg, issue, body);
+      if (!uni) row_pipe(m.col, base, card, dg, issue, body);
     }
     // d row sum over the L padded slots (lower slots were filled by k_edge_visc)
     double* __restrict__ d = w.d;
@@ -686,7 +668,7 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_LOW(D), D)) k_low_o
     // fields per slot: U_j (NV), alpha_j, phi_j, c (D), d
     constexpr int NQ = EF_VP_LOW(D) ? D + 1 : 0;  // v_j, p_j
     constexpr int F = NV + 2 + D + 1 + NQ;
-    __shared__ double buf[EF_LOW_STAGES(D)][F][EF_TPB_D(D)];
+    __shared__ double buf[2][F][EF_TPB_D(D)];
     const int t = threadIdx.x;
     auto issue = [&](int s, int j, int st) {
       const int p = base + s * 32;
@@ -713,7 +695,7 @@ __global__ void __launch_bounds__(EF_TPB_D(D), EF_LB(EF_MINB_LOW(D), D)) k_low_o
       for (int a = 0; a < NQ; ++a) vpj[a] = buf[st][NV + 3 + D + a][t];
       slot(Uj, cc, buf[st][NV + 2 + D][t], buf[st][NV][t], buf[st][NV + 1][t], vpj);
     };
-    if (!uni) row_pipe<EF_LOW_STAGES(D)>(m.col, base, card, dg, issue, body);
+    if (!uni) row_pipe(m.col, base, card, dg, issue, body);
   }
   const double fac = tau * m.inv_m[i];
 #pragma unroll
@@ -835,19 +817,6 @@ __device__ __forceinline__ void edge_lim_one(const Layout& m, const Gas& g, cons
   // forms the same product P_(q-1) (1 - min l) itself, which saves the largest
   // write of the stage.  Every other pass stores its P_q.
   const bool last = q == sp.passes - 1;
-#if EF_LIM_LOADS == 1
-  // both rows' limiter inputs are requested before the P stores (a load cannot be moved
-  // above a store that may alias it): one round trip for U^L and the bounds of i and j,
-  // overlapped with the stores, instead of one after the stores and one after limiter(i)
-  double Uni[NV], Unj[NV], bi3[3], bj3[3];
-  load_node<NV>(w.Unext, NP, i, Uni);
-  load_node<NV>(w.Unext, NP, j, Unj);
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    bi3[k] = w.bounds[k * NP + i];
-    bj3[k] = w.bounds[k * NP + j];
-  }
-#endif
   if (FIRST || !last) {
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
@@ -855,28 +824,11 @@ __device__ __forceinline__ void edge_lim_one(const Layout& m, const Gas& g, cons
       w.P[(size_t)k * NPL + pt] = Pj[k];
     }
   }
-#if EF_LIM_LOADS == 1
-  const double li = limiter<D>(Uni, Pi, bi3[0], bi3[1], bi3[2], sp.newton, g);
-  const double lj = limiter<D>(Unj, Pj, bj3[0], bj3[1], bj3[2], sp.newton, g);
-#elif EF_LIM_LOADS == 2
-  // after the stores, but both rows at once
-  double Uni[NV], Unj[NV], bi3[3], bj3[3];
-  load_node<NV>(w.Unext, NP, i, Uni);
-  load_node<NV>(w.Unext, NP, j, Unj);
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    bi3[k] = w.bounds[k * NP + i];
-    bj3[k] = w.bounds[k * NP + j];
-  }
-  const double li = limiter<D>(Uni, Pi, bi3[0], bi3[1], bi3[2], sp.newton, g);
-  const double lj = limiter<D>(Unj, Pj, bj3[0], bj3[1], bj3[2], sp.newton, g);
-#else
   double Un[NV];
   load_node<NV>(w.Unext, NP, i, Un);
   const double li = limiter<D>(Un, Pi, w.bounds[i], w.bounds[NP + i], w.bounds[2 * NP + i], sp.newton, g);
   load_node<NV>(w.Unext, NP, j, Un);
   const double lj = limiter<D>(Un, Pj, w.bounds[j], w.bounds[NP + j], w.bounds[2 * NP + j], sp.newton, g);
-#endif
   edge_lim_store<D>(m, w, sp, q, p, j, pt, e, i, li, lj);
 }
 
