@@ -229,3 +229,48 @@ def test_device_dij_corner_cases_equal_oracle(dim):
     assert np.array_equal(bad, bo) and bo[s[9]].all() and bo[s[10]].all() and not bo[s[0]].any()
     good = bo == 0  # a flagged pair raises; its value is not used
     assert np.array_equal(d[good].view(np.int64), do[good].view(np.int64))
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_device_dij_psi_sign_near_ties_equal_oracle(dim):
+    """The straight-line path decides the sign of psi = f_lo + du (riemann.py:103) from an
+    approximation with a certified margin (ef_math.cuh: lambda_sl) and leaves near-ties to
+    the general code: pairs whose velocity jump cancels the shock function to a relative
+    1e-6 ... one ulp, and equal-pressure pairs (f_lo = +0: the sign is du's) with
+    compressive, expansive and zero velocity jumps."""
+    rng = np.random.default_rng(401 + dim)
+    n = 40000
+    g = AIR.gamma
+    rhoL, rhoR = np.exp(rng.uniform(-2, 2, n)), np.exp(rng.uniform(-2, 2, n))
+    pL, pR = np.exp(rng.uniform(-2, 2, n)), np.exp(rng.uniform(-2, 2, n))
+    eq = np.arange(n) % 4 == 0
+    pR[eq] = pL[eq]
+    lo = pL < pR
+    p_lo, p_hi, rho_lo = np.where(lo, pL, pR), np.where(lo, pR, pL), np.where(lo, rhoL, rhoR)
+    F = np.sqrt(2.0) * (p_hi - p_lo) / np.sqrt(rho_lo * ((g + 1.0) * p_hi + (g - 1.0) * p_lo))
+    eps = rng.choice([0.0, 1e-16, -1e-16, 3e-16, -3e-16, 1e-13, -1e-13, 1e-10, -1e-10, 1e-6, -1e-6], n)
+    du = -F * (1.0 + eps)
+    du[eq] = rng.choice([0.0, -0.3, 0.3, -1e-12, 1e-12], int(eq.sum()))
+    uL = rng.normal(0.0, 0.5, n)
+    uR = uL + du
+    nrm = rng.normal(0.0, 1.0, (n, dim))
+    nrm[: n // 2, 1:] = 0.0  # axis-aligned: the projections carry u exactly
+    nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+    t = rng.normal(0.0, 0.3, (n, dim))
+    t -= (t * nrm).sum(axis=1, keepdims=True) * nrm  # a common tangential velocity
+    t[: n // 2] = 0.0
+
+    def state(rho, u, p):
+        v = u[:, None] * nrm + t
+        U = np.empty((n, dim + 2))
+        U[:, 0] = rho
+        U[:, 1:-1] = rho[:, None] * v
+        U[:, -1] = p / AIR.gm1 + 0.5 * rho * (v * v).sum(axis=1)
+        return U
+
+    Ui, Uj = state(rhoL, uL, pL), state(rhoR, uR, pR)
+    cij = nrm * np.exp(rng.uniform(-8, 0, n))[:, None]
+    d, bad = eval_dij(Ui, Uj, cij, -cij)
+    do, bo = O.eval_dij(Ui, Uj, cij, -cij)
+    assert not bo.any() and np.array_equal(bad, bo)
+    assert np.array_equal(d.view(np.int64), do.view(np.int64))
