@@ -89,7 +89,8 @@ constexpr int TPB = EF_TPB;  // state I/O, halo and pow kernels
 #define EF_MINB_LOW2 5
 #endif
 #ifndef EF_MINB_EDGE3
-#define EF_MINB_EDGE3 7  // straight-line d_ij: 72 registers (5: 3.00, 6: 2.90, 7: 2.63, 8: 2.69, 10: 2.97 ms on the 160^3 box)
+#define EF_MINB_EDGE3 6  // 80 registers, 20 bytes of spills (7: 72 registers, 80 bytes: +0.7% at base clocks, +1.4% on C5 320^3; before the
+                         // trimmed pows and lambda 7 was the best: 5: 3.00, 6: 2.90, 7: 2.63, 8: 2.69, 10: 2.97 ms on the 160^3 box)
 #endif
 #define EF_MINB_EDGE(D) ((D) == 3 ? EF_MINB_EDGE3 : EF_MINB_EDGE2)
 #ifndef EF_MINB_ROW3
